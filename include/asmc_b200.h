@@ -1,0 +1,228 @@
+/*
+ * asmc_b200.h -- C-ABI of the B200-native SAIS / SSMC sampler hot path.
+ *
+ * This is the drop-in boundary between the host side (the C++ mirror of the
+ * reference `asmc` API in paper_2408_12057_b200/csrc/host/, its pybind11
+ * module, bench.py) and the sm_100a CUDA kernels in libasmc_b200.so.  Plain C
+ * types only: pointers, sizes, PODs; host buffers in, host buffers out.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/).  The reference has no FFI of its
+ * own besides pybind11 (python/bindings.cpp), so the entry points are what
+ * those bindings call into:
+ *
+ *   asmc_run_smc          <- asmc::run_smc            include/asmc/engine.hpp:77-78, src/engine.cpp:97-188
+ *   asmc_run_sais_single  <- asmc::run_sais_single    include/asmc/drivers.hpp:84-86, src/drivers.cpp:72-182
+ *   asmc_run_rounds       <- asmc::run_ssmc/run_sais  include/asmc/drivers.hpp:48-55, src/drivers.cpp:186-232
+ *   asmc_sais_partials    <- the per-wave block fold of run_sais_single, src/drivers.cpp:113-146
+ *                            (one particle range per GPU; see asmc_fold_partials)
+ *   asmc_fold_partials    <- the ordered fold + report tail, src/drivers.cpp:137-176
+ *   asmc_systematic_resample <- asmc::systematic_resample  src/engine.cpp:61-80
+ *   asmc_ess              <- asmc::ess                src/engine.cpp:46-59
+ *   asmc_barrier_estimate <- asmc::barrier_estimate   src/schedule.cpp:41-56
+ *   asmc_generate_schedule<- asmc::generate_schedule  src/schedule.cpp:144-187
+ *   asmc_local_barrier    <- asmc::local_barrier      src/schedule.cpp:189-197
+ *   asmc_budget           <- asmc::budget             src/drivers.cpp:33-49
+ *   asmc_rng_*            <- asmc::rng::Stream        include/asmc/rng.hpp:41-105 (parity hooks)
+ *   asmc_trajectories     <- detail::weight_and_move  src/engine_detail.hpp:27-41 (parity hook:
+ *                            per-particle states after every step of a SAIS pass)
+ *
+ * Error convention: every function returns ASMC_OK (0) or one of the codes
+ * below; asmc_last_error() returns the thread-local message.  The host C++
+ * mirror rethrows the reference exception class with that message
+ * (include/asmc/errors.hpp:9-37, std::invalid_argument, std::domain_error).
+ * There is no CPU fallback: a target or kernel the device does not implement
+ * returns ASMC_ERR_CAPABILITY, a missing GPU returns ASMC_ERR_CUDA.
+ */
+#ifndef ASMC_B200_H
+#define ASMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ---- */
+#define ASMC_OK 0
+#define ASMC_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument            */
+#define ASMC_ERR_DOMAIN 2           /* std::domain_error                */
+#define ASMC_ERR_CAPABILITY 3       /* asmc::capability_error           */
+#define ASMC_ERR_DEGENERATE 4       /* asmc::degenerate_weights_error   */
+#define ASMC_ERR_EVALUATION 5       /* asmc::evaluation_error           */
+#define ASMC_ERR_CUDA 6             /* device missing / CUDA failure    */
+#define ASMC_ERR_INTERNAL 7
+
+/* ---- target plugins (include/asmc/target.hpp:54-96 + new plugins) ---- */
+#define ASMC_TARGET_GAUSSIAN_SHIFT 0 /* p = {mu0, mu1, sigma}                       target.cpp:57-113  */
+#define ASMC_TARGET_MIXTURE 1        /* p = {ref_sigma, weight, mu1, s1, mu2, s2}   target.cpp:115-157 */
+#define ASMC_TARGET_SCALE_GAUSSIAN 2 /* p = {sigma0, sigma1}: N(0,s0^2 I) -> N(0,s1^2 I), config 2 (new) */
+
+/* ---- forward kernels (include/asmc/kernel.hpp:11-27) ---- */
+#define ASMC_KERNEL_IDEALIZED 0
+#define ASMC_KERNEL_RWMH 1
+#define ASMC_KERNEL_IDENTITY 2
+#define ASMC_MAX_STEP_SIZES 16
+
+/* ---- resampling policies (include/asmc/engine.hpp:22) ---- */
+#define ASMC_POLICY_NEVER 0
+#define ASMC_POLICY_ALWAYS 1
+#define ASMC_POLICY_ADAPTIVE_ESS 2
+#define ASMC_POLICY_STABILIZED 3
+
+/* ---- driver modes (include/asmc/drivers.hpp:12) ---- */
+#define ASMC_MODE_SSMC 0
+#define ASMC_MODE_SAIS 1
+
+/* ---- execution options (new; the reference has one CPU path) ---- */
+#define ASMC_RNG_XOSHIRO 0 /* the reference's keyed xoshiro256++ streams, bit-identical words */
+#define ASMC_RNG_PHILOX 1  /* counter-based Philox4x32-10 (oracle/shadow/asmc/rng.hpp)       */
+#define ASMC_PREC_FP64 0   /* reference arithmetic: fp64 state, reference operation order   */
+#define ASMC_PREC_FP32 1   /* fp32 positions/densities, fp64 log-weights and accumulators   */
+
+typedef struct asmc_target_desc {
+  int32_t kind;
+  int32_t reserved;
+  uint64_t dim;
+  double p[8];
+} asmc_target_desc;
+
+typedef struct asmc_kernel_desc {
+  int32_t kind;
+  int32_t n_step_sizes;
+  int32_t sweeps;
+  int32_t reserved;
+  double step_sizes[ASMC_MAX_STEP_SIZES];
+} asmc_kernel_desc;
+
+typedef struct asmc_exec {
+  int32_t rng;       /* ASMC_RNG_*  */
+  int32_t precision; /* ASMC_PREC_* */
+  int32_t device;    /* CUDA ordinal */
+  int32_t lanes;     /* lanes per particle: 0 = auto, else 1/4/8/32 (fp32 + philox only) */
+} asmc_exec;
+
+/* LogAccumulator state (include/asmc/logsum.hpp:47-48 / :82-83). */
+typedef struct asmc_logacc {
+  double max;
+  double sum;
+} asmc_logacc;
+
+/* RunReport fields (include/asmc/engine.hpp:33-45).  Arrays are caller-owned,
+ * length T+1 (resample_times: capacity T); any of them may be NULL. */
+typedef struct asmc_report {
+  double* log_g0;
+  double* log_g1;
+  double* log_g2;
+  double* ess_trace; /* run_smc only; left untouched by SAIS (empty in the reference) */
+  double* cum_log_z;
+  uint8_t* resampled;
+  int32_t* resample_times;
+  int32_t n_resample_times;
+  int32_t reserved;
+  double log_z_hat;
+  double elbo_hat;
+  double wall_seconds;
+  uint64_t kernel_applications;
+} asmc_report;
+
+/* ---- library ---- */
+const char* asmc_last_error(void);
+int asmc_version(void);
+/* number of CUDA devices; 0 on a host without a GPU (never a CPU fallback) */
+int asmc_device_count(void);
+/* kernels launched on the calling thread since the last reset (bench accounting) */
+uint64_t asmc_launch_count(int reset);
+
+/* ---- samplers ---- */
+int asmc_run_smc(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                 const double* betas, int32_t steps, uint64_t n_particles, int32_t policy,
+                 double rho, uint64_t seed, uint64_t round, const asmc_exec* exec,
+                 asmc_report* out);
+
+int asmc_run_sais_single(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                         const double* betas, int32_t steps, uint64_t n_particles,
+                         uint64_t seed, uint64_t round, const asmc_exec* exec,
+                         asmc_report* out);
+
+/* Per-round outputs of asmc_run_rounds; arrays sized rounds (scalars) or
+ * rounds * (max_steps + 1) (per-step rows, row k = round k+1). */
+typedef struct asmc_rounds_out {
+  int32_t max_steps; /* row stride - 1; must be >= every round's T */
+  int32_t reserved;
+  uint64_t* n_particles;
+  int32_t* steps;
+  double* betas;
+  double* log_g0;
+  double* log_g1;
+  double* log_g2;
+  double* ess_trace; /* ssmc only */
+  double* cum_log_z;
+  uint8_t* resampled;
+  double* lambda; /* barrier knots Lambda_hat_t, schedule.cpp:41-56 */
+  double* log_z_hat;
+  double* elbo_hat;
+  double* wall_seconds;
+  uint64_t* kernel_applications;
+} asmc_rounds_out;
+
+int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                    int32_t mode, uint64_t n_particles, int32_t rounds, int32_t policy,
+                    double rho, uint64_t seed, uint64_t memory_cap_bytes,
+                    const asmc_exec* exec, asmc_rounds_out* out);
+
+/* Multi-GPU SAIS: partials of particles [p_begin, p_end) of an n_particles round.
+ * p_begin must be a multiple of ASMC_FOLD_CHUNK.  Writes per fold chunk
+ * (ASMC_FOLD_CHUNK particles) and per step t = 1..T the four accumulators
+ * g0, g1, g2, elbo as asmc_logacc:
+ *   partials[((c * (T + 1) + t) * 4 + a]   for c in [0, chunks(p_begin, p_end)).
+ * The chunk partial is a fixed tree over 256-particle blocks, so the fold of
+ * all chunks (in chunk order) is independent of how chunks map to GPUs. */
+#define ASMC_FOLD_CHUNK 262144
+uint64_t asmc_fold_chunks(uint64_t p_begin, uint64_t p_end);
+int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                       const double* betas, int32_t steps, uint64_t n_particles,
+                       uint64_t p_begin, uint64_t p_end, uint64_t seed, uint64_t round,
+                       const asmc_exec* exec, asmc_logacc* partials);
+/* Ordered fold of all chunk partials of a round (chunk order) and the report
+ * tail of run_sais_single (drivers.cpp:148-176). Host-side scalar code. */
+int asmc_fold_partials(const asmc_logacc* partials, uint64_t chunks, int32_t steps,
+                       uint64_t n_particles, asmc_report* out);
+
+/* ---- parity hooks ---- */
+/* key = {seed, round, particle, step, substep} (rng.hpp:11-17) */
+int asmc_rng_u64(int32_t rng, const uint64_t key[5], uint64_t count, uint64_t* out);
+int asmc_rng_uniform(int32_t rng, const uint64_t key[5], uint64_t count, double* out);
+/* normals computed in `precision` (fp64: double Box-Muller; fp32: device fp32 path) */
+int asmc_rng_normal(int32_t rng, int32_t precision, const uint64_t key[5], uint64_t count,
+                    double* out);
+
+/* States after every step of a SAIS pass for the listed particles:
+ * x_out[(i * (T + 1) + t) * dim + k], log_w_out[i * (T + 1) + t], t = 0 is the init draw. */
+int asmc_trajectories(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                      const double* betas, int32_t steps, uint64_t seed, uint64_t round,
+                      const uint64_t* particles, uint64_t count, const asmc_exec* exec,
+                      double* x_out, double* log_w_out);
+
+/* Systematic resampling on the device (engine.cpp:61-80) with the blocked,
+ * deterministic CDF described in DESIGN.md; u is the uniform the reference
+ * draws from key (seed, round, 0, t, resample). */
+int asmc_systematic_resample(const double* log_weights, uint64_t n, double u, int32_t device,
+                             uint32_t* ancestors);
+int asmc_ess(const double* log_weights, uint64_t n, int32_t device, double* out);
+
+/* ---- schedule adaptation (device kernels, bit-exact with the host oracle) ---- */
+int asmc_barrier_estimate(const double* log_g0, const double* log_g1, const double* log_g2,
+                          const double* betas, int32_t steps, int32_t device, double* lambda);
+int asmc_generate_schedule(const double* lambda, const double* beta, int32_t knots,
+                           int32_t t_new, int32_t device, double* betas_out);
+int asmc_local_barrier(const double* lambda, const double* beta, int32_t knots, int32_t device,
+                       double* out);
+int asmc_budget(uint64_t n_particles, int32_t steps, uint64_t dim, uint64_t memory_cap_bytes,
+                int32_t mode, uint64_t* n_out, int32_t* steps_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASMC_B200_H */
