@@ -1,0 +1,269 @@
+"""ctypes binding of the C-ABI in include/asmc_b200.h (libasmc_b200.so).
+
+This is the reference-facing drop-in boundary seen from Python: plain host
+arrays in, host arrays out, one call per sampler invocation.  Loading fails
+loudly when the native library is missing -- there is no CPU fallback.
+"""
+import ctypes as C
+import math
+import os
+
+import numpy as np
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libasmc_b200.so")
+
+_P = C.POINTER
+
+
+def _arr(a, ctype):
+    return a.ctypes.data_as(_P(ctype))
+
+
+class AsmcError(RuntimeError):
+    """Raised for a non-zero C-ABI return code; ``code`` is the ASMC_ERR_* value."""
+
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+        self.msg = msg
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"libasmc_b200.so not built at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        L.asmc_last_error.restype = C.c_char_p
+        L.asmc_launch_count.restype = C.c_uint64
+        L.asmc_launch_count.argtypes = [C.c_int]
+        L.asmc_fold_chunks.restype = C.c_uint64
+        L.asmc_fold_chunks.argtypes = [C.c_uint64, C.c_uint64]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise AsmcError(rc, lib().asmc_last_error().decode())
+
+
+def device_count():
+    return lib().asmc_device_count()
+
+
+def launch_count(reset=False):
+    return lib().asmc_launch_count(1 if reset else 0)
+
+
+def _report(T):
+    bufs = dict(log_g0=np.full(T + 1, -np.inf), log_g1=np.full(T + 1, -np.inf),
+                log_g2=np.full(T + 1, -np.inf), ess_trace=np.zeros(T + 1),
+                cum_log_z=np.zeros(T + 1), resampled=np.zeros(T + 1, np.uint8),
+                resample_times=np.zeros(T + 1, np.int32))
+    rep = abi.Report()
+    for k in ("log_g0", "log_g1", "log_g2", "ess_trace", "cum_log_z"):
+        setattr(rep, k, _arr(bufs[k], C.c_double))
+    rep.resampled = _arr(bufs["resampled"], C.c_uint8)
+    rep.resample_times = _arr(bufs["resample_times"], C.c_int32)
+    return rep, bufs
+
+
+def _finish(rep, bufs, smc):
+    out = dict(bufs)
+    if not smc:
+        out["ess_trace"] = np.zeros(0)
+    out["resample_times"] = list(bufs["resample_times"][: rep.n_resample_times])
+    out.update(log_z_hat=rep.log_z_hat, elbo_hat=rep.elbo_hat,
+               kernel_applications=rep.kernel_applications, wall_seconds=rep.wall_seconds)
+    return out
+
+
+def run_smc(target, kernel, betas, n, policy=abi.POLICY_ADAPTIVE_ESS, rho=0.5, seed=0, round=0,
+            exec_=None):
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    T = len(betas) - 1
+    rep, bufs = _report(T)
+    ex = exec_ or abi.execopts()
+    _check(lib().asmc_run_smc(C.byref(target), C.byref(kernel), _arr(betas, C.c_double),
+                              C.c_int32(T), C.c_uint64(n), C.c_int32(policy), C.c_double(rho),
+                              C.c_uint64(seed), C.c_uint64(round), C.byref(ex), C.byref(rep)))
+    return _finish(rep, bufs, True)
+
+
+def run_sais_single(target, kernel, betas, n, seed=0, round=0, exec_=None):
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    T = len(betas) - 1
+    rep, bufs = _report(T)
+    ex = exec_ or abi.execopts()
+    _check(lib().asmc_run_sais_single(C.byref(target), C.byref(kernel), _arr(betas, C.c_double),
+                                      C.c_int32(T), C.c_uint64(n), C.c_uint64(seed),
+                                      C.c_uint64(round), C.byref(ex), C.byref(rep)))
+    return _finish(rep, bufs, False)
+
+
+def plan_steps(rounds, n1, dim, memory_cap, mode):
+    ns, ts = [n1], [1]
+    for _ in range(1, rounds):
+        nn, tt = budget(ns[-1], ts[-1], dim, memory_cap, mode)
+        ns.append(nn)
+        ts.append(tt)
+    return ns, ts
+
+
+def run_rounds(target, kernel, mode, n, rounds, policy=abi.POLICY_ADAPTIVE_ESS, rho=0.5, seed=0,
+               memory_cap=4096 << 20, exec_=None):
+    _, ts = plan_steps(rounds, n, target.dim, memory_cap, mode)
+    max_steps = max(ts)
+    R, S = rounds, max_steps + 1
+    bufs = dict(n_particles=np.zeros(R, np.uint64), steps=np.zeros(R, np.int32),
+                betas=np.zeros((R, S)), log_g0=np.zeros((R, S)), log_g1=np.zeros((R, S)),
+                log_g2=np.zeros((R, S)), ess_trace=np.zeros((R, S)), cum_log_z=np.zeros((R, S)),
+                resampled=np.zeros((R, S), np.uint8), lambda_=np.zeros((R, S)),
+                log_z_hat=np.zeros(R), elbo_hat=np.zeros(R), wall_seconds=np.zeros(R),
+                kernel_applications=np.zeros(R, np.uint64))
+    out = abi.RoundsOut()
+    out.max_steps = max_steps
+    types = dict(n_particles=C.c_uint64, steps=C.c_int32, resampled=C.c_uint8,
+                 kernel_applications=C.c_uint64)
+    for k, v in bufs.items():
+        setattr(out, k, _arr(v, types.get(k, C.c_double)))
+    ex = exec_ or abi.execopts()
+    _check(lib().asmc_run_rounds(C.byref(target), C.byref(kernel), C.c_int32(mode), C.c_uint64(n),
+                                 C.c_int32(rounds), C.c_int32(policy), C.c_double(rho),
+                                 C.c_uint64(seed), C.c_uint64(memory_cap), C.byref(ex),
+                                 C.byref(out)))
+    return bufs
+
+
+def fold_chunks(p_begin, p_end):
+    return lib().asmc_fold_chunks(C.c_uint64(p_begin), C.c_uint64(p_end))
+
+
+def sais_partials(target, kernel, betas, n, p_begin, p_end, seed=0, round=0, exec_=None):
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    T = len(betas) - 1
+    nch = fold_chunks(p_begin, p_end)
+    out = np.zeros((max(nch, 1), T + 1, 4, 2))
+    ex = exec_ or abi.execopts(abi.RNG_PHILOX, abi.PREC_FP32)
+    _check(lib().asmc_sais_partials(C.byref(target), C.byref(kernel), _arr(betas, C.c_double),
+                                    C.c_int32(T), C.c_uint64(n), C.c_uint64(p_begin),
+                                    C.c_uint64(p_end), C.c_uint64(seed), C.c_uint64(round),
+                                    C.byref(ex), _arr(out, C.c_double)))
+    return out[:nch]
+
+
+def fold_partials(partials, n):
+    partials = np.ascontiguousarray(partials, dtype=np.float64)
+    chunks, T1 = partials.shape[0], partials.shape[1]
+    T = T1 - 1
+    rep, bufs = _report(T)
+    _check(lib().asmc_fold_partials(_arr(partials, C.c_double), C.c_uint64(chunks), C.c_int32(T),
+                                    C.c_uint64(n), C.byref(rep)))
+    return _finish(rep, bufs, False)
+
+
+def trajectories(target, kernel, betas, seed, round, particles, exec_=None):
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    T = len(betas) - 1
+    pids = np.ascontiguousarray(particles, dtype=np.uint64)
+    x = np.zeros((len(pids), T + 1, target.dim))
+    lw = np.zeros((len(pids), T + 1))
+    ex = exec_ or abi.execopts()
+    _check(lib().asmc_trajectories(C.byref(target), C.byref(kernel), _arr(betas, C.c_double),
+                                   C.c_int32(T), C.c_uint64(seed), C.c_uint64(round),
+                                   _arr(pids, C.c_uint64), C.c_uint64(len(pids)), C.byref(ex),
+                                   _arr(x, C.c_double), _arr(lw, C.c_double)))
+    return x, lw
+
+
+def _key(key):
+    return (C.c_uint64 * 5)(*[int(k) for k in key])
+
+
+def rng_u64(rng, key, count):
+    out = np.zeros(count, np.uint64)
+    _check(lib().asmc_rng_u64(C.c_int32(rng), _key(key), C.c_uint64(count), _arr(out, C.c_uint64)))
+    return out
+
+
+def rng_uniform(rng, key, count):
+    out = np.zeros(count)
+    _check(lib().asmc_rng_uniform(C.c_int32(rng), _key(key), C.c_uint64(count),
+                                  _arr(out, C.c_double)))
+    return out
+
+
+def rng_normal(rng, key, count, precision=abi.PREC_FP64):
+    out = np.zeros(count)
+    _check(lib().asmc_rng_normal(C.c_int32(rng), C.c_int32(precision), _key(key),
+                                 C.c_uint64(count), _arr(out, C.c_double)))
+    return out
+
+
+def systematic_resample(log_w, u, device=0):
+    lw = np.ascontiguousarray(log_w, dtype=np.float64)
+    out = np.zeros(len(lw), np.uint32)
+    _check(lib().asmc_systematic_resample(_arr(lw, C.c_double), C.c_uint64(len(lw)),
+                                          C.c_double(u), C.c_int32(device), _arr(out, C.c_uint32)))
+    return out
+
+
+def ess(log_w, device=0):
+    lw = np.ascontiguousarray(log_w, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().asmc_ess(_arr(lw, C.c_double), C.c_uint64(len(lw)), C.c_int32(device),
+                          C.byref(out)))
+    return out.value
+
+
+def barrier_estimate(g0, g1, g2, betas, device=0):
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    g = [np.ascontiguousarray(v, dtype=np.float64) for v in (g0, g1, g2)]
+    T = len(betas) - 1
+    lam = np.zeros(T + 1)
+    _check(lib().asmc_barrier_estimate(*[_arr(v, C.c_double) for v in g], _arr(betas, C.c_double),
+                                       C.c_int32(T), C.c_int32(device), _arr(lam, C.c_double)))
+    return lam
+
+
+def generate_schedule(lam, beta, t_new, device=0):
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    beta = np.ascontiguousarray(beta, dtype=np.float64)
+    out = np.zeros(t_new + 1)
+    _check(lib().asmc_generate_schedule(_arr(lam, C.c_double), _arr(beta, C.c_double),
+                                        C.c_int32(len(lam)), C.c_int32(t_new), C.c_int32(device),
+                                        _arr(out, C.c_double)))
+    return out
+
+
+def local_barrier(lam, beta, device=0):
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    beta = np.ascontiguousarray(beta, dtype=np.float64)
+    out = np.zeros(len(lam))
+    _check(lib().asmc_local_barrier(_arr(lam, C.c_double), _arr(beta, C.c_double),
+                                    C.c_int32(len(lam)), C.c_int32(device), _arr(out, C.c_double)))
+    return out
+
+
+def budget(n, steps, dim, cap, mode):
+    nn, tt = C.c_uint64(), C.c_int32()
+    _check(lib().asmc_budget(C.c_uint64(n), C.c_int32(steps), C.c_uint64(dim), C.c_uint64(cap),
+                             C.c_int32(mode), C.byref(nn), C.byref(tt)))
+    return nn.value, tt.value
+
+
+EXPORTED = [
+    "asmc_last_error", "asmc_version", "asmc_device_count", "asmc_launch_count", "asmc_run_smc",
+    "asmc_run_sais_single", "asmc_run_rounds", "asmc_fold_chunks", "asmc_sais_partials",
+    "asmc_fold_partials", "asmc_rng_u64", "asmc_rng_uniform", "asmc_rng_normal",
+    "asmc_trajectories", "asmc_systematic_resample", "asmc_ess", "asmc_barrier_estimate",
+    "asmc_generate_schedule", "asmc_local_barrier", "asmc_budget",
+]

@@ -1,0 +1,948 @@
+// C-ABI entry points (include/asmc_b200.h) and the host-side orchestration of
+// the device pipelines.  Host code here only validates, sizes buffers and
+// enqueues kernels; every sampler computation runs on the GPU.  There is no
+// CPU fallback: without a device every sampler entry returns ASMC_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "asmc_b200.h"
+#include "dispatch.h"
+#include "engine_kernels.h"
+
+using namespace asmcdev;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(expr)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(ASMC_ERR_CUDA, "CUDA error %s at %s:%d", cudaGetErrorString(e_),       \
+                  __FILE__, __LINE__);                                                   \
+  } while (0)
+#define TRY(expr)          \
+  do {                     \
+    int rc_ = (expr);      \
+    if (rc_) return rc_;   \
+  } while (0)
+#define LCH(expr)          \
+  do {                     \
+    ++g_launches;          \
+    CU(expr);              \
+  } while (0)
+
+struct DevCtx {
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+};
+
+int get_ctx(int device, DevCtx** out) {
+  static thread_local std::map<int, DevCtx> ctxs;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(ASMC_ERR_CUDA, "no CUDA device available (the sampler has no CPU fallback)");
+  }
+  if (device < 0 || device >= count) return fail(ASMC_ERR_CUDA, "invalid CUDA device %d", device);
+  CU(cudaSetDevice(device));
+  auto it = ctxs.find(device);
+  if (it == ctxs.end()) {
+    DevCtx c;
+    CU(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    CU(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, device));
+    it = ctxs.emplace(device, c).first;
+  }
+  *out = &it->second;
+  return 0;
+}
+
+// Stream-ordered device buffer (cudaMallocAsync pool).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  int alloc(size_t n, cudaStream_t st) {
+    s = st;
+    if (n == 0) n = 1;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st));
+    return 0;
+  }
+};
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// ---------------------------------------------------------------- checks --
+// Schedule::validate (src/engine.cpp:29-39)
+int check_schedule(const double* b, int T) {
+  if (!b || T < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "schedule needs at least one step");
+  if (b[0] != 0.0) return fail(ASMC_ERR_INVALID_ARGUMENT, "schedule must start at beta = 0");
+  if (b[T] != 1.0) return fail(ASMC_ERR_INVALID_ARGUMENT, "schedule must end at beta = 1");
+  for (int t = 1; t <= T; ++t)
+    if (!(b[t] > b[t - 1]))
+      return fail(ASMC_ERR_INVALID_ARGUMENT, "schedule must be strictly increasing at index %d", t);
+  return 0;
+}
+
+// validate_kernel (src/kernel.cpp:12-22)
+int check_kernel(const asmc_kernel_desc* k) {
+  if (!k) return fail(ASMC_ERR_INVALID_ARGUMENT, "null kernel descriptor");
+  if (k->kind == ASMC_KERNEL_RWMH) {
+    if (k->n_step_sizes < 1)
+      return fail(ASMC_ERR_INVALID_ARGUMENT, "rwmh_cycle requires at least one step size");
+    if (k->n_step_sizes > ASMC_MAX_STEP_SIZES)
+      return fail(ASMC_ERR_CAPABILITY, "at most %d rwmh step sizes are supported on the device",
+                  ASMC_MAX_STEP_SIZES);
+    for (int i = 0; i < k->n_step_sizes; ++i)
+      if (!(k->step_sizes[i] > 0.0))
+        return fail(ASMC_ERR_INVALID_ARGUMENT, "rwmh step sizes must be positive");
+    if (k->sweeps < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "rwmh sweeps must be at least 1");
+  } else if (k->kind != ASMC_KERNEL_IDEALIZED && k->kind != ASMC_KERNEL_IDENTITY) {
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown kernel kind");
+  }
+  return 0;
+}
+
+// constructor checks (src/target.cpp:57-63, 115-131; scale plugin)
+int check_target(const asmc_target_desc* t) {
+  if (!t) return fail(ASMC_ERR_INVALID_ARGUMENT, "null target descriptor");
+  const double* p = t->p;
+  switch (t->kind) {
+    case ASMC_TARGET_GAUSSIAN_SHIFT:
+      if (!(p[2] > 0.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "sigma must be positive");
+      break;
+    case ASMC_TARGET_MIXTURE:
+      if (!(p[0] > 0.0 && p[3] > 0.0 && p[5] > 0.0))
+        return fail(ASMC_ERR_INVALID_ARGUMENT, "mixture sigmas must be positive");
+      if (!(p[1] > 0.0 && p[1] < 1.0))
+        return fail(ASMC_ERR_INVALID_ARGUMENT, "mixture weight must lie strictly in (0, 1)");
+      break;
+    case ASMC_TARGET_SCALE_GAUSSIAN:
+      if (!(p[0] > 0.0 && p[1] > 0.0))
+        return fail(ASMC_ERR_INVALID_ARGUMENT, "scale sigmas must be positive");
+      break;
+    default:
+      return fail(ASMC_ERR_CAPABILITY, "target kind %d has no device implementation", t->kind);
+  }
+  if (t->dim == 0) return fail(ASMC_ERR_INVALID_ARGUMENT, "dim must be at least 1");
+  if (t->dim > 1024)
+    return fail(ASMC_ERR_CAPABILITY, "dim %llu exceeds the device kernels' limit of 1024",
+                (unsigned long long)t->dim);
+  return 0;
+}
+
+int check_pair(const asmc_target_desc* t, const asmc_kernel_desc* k) {
+  TRY(check_target(t));
+  TRY(check_kernel(k));
+  if (k->kind == ASMC_KERNEL_IDEALIZED && t->kind == ASMC_TARGET_MIXTURE)
+    return fail(ASMC_ERR_CAPABILITY, "idealized_exact kernel requires an exact sampler");
+  return 0;
+}
+
+// host-side constants with glibc, so the fp64 path sees the reference's bits
+TgtParams make_params(const asmc_target_desc* t) {
+  TgtParams P;
+  std::memset(&P, 0, sizeof P);
+  P.kind = t->kind;
+  P.dim = t->dim;
+  for (int i = 0; i < 8; ++i) P.p[i] = t->p[i];
+  const double* p = t->p;
+  switch (t->kind) {
+    case ASMC_TARGET_GAUSSIAN_SHIFT:
+      P.c[0] = std::log(p[2]);
+      P.c[1] = (p[1] - p[0]) / (p[2] * p[2]);
+      P.c[2] = 0.5 * (p[0] + p[1]);
+      P.c[3] = 1.0 / (p[2] * p[2]);
+      break;
+    case ASMC_TARGET_MIXTURE:
+      P.c[0] = std::log(p[0]);
+      P.c[1] = std::log(p[1]);
+      P.c[2] = std::log1p(-p[1]);
+      P.c[3] = std::log(p[3]);
+      P.c[4] = std::log(p[5]);
+      break;
+    case ASMC_TARGET_SCALE_GAUSSIAN:
+      P.c[0] = std::log(p[0]);
+      P.c[1] = std::log(p[1]);
+      P.c[2] = 1.0 / (p[0] * p[0]);
+      P.c[3] = 1.0 / (p[1] * p[1]);
+      P.c[4] = 0.5 * (P.c[2] - P.c[3]);
+      P.c[5] = P.c[1] - P.c[0];
+      break;
+  }
+  return P;
+}
+
+KernelCfg make_kcfg(const asmc_kernel_desc* k) {
+  KernelCfg c;
+  std::memset(&c, 0, sizeof c);
+  c.kind = k->kind;
+  c.n_steps = k->n_step_sizes;
+  c.sweeps = k->sweeps;
+  for (int i = 0; i < k->n_step_sizes && i < ASMC_MAX_STEP_SIZES; ++i) c.steps[i] = k->step_sizes[i];
+  if (c.kind != ASMC_KERNEL_RWMH) {
+    c.n_steps = 1;
+    c.sweeps = 1;
+  }
+  return c;
+}
+
+asmc_exec default_exec() {
+  asmc_exec e;
+  e.rng = ASMC_RNG_XOSHIRO;
+  e.precision = ASMC_PREC_FP64;
+  e.device = 0;
+  e.lanes = 0;
+  return e;
+}
+
+int choose_layout(const asmc_exec& ex, uint64_t d, Layout* L) {
+  if (ex.rng != ASMC_RNG_XOSHIRO && ex.rng != ASMC_RNG_PHILOX)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown rng %d", ex.rng);
+  if (ex.precision != ASMC_PREC_FP64 && ex.precision != ASMC_PREC_FP32)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown precision %d", ex.precision);
+  const bool seq_only = ex.precision == ASMC_PREC_FP64 || ex.rng == ASMC_RNG_XOSHIRO;
+  if (seq_only) {
+    if (ex.lanes > 1)
+      return fail(ASMC_ERR_CAPABILITY, "lanes > 1 needs rng = philox and precision = fp32");
+    *L = Layout{1, d <= 16 ? 16 : 1024};
+    return 0;
+  }
+  int lanes = ex.lanes;
+  if (lanes == 0) lanes = d <= 16 ? 1 : (d <= 128 ? 4 : 32);
+  if (lanes == 1) *L = Layout{1, d <= 16 ? 16 : 1024};
+  else if (lanes == 4 && d <= 128) *L = Layout{4, 32};
+  else if (lanes == 32 && d <= 1024) *L = Layout{32, 32};
+  else return fail(ASMC_ERR_CAPABILITY, "lanes %d not available for dim %llu", lanes, (unsigned long long)d);
+  return 0;
+}
+
+cudaError_t launch_pass(const asmc_exec& ex, Layout L, const PassArgs& A, uint64_t blocks,
+                        cudaStream_t s) {
+  if (blocks == 0) return cudaSuccess;
+  if (ex.precision == ASMC_PREC_FP64) return launch_pass_fp64(A.tg.kind, ex.rng, L, A, blocks, s);
+  return launch_pass_fp32(A.tg.kind, ex.rng, L, A, blocks, s);
+}
+
+PassArgs base_args(const asmc_target_desc* t, const asmc_kernel_desc* k) {
+  PassArgs A;
+  std::memset(&A, 0, sizeof A);
+  A.tg = make_params(t);
+  A.kc = make_kcfg(k);
+  return A;
+}
+
+uint64_t nblocks(uint64_t n) { return (n + kBlock - 1) / kBlock; }
+
+// Map the device error word / state to the reference's exception texts.
+int device_error(int code, int step, double val) {
+  switch (code) {
+    case 0: return 0;
+    case ASMC_ERR_DEGENERATE:
+      return fail(ASMC_ERR_DEGENERATE, "all log-weights are -inf at step %d", step);
+    case ASMC_ERR_DEGENERATE + 100:
+      return fail(ASMC_ERR_DEGENERATE, "weights degenerate at step %d (max log-weight %f)", step, val);
+    case ASMC_ERR_EVALUATION:
+      return fail(ASMC_ERR_EVALUATION, "incremental weight undefined: gamma_beta(x) = 0");
+    default:
+      return fail(code, "device error %d", code);
+  }
+}
+
+// Device buffers of one round's outputs.
+struct RoundBufs {
+  DBuf<double> g0, g1, g2, ess, cz, lam, scal;
+  DBuf<uint8_t> rs;
+  DBuf<int32_t> rt;
+  DBuf<SmcState> st;
+  DBuf<RoundDev> rd;
+  RoundDev host{};
+  int alloc(int T, cudaStream_t s) {
+    TRY(g0.alloc(T + 1, s));
+    TRY(g1.alloc(T + 1, s));
+    TRY(g2.alloc(T + 1, s));
+    TRY(ess.alloc(T + 1, s));
+    TRY(cz.alloc(T + 1, s));
+    TRY(lam.alloc(T + 1, s));
+    TRY(scal.alloc(2, s));
+    TRY(rs.alloc(T + 1, s));
+    TRY(rt.alloc(T + 1, s));
+    TRY(st.alloc(1, s));
+    TRY(rd.alloc(1, s));
+    CU(cudaMemsetAsync(st.p, 0, sizeof(SmcState), s));
+    host = RoundDev{g0.p, g1.p, g2.p, ess.p, cz.p, rs.p, rt.p, lam.p, scal.p, st.p};
+    CU(cudaMemcpyAsync(rd.p, &host, sizeof host, cudaMemcpyHostToDevice, s));
+    return 0;
+  }
+};
+
+// ---------------------------------------------------------------- SAIS --
+// One SAIS round over particles [0, n): fused pass + fold + report.
+struct SaisWork {
+  DBuf<LogAcc> part, chunk, tot;
+};
+
+int enqueue_sais_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs& base,
+                       const double* d_betas, int T, uint64_t n, uint64_t seed, uint64_t round,
+                       RoundDev* d_rd, int* d_err, SaisWork& W) {
+  const uint64_t nblk = nblocks(n);
+  const uint64_t nchunks = (nblk + kChunkBlocks - 1) / kChunkBlocks;
+  TRY(W.part.alloc((size_t)(T + 1) * kNAcc * nblk, C->stream));
+  TRY(W.chunk.alloc((size_t)(T + 1) * kNAcc * nchunks, C->stream));
+  TRY(W.tot.alloc((size_t)(T + 1) * kNAcc, C->stream));
+  PassArgs A = base;
+  A.betas = d_betas;
+  A.T = T;
+  A.t_begin = 1;
+  A.t_end = T;
+  A.mode = kModeSais;
+  A.row_base = 0;
+  A.n = n;
+  A.p_begin = 0;
+  A.n_local = n;
+  A.seed = seed;
+  A.round = round;
+  A.part = W.part.p;
+  A.part_stride = nblk;
+  A.err = d_err;
+  LCH(launch_pass(ex, L, A, nblk, C->stream));
+  LCH(launch_fold(ex.precision == ASMC_PREC_FP64, W.part.p, nblk, nblk, 1, T, 4, W.chunk.p, W.tot.p,
+                  C->stream));
+  LCH(launch_sais_report(W.tot.p, T, n, d_rd, C->stream));
+  return 0;
+}
+
+// ---------------------------------------------------------------- SSMC --
+struct SmcWork {
+  DBuf<char> xa, xb;
+  DBuf<void*> xbuf;
+  DBuf<int> xcur;
+  DBuf<double> lw, cum, btot;
+  DBuf<uint32_t> anc;
+  DBuf<LogAcc> part, chunk, tot;
+};
+
+int enqueue_smc_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs& base,
+                      const double* d_betas, int T, uint64_t n, int policy, double rho,
+                      uint64_t seed, uint64_t round, RoundDev* d_rd, SmcState* d_st, SmcWork& W) {
+  const uint64_t d = base.tg.dim;
+  const size_t real = ex.precision == ASMC_PREC_FP64 ? sizeof(double) : sizeof(float);
+  const uint64_t nblk = nblocks(n);
+  const uint64_t nchunks = (nblk + kChunkBlocks - 1) / kChunkBlocks;
+  TRY(W.xa.alloc(n * d * real, C->stream));
+  TRY(W.xb.alloc(n * d * real, C->stream));
+  TRY(W.xbuf.alloc(2, C->stream));
+  TRY(W.xcur.alloc(1, C->stream));
+  TRY(W.lw.alloc(n, C->stream));
+  TRY(W.cum.alloc(n, C->stream));
+  TRY(W.btot.alloc(nblk, C->stream));
+  TRY(W.anc.alloc(n, C->stream));
+  TRY(W.part.alloc((size_t)kNAcc * nblk, C->stream));
+  TRY(W.chunk.alloc((size_t)kNAcc * nchunks, C->stream));
+  TRY(W.tot.alloc(kNAcc, C->stream));
+  void* ptrs[2] = {W.xa.p, W.xb.p};
+  CU(cudaMemcpyAsync(W.xbuf.p, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemsetAsync(W.xcur.p, 0, sizeof(int), C->stream));
+
+  PassArgs A = base;
+  A.betas = d_betas;
+  A.T = T;
+  A.n = n;
+  A.p_begin = 0;
+  A.n_local = n;
+  A.seed = seed;
+  A.round = round;
+  A.xbuf = W.xbuf.p;
+  A.xcur = W.xcur.p;
+  A.lw = W.lw.p;
+  A.part = W.part.p;
+  A.part_stride = nblk;
+  A.err = &d_st->err;
+  A.mode = kModeSmcInit;  // engine_detail.hpp:91-100
+  LCH(launch_pass(ex, L, A, nblk, C->stream));
+  const bool exact = ex.precision == ASMC_PREC_FP64;
+  for (int t = 1; t <= T; ++t) {
+    A.mode = kModeSmcStep;
+    A.t_begin = A.t_end = t;
+    A.row_base = t;
+    LCH(launch_pass(ex, L, A, nblk, C->stream));
+    LCH(launch_fold(exact, W.part.p, nblk, nblk, 0, 1, kNAcc, W.chunk.p, W.tot.p, C->stream));
+    LCH(launch_smc_decide(W.tot.p, t, T, n, policy, rho, seed, round, ex.rng, d_rd, C->stream));
+    LCH(launch_resample(W.lw.p, n, d_st, W.cum.p, W.btot.p, W.anc.p, C->stream));
+    g_launches += 3;  // launch_resample issues four kernels
+    LCH(launch_gather(W.anc.p, n, d * real, W.xbuf.p, W.xcur.p, W.lw.p, d_st, C->sms, C->stream));
+    g_launches += 1;
+  }
+  return 0;
+}
+
+int copy_round(cudaStream_t s, RoundBufs& R, int T, bool smc, asmc_report* out, SmcState* st) {
+  std::vector<double> tmp(T + 1);
+  auto get = [&](const double* src, double* dst) -> int {
+    if (!dst) return 0;
+    CU(cudaMemcpyAsync(dst, src, sizeof(double) * (T + 1), cudaMemcpyDeviceToHost, s));
+    return 0;
+  };
+  TRY(get(R.g0.p, out->log_g0));
+  TRY(get(R.g1.p, out->log_g1));
+  TRY(get(R.g2.p, out->log_g2));
+  if (smc) TRY(get(R.ess.p, out->ess_trace));
+  TRY(get(R.cz.p, out->cum_log_z));
+  if (out->resampled)
+    CU(cudaMemcpyAsync(out->resampled, R.rs.p, T + 1, cudaMemcpyDeviceToHost, s));
+  double scal[2];
+  CU(cudaMemcpyAsync(scal, R.scal.p, sizeof scal, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(st, R.st.p, sizeof(SmcState), cudaMemcpyDeviceToHost, s));
+  std::vector<int32_t> rt(T + 1);
+  CU(cudaMemcpyAsync(rt.data(), R.rt.p, sizeof(int32_t) * (T + 1), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  out->log_z_hat = scal[0];
+  out->elbo_hat = scal[1];
+  if (smc) {
+    out->n_resample_times = st->n_resample;
+    if (out->resample_times)
+      for (int i = 0; i < st->n_resample; ++i) out->resample_times[i] = rt[i];
+  } else {
+    out->n_resample_times = 1;
+    if (out->resample_times) out->resample_times[0] = T;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* asmc_last_error(void) { return g_err.c_str(); }
+int asmc_version(void) { return 1; }
+int asmc_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+uint64_t asmc_launch_count(int reset) {
+  const uint64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+int asmc_run_sais_single(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                         const double* betas, int32_t T, uint64_t n, uint64_t seed,
+                         uint64_t round, const asmc_exec* exec, asmc_report* out) {
+  TRY(check_schedule(betas, T));
+  if (n < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "n_particles must be at least 1");
+  TRY(check_pair(target, kernel));
+  if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null report");
+  const asmc_exec ex = exec ? *exec : default_exec();
+  Layout L;
+  TRY(choose_layout(ex, target->dim, &L));
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C));
+  const double t0 = now_s();
+  DBuf<double> d_betas;
+  TRY(d_betas.alloc(T + 1, C->stream));
+  CU(cudaMemcpyAsync(d_betas.p, betas, sizeof(double) * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  RoundBufs R;
+  TRY(R.alloc(T, C->stream));
+  SaisWork W;
+  const PassArgs base = base_args(target, kernel);
+  TRY(enqueue_sais_round(C, ex, L, base, d_betas.p, T, n, seed, round, R.rd.p, &R.st.p->err, W));
+  SmcState st;
+  TRY(copy_round(C->stream, R, T, false, out, &st));
+  TRY(device_error(st.err, st.err_step, st.err_val));
+  out->kernel_applications = n * (uint64_t)T;
+  out->wall_seconds = now_s() - t0;
+  return 0;
+}
+
+int asmc_run_smc(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                 const double* betas, int32_t T, uint64_t n, int32_t policy, double rho,
+                 uint64_t seed, uint64_t round, const asmc_exec* exec, asmc_report* out) {
+  TRY(check_schedule(betas, T));
+  if (n < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "n_particles must be at least 1");
+  if (!(rho >= 0.0 && rho <= 1.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "rho must lie in [0, 1]");
+  if (policy < ASMC_POLICY_NEVER || policy > ASMC_POLICY_STABILIZED)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown resampling policy");
+  TRY(check_pair(target, kernel));
+  if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null report");
+  if (n > 0xffffffffull) return fail(ASMC_ERR_CAPABILITY, "ancestor indices are 32-bit");
+  const asmc_exec ex = exec ? *exec : default_exec();
+  Layout L;
+  TRY(choose_layout(ex, target->dim, &L));
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C));
+  const double t0 = now_s();
+  DBuf<double> d_betas;
+  TRY(d_betas.alloc(T + 1, C->stream));
+  CU(cudaMemcpyAsync(d_betas.p, betas, sizeof(double) * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  RoundBufs R;
+  TRY(R.alloc(T, C->stream));
+  SmcWork W;
+  const PassArgs base = base_args(target, kernel);
+  TRY(enqueue_smc_round(C, ex, L, base, d_betas.p, T, n, policy, rho, seed, round, R.rd.p, R.st.p, W));
+  SmcState st;
+  TRY(copy_round(C->stream, R, T, true, out, &st));
+  TRY(device_error(st.err, st.err_step, st.err_val));
+  out->kernel_applications = n * (uint64_t)T;
+  out->wall_seconds = now_s() - t0;
+  return 0;
+}
+
+int asmc_budget(uint64_t n, int32_t steps, uint64_t dim, uint64_t cap, int32_t mode,
+                uint64_t* n_out, int32_t* t_out) {
+  // drivers.cpp:33-49 (integer/double plumbing of the round loop)
+  if (n < 1 || steps < 1)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "budget needs n_particles and steps >= 1");
+  const double root2 = std::sqrt(2.0);
+  const uint64_t gn = (uint64_t)std::ceil(root2 * (double)n);
+  const int gt = (int)std::ceil(root2 * (double)steps);
+  if (mode == ASMC_MODE_SSMC) {
+    const double bytes = (double)gn * (double)dim * 8.0;
+    if (bytes > (double)cap) {
+      *n_out = n;
+      *t_out = 2 * steps;
+      return 0;
+    }
+  }
+  *n_out = gn;
+  *t_out = gt;
+  return 0;
+}
+
+int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kernel, int32_t mode,
+                    uint64_t n1, int32_t rounds, int32_t policy, double rho, uint64_t seed,
+                    uint64_t memory_cap, const asmc_exec* exec, asmc_rounds_out* out) {
+  // DriverOptions::validate (drivers.cpp:16-21)
+  if (n1 < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "n_particles must be at least 1");
+  if (rounds < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "rounds must be at least 1");
+  if (!(rho >= 0.0 && rho <= 1.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "rho must lie in [0, 1]");
+  if (mode != ASMC_MODE_SAIS && mode != ASMC_MODE_SSMC)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown driver mode");
+  TRY(check_pair(target, kernel));
+  if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null output");
+  const asmc_exec ex = exec ? *exec : default_exec();
+  Layout L;
+  TRY(choose_layout(ex, target->dim, &L));
+  // The (N_k, T_k) plan depends on the budget rule only, so the whole round
+  // loop is enqueued up front; only the betas are data-dependent (device).
+  std::vector<uint64_t> ns(rounds);
+  std::vector<int> ts(rounds);
+  ns[0] = n1;
+  ts[0] = 1;
+  for (int k = 1; k < rounds; ++k) TRY(asmc_budget(ns[k - 1], ts[k - 1], target->dim, memory_cap, mode, &ns[k], &ts[k]));
+  int tmax = 0;
+  for (int k = 0; k < rounds; ++k) tmax = ts[k] > tmax ? ts[k] : tmax;
+  if (tmax > out->max_steps) return fail(ASMC_ERR_INVALID_ARGUMENT, "max_steps too small (%d needed)", tmax);
+  if (mode == ASMC_MODE_SSMC)
+    for (int k = 0; k < rounds; ++k)
+      if (ns[k] > 0xffffffffull) return fail(ASMC_ERR_CAPABILITY, "ancestor indices are 32-bit");
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C));
+  const int stride = out->max_steps + 1;
+  std::vector<RoundBufs> R(rounds);
+  std::vector<DBuf<double>> betas(rounds);
+  DBuf<double> sched_scratch;
+  TRY(sched_scratch.alloc(5 * (size_t)(tmax + 1), C->stream));
+  for (int k = 0; k < rounds; ++k) {
+    TRY(R[k].alloc(ts[k], C->stream));
+    TRY(betas[k].alloc(ts[k] + 1, C->stream));
+  }
+  const double b01[2] = {0.0, 1.0};
+  CU(cudaMemcpyAsync(betas[0].p, b01, sizeof b01, cudaMemcpyHostToDevice, C->stream));
+  const PassArgs base = base_args(target, kernel);
+  DBuf<int> gerr;  // pass-kernel evaluation errors and schedule-generation failures
+  TRY(gerr.alloc(1, C->stream));
+  CU(cudaMemsetAsync(gerr.p, 0, sizeof(int), C->stream));
+  std::vector<cudaEvent_t> ev(rounds + 1);
+  for (auto& e : ev) CU(cudaEventCreate(&e));
+  CU(cudaEventRecord(ev[0], C->stream));
+  for (int k = 0; k < rounds; ++k) {
+    if (mode == ASMC_MODE_SAIS) {
+      SaisWork w;  // stream-ordered: freed after this round's kernels retire
+      TRY(enqueue_sais_round(C, ex, L, base, betas[k].p, ts[k], ns[k], seed, (uint64_t)(k + 1),
+                             R[k].rd.p, gerr.p, w));
+    } else {
+      SmcWork w;
+      TRY(enqueue_smc_round(C, ex, L, base, betas[k].p, ts[k], ns[k], policy, rho, seed,
+                            (uint64_t)(k + 1), R[k].rd.p, R[k].st.p, w));
+    }
+    if (k + 1 < rounds) {
+      LCH(launch_generate_schedule(R[k].lam.p, betas[k].p, ts[k] + 1, ts[k + 1], betas[k + 1].p,
+                                   sched_scratch.p, gerr.p, C->stream));
+    }
+    CU(cudaEventRecord(ev[k + 1], C->stream));
+  }
+  CU(cudaStreamSynchronize(C->stream));
+  int herr = 0;
+  CU(cudaMemcpy(&herr, gerr.p, sizeof(int), cudaMemcpyDeviceToHost));
+  int rc = 0;
+  for (int k = 0; k < rounds && !rc; ++k) {
+    const int T = ts[k];
+    std::vector<double> g0(T + 1), g1(T + 1), g2(T + 1), es(T + 1), cz(T + 1), b(T + 1);
+    std::vector<uint8_t> rs(T + 1);
+    std::vector<int32_t> rt(T + 1);
+    asmc_report rep{g0.data(), g1.data(), g2.data(), es.data(), cz.data(), rs.data(), rt.data(),
+                    0, 0, 0, 0, 0, 0};
+    SmcState st;
+    TRY(copy_round(C->stream, R[k], T, mode == ASMC_MODE_SSMC, &rep, &st));
+    TRY(device_error(st.err, st.err_step, st.err_val));
+    if (herr == ASMC_ERR_EVALUATION) return device_error(herr, 0, 0.0);
+    if (herr) return fail(herr, "schedule generation after round %d failed validation", k + 1);
+    std::vector<double> lam(T + 1);
+    CU(cudaMemcpy(lam.data(), R[k].lam.p, sizeof(double) * (T + 1), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(b.data(), betas[k].p, sizeof(double) * (T + 1), cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+    const size_t r0 = (size_t)k * stride;
+    if (out->n_particles) out->n_particles[k] = ns[k];
+    if (out->steps) out->steps[k] = T;
+    for (int t = 0; t <= T; ++t) {
+      if (out->betas) out->betas[r0 + t] = b[t];
+      if (out->log_g0) out->log_g0[r0 + t] = g0[t];
+      if (out->log_g1) out->log_g1[r0 + t] = g1[t];
+      if (out->log_g2) out->log_g2[r0 + t] = g2[t];
+      if (out->ess_trace && mode == ASMC_MODE_SSMC) out->ess_trace[r0 + t] = es[t];
+      if (out->cum_log_z) out->cum_log_z[r0 + t] = cz[t];
+      if (out->resampled) out->resampled[r0 + t] = rs[t];
+      if (out->lambda) out->lambda[r0 + t] = lam[t];
+    }
+    if (out->log_z_hat) out->log_z_hat[k] = rep.log_z_hat;
+    if (out->elbo_hat) out->elbo_hat[k] = rep.elbo_hat;
+    if (out->wall_seconds) out->wall_seconds[k] = ms * 1e-3;
+    if (out->kernel_applications) out->kernel_applications[k] = ns[k] * (uint64_t)T;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+uint64_t asmc_fold_chunks(uint64_t p_begin, uint64_t p_end) {
+  if (p_end <= p_begin) return 0;
+  return (p_end - p_begin + ASMC_FOLD_CHUNK - 1) / ASMC_FOLD_CHUNK;
+}
+
+int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                       const double* betas, int32_t T, uint64_t n, uint64_t p_begin, uint64_t p_end,
+                       uint64_t seed, uint64_t round, const asmc_exec* exec, asmc_logacc* partials) {
+  TRY(check_schedule(betas, T));
+  TRY(check_pair(target, kernel));
+  if (p_begin % ASMC_FOLD_CHUNK != 0)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "p_begin must be a multiple of ASMC_FOLD_CHUNK");
+  if (p_end > n || p_end < p_begin) return fail(ASMC_ERR_INVALID_ARGUMENT, "bad particle range");
+  const asmc_exec ex = exec ? *exec : default_exec();
+  if (ex.precision == ASMC_PREC_FP64)
+    return fail(ASMC_ERR_CAPABILITY, "sharded partials use the fp32 tree fold; fp64 reference order is single-GPU");
+  Layout L;
+  TRY(choose_layout(ex, target->dim, &L));
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C));
+  const uint64_t nloc = p_end - p_begin, nblk = nblocks(nloc);
+  const uint64_t nch = asmc_fold_chunks(p_begin, p_end);
+  if (nch == 0) return 0;
+  DBuf<double> d_betas;
+  TRY(d_betas.alloc(T + 1, C->stream));
+  CU(cudaMemcpyAsync(d_betas.p, betas, sizeof(double) * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  DBuf<LogAcc> part, chunk;
+  DBuf<int> err;
+  TRY(part.alloc((size_t)(T + 1) * kNAcc * nblk, C->stream));
+  TRY(chunk.alloc((size_t)(T + 1) * kNAcc * nch, C->stream));
+  TRY(err.alloc(1, C->stream));
+  CU(cudaMemsetAsync(err.p, 0, sizeof(int), C->stream));
+  PassArgs A = base_args(target, kernel);
+  A.betas = d_betas.p;
+  A.T = T;
+  A.t_begin = 1;
+  A.t_end = T;
+  A.mode = kModeSais;
+  A.n = n;
+  A.p_begin = p_begin;
+  A.n_local = nloc;
+  A.seed = seed;
+  A.round = round;
+  A.part = part.p;
+  A.part_stride = nblk;
+  A.err = err.p;
+  LCH(launch_pass(ex, L, A, nblk, C->stream));
+  LCH(launch_fold_chunks(part.p, nblk, nblk, 1, T, 4, nch, chunk.p, C->stream));
+  std::vector<LogAcc> h((size_t)(T + 1) * kNAcc * nch);
+  CU(cudaMemcpyAsync(h.data(), chunk.p, h.size() * sizeof(LogAcc), cudaMemcpyDeviceToHost, C->stream));
+  int herr = 0;
+  CU(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  TRY(device_error(herr, 0, 0.0));
+  for (uint64_t c = 0; c < nch; ++c)
+    for (int t = 0; t <= T; ++t)
+      for (int a = 0; a < 4; ++a) {
+        const LogAcc v = t == 0 ? LogAcc{-HUGE_VAL, 0.0} : h[((size_t)t * kNAcc + a) * nch + c];
+        partials[(c * (T + 1) + t) * 4 + a] = asmc_logacc{v.max, v.sum};
+      }
+  return 0;
+}
+
+int asmc_fold_partials(const asmc_logacc* partials, uint64_t chunks, int32_t T, uint64_t n,
+                       asmc_report* out) {
+  if (T < 1 || chunks == 0) return fail(ASMC_ERR_INVALID_ARGUMENT, "nothing to fold");
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  DevCtx* C;
+  TRY(get_ctx(dev, &C));
+  std::vector<LogAcc> h((size_t)(T + 1) * kNAcc * chunks, LogAcc{-HUGE_VAL, 0.0});
+  for (uint64_t c = 0; c < chunks; ++c)
+    for (int t = 1; t <= T; ++t)
+      for (int a = 0; a < 4; ++a) {
+        const asmc_logacc v = partials[(c * (T + 1) + t) * 4 + a];
+        h[((size_t)t * kNAcc + a) * chunks + c] = LogAcc{v.max, v.sum};
+      }
+  DBuf<LogAcc> chunk, tot;
+  TRY(chunk.alloc(h.size(), C->stream));
+  TRY(tot.alloc((size_t)(T + 1) * kNAcc, C->stream));
+  CU(cudaMemcpyAsync(chunk.p, h.data(), h.size() * sizeof(LogAcc), cudaMemcpyHostToDevice, C->stream));
+  RoundBufs R;
+  TRY(R.alloc(T, C->stream));
+  LCH(launch_fold_chunks_final(chunk.p, chunks, 1, T, 4, tot.p, C->stream));
+  LCH(launch_sais_report(tot.p, T, n, R.rd.p, C->stream));
+  SmcState st;
+  TRY(copy_round(C->stream, R, T, false, out, &st));
+  TRY(device_error(st.err, st.err_step, st.err_val));
+  out->kernel_applications = n * (uint64_t)T;
+  return 0;
+}
+
+int asmc_trajectories(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                      const double* betas, int32_t T, uint64_t seed, uint64_t round,
+                      const uint64_t* particles, uint64_t count, const asmc_exec* exec,
+                      double* x_out, double* log_w_out) {
+  TRY(check_schedule(betas, T));
+  TRY(check_pair(target, kernel));
+  const asmc_exec ex = exec ? *exec : default_exec();
+  Layout L;
+  TRY(choose_layout(ex, target->dim, &L));
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C));
+  const uint64_t d = target->dim;
+  DBuf<double> d_betas, rx, rl;
+  DBuf<uint64_t> pids;
+  DBuf<int> err;
+  TRY(d_betas.alloc(T + 1, C->stream));
+  TRY(rx.alloc(count * (T + 1) * d, C->stream));
+  TRY(rl.alloc(count * (T + 1), C->stream));
+  TRY(pids.alloc(count, C->stream));
+  TRY(err.alloc(1, C->stream));
+  CU(cudaMemsetAsync(err.p, 0, sizeof(int), C->stream));
+  CU(cudaMemcpyAsync(d_betas.p, betas, sizeof(double) * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemcpyAsync(pids.p, particles, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, C->stream));
+  PassArgs A = base_args(target, kernel);
+  A.betas = d_betas.p;
+  A.T = T;
+  A.t_begin = 1;
+  A.t_end = T;
+  A.mode = kModeTraj;
+  A.n_local = count;
+  A.seed = seed;
+  A.round = round;
+  A.pids = pids.p;
+  A.rec_x = rx.p;
+  A.rec_lw = rl.p;
+  A.err = err.p;
+  LCH(launch_pass(ex, L, A, nblocks(count), C->stream));
+  CU(cudaMemcpyAsync(x_out, rx.p, sizeof(double) * count * (T + 1) * d, cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaMemcpyAsync(log_w_out, rl.p, sizeof(double) * count * (T + 1), cudaMemcpyDeviceToHost, C->stream));
+  int herr = 0;
+  CU(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  return device_error(herr, 0, 0.0);
+}
+
+static int rng_common(int32_t rng, int what, int32_t prec, const uint64_t key[5], uint64_t count,
+                      void* out) {
+  if (rng != ASMC_RNG_XOSHIRO && rng != ASMC_RNG_PHILOX)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown rng %d", rng);
+  DevCtx* C;
+  TRY(get_ctx(0, &C));
+  DBuf<uint64_t> buf;
+  TRY(buf.alloc(count, C->stream));
+  LCH(launch_rng(rng, what, prec, key, count, buf.p, C->stream));
+  CU(cudaMemcpyAsync(out, buf.p, 8 * count, cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  return 0;
+}
+int asmc_rng_u64(int32_t rng, const uint64_t key[5], uint64_t count, uint64_t* out) {
+  return rng_common(rng, 0, ASMC_PREC_FP64, key, count, out);
+}
+int asmc_rng_uniform(int32_t rng, const uint64_t key[5], uint64_t count, double* out) {
+  return rng_common(rng, 1, ASMC_PREC_FP64, key, count, out);
+}
+int asmc_rng_normal(int32_t rng, int32_t precision, const uint64_t key[5], uint64_t count,
+                    double* out) {
+  return rng_common(rng, 2, precision, key, count, out);
+}
+
+int asmc_systematic_resample(const double* log_w, uint64_t n, double u, int32_t device,
+                             uint32_t* ancestors) {
+  if (n == 0) return fail(ASMC_ERR_INVALID_ARGUMENT, "cannot resample an empty system");
+  if (n > 0xffffffffull) return fail(ASMC_ERR_CAPABILITY, "ancestor indices are 32-bit");
+  DevCtx* C;
+  TRY(get_ctx(device, &C));
+  DBuf<double> lw, cum, btot;
+  DBuf<uint32_t> anc;
+  DBuf<SmcState> st;
+  TRY(lw.alloc(n, C->stream));
+  TRY(cum.alloc(n, C->stream));
+  TRY(btot.alloc(nblocks(n), C->stream));
+  TRY(anc.alloc(n, C->stream));
+  TRY(st.alloc(1, C->stream));
+  SmcState h;
+  std::memset(&h, 0, sizeof h);
+  h.resample_now = 1;
+  h.u = u;
+  CU(cudaMemcpyAsync(st.p, &h, sizeof h, cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemcpyAsync(lw.p, log_w, sizeof(double) * n, cudaMemcpyHostToDevice, C->stream));
+  LCH(launch_max(lw.p, n, st.p, C->stream));
+  LCH(launch_resample(lw.p, n, st.p, cum.p, btot.p, anc.p, C->stream));
+  CU(cudaMemcpyAsync(ancestors, anc.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaMemcpyAsync(&h, st.p, sizeof h, cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  if (h.err) return fail(ASMC_ERR_DEGENERATE, "all log-weights are -inf");
+  return 0;
+}
+
+int asmc_ess(const double* log_w, uint64_t n, int32_t device, double* out) {
+  if (n == 0) return fail(ASMC_ERR_INVALID_ARGUMENT, "ess of empty weight vector");
+  DevCtx* C;
+  TRY(get_ctx(device, &C));
+  DBuf<double> lw, r;
+  DBuf<int> err;
+  TRY(lw.alloc(n, C->stream));
+  TRY(r.alloc(1, C->stream));
+  TRY(err.alloc(1, C->stream));
+  CU(cudaMemsetAsync(err.p, 0, sizeof(int), C->stream));
+  CU(cudaMemcpyAsync(lw.p, log_w, sizeof(double) * n, cudaMemcpyHostToDevice, C->stream));
+  LCH(launch_ess(lw.p, n, r.p, err.p, C->stream));
+  int herr = 0;
+  CU(cudaMemcpyAsync(out, r.p, sizeof(double), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  if (herr) return fail(ASMC_ERR_DEGENERATE, "all log-weights are -inf");
+  return 0;
+}
+
+// schedule.cpp:121-141 messages, checked on the host before the device inversion
+static int check_barrier(const double* lambda, const double* beta, int n) {
+  if (n < 2) return fail(ASMC_ERR_INVALID_ARGUMENT, "barrier estimate needs at least two matched knots");
+  if (lambda[0] != 0.0) return fail(ASMC_ERR_INVALID_ARGUMENT, "barrier estimate must start at Lambda = 0");
+  if (beta[0] != 0.0 || beta[n - 1] != 1.0)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "barrier estimate must span beta in [0, 1]");
+  for (int i = 1; i < n; ++i) {
+    if (lambda[i] < lambda[i - 1]) return fail(ASMC_ERR_INVALID_ARGUMENT, "barrier knots must be nondecreasing");
+    if (!(beta[i] > beta[i - 1]))
+      return fail(ASMC_ERR_INVALID_ARGUMENT, "barrier beta knots must be strictly increasing");
+  }
+  return 0;
+}
+
+int asmc_barrier_estimate(const double* g0, const double* g1, const double* g2,
+                          const double* betas, int32_t T, int32_t device, double* lambda) {
+  TRY(check_schedule(betas, T));
+  for (int t = 1; t <= T; ++t)
+    if (g0[t] == -HUGE_VAL)
+      return fail(ASMC_ERR_INVALID_ARGUMENT, "no increment statistics recorded for step %d", t);
+  DevCtx* C;
+  TRY(get_ctx(device, &C));
+  DBuf<double> a, b, c, l;
+  DBuf<int> err;
+  TRY(a.alloc(T + 1, C->stream));
+  TRY(b.alloc(T + 1, C->stream));
+  TRY(c.alloc(T + 1, C->stream));
+  TRY(l.alloc(T + 1, C->stream));
+  TRY(err.alloc(1, C->stream));
+  CU(cudaMemsetAsync(err.p, 0, sizeof(int), C->stream));
+  CU(cudaMemcpyAsync(a.p, g0, 8 * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemcpyAsync(b.p, g1, 8 * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemcpyAsync(c.p, g2, 8 * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  LCH(launch_barrier(a.p, b.p, c.p, T, l.p, err.p, C->stream));
+  CU(cudaMemcpyAsync(lambda, l.p, 8 * (T + 1), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  return 0;
+}
+
+int asmc_generate_schedule(const double* lambda, const double* beta, int32_t knots, int32_t t_new,
+                           int32_t device, double* out) {
+  TRY(check_barrier(lambda, beta, knots));
+  if (t_new < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "schedule needs at least one step");
+  DevCtx* C;
+  TRY(get_ctx(device, &C));
+  DBuf<double> l, b, o, s;
+  DBuf<int> err;
+  TRY(l.alloc(knots, C->stream));
+  TRY(b.alloc(knots, C->stream));
+  TRY(o.alloc(t_new + 1, C->stream));
+  TRY(s.alloc(5 * (size_t)knots, C->stream));
+  TRY(err.alloc(1, C->stream));
+  CU(cudaMemsetAsync(err.p, 0, sizeof(int), C->stream));
+  CU(cudaMemcpyAsync(l.p, lambda, 8 * knots, cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemcpyAsync(b.p, beta, 8 * knots, cudaMemcpyHostToDevice, C->stream));
+  LCH(launch_generate_schedule(l.p, b.p, knots, t_new, o.p, s.p, err.p, C->stream));
+  int herr = 0;
+  CU(cudaMemcpyAsync(out, o.p, 8 * (t_new + 1), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  if (herr) return fail(herr, "generated schedule is not strictly increasing");
+  return 0;
+}
+
+int asmc_local_barrier(const double* lambda, const double* beta, int32_t knots, int32_t device,
+                       double* out) {
+  TRY(check_barrier(lambda, beta, knots));
+  DevCtx* C;
+  TRY(get_ctx(device, &C));
+  DBuf<double> l, b, o, s;
+  DBuf<int> err;
+  TRY(l.alloc(knots, C->stream));
+  TRY(b.alloc(knots, C->stream));
+  TRY(o.alloc(knots, C->stream));
+  TRY(s.alloc(3 * (size_t)knots, C->stream));
+  TRY(err.alloc(1, C->stream));
+  CU(cudaMemsetAsync(err.p, 0, sizeof(int), C->stream));
+  CU(cudaMemcpyAsync(l.p, lambda, 8 * knots, cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemcpyAsync(b.p, beta, 8 * knots, cudaMemcpyHostToDevice, C->stream));
+  LCH(launch_local_barrier(l.p, b.p, knots, o.p, s.p, err.p, C->stream));
+  int herr = 0;
+  CU(cudaMemcpyAsync(out, o.p, 8 * knots, cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  if (herr) return fail(herr, "interpolant abscissae must be strictly increasing");
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// Shared device definitions for the B200 SAIS/SSMC kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "asmc_b200.h"
+
+namespace asmcdev {
+
+constexpr int kBlock = 256;  // particles per reduction block (include/asmc/logsum.hpp:15)
+constexpr int kNAcc = 6;     // per-step accumulators: g0, g1, g2, elbo, sq(2 log w), top-2 max
+constexpr int kAccG0 = 0, kAccG1 = 1, kAccG2 = 2, kAccElbo = 3, kAccSq = 4, kAccTop2 = 5;
+constexpr int kChunkBlocks = ASMC_FOLD_CHUNK / kBlock;  // 1024 blocks per fold chunk
+
+struct LogAcc {
+  double max;
+  double sum;
+};
+
+__host__ __device__ __forceinline__ LogAcc lacc_empty() { return LogAcc{-__builtin_huge_val(), 0.0}; }
+
+// LogAccumulator::add (include/asmc/logsum.hpp:20-28)
+__device__ __forceinline__ void lacc_add(LogAcc& a, double l) {
+  if (l == -__builtin_huge_val()) return;
+  if (l <= a.max) {
+    a.sum += exp(l - a.max);
+  } else {
+    a.sum = a.sum * exp(a.max - l) + 1.0;
+    a.max = l;
+  }
+}
+
+// SignedLogAccumulator::add (logsum.hpp:55-63)
+__device__ __forceinline__ void sacc_add(LogAcc& a, double log_abs, double sign) {
+  if (log_abs == -__builtin_huge_val() || sign == 0.0) return;
+  if (log_abs <= a.max) {
+    a.sum += sign * exp(log_abs - a.max);
+  } else {
+    a.sum = a.sum * exp(a.max - log_abs) + sign;
+    a.max = log_abs;
+  }
+}
+
+// LogAccumulator::combine / SignedLogAccumulator::combine (logsum.hpp:30-38, 65-73).
+// Both branches give the same bits for combine(a,b) and combine(b,a), so the
+// xor-butterfly trees below leave every lane with the identical value.
+__device__ __forceinline__ void lacc_combine(LogAcc& a, const LogAcc& o) {
+  if (o.max == -__builtin_huge_val()) return;
+  if (o.max <= a.max) {
+    a.sum += o.sum * exp(o.max - a.max);
+  } else {
+    a.sum = a.sum * exp(a.max - o.max) + o.sum;
+    a.max = o.max;
+  }
+}
+
+// top-2 maxima as (max=m1, sum=m2); exact and order-free (engine_detail.hpp:130-154)
+__device__ __forceinline__ void top2_add(LogAcc& a, double v) {
+  if (v > a.max) {
+    a.sum = a.max;
+    a.max = v;
+  } else if (v > a.sum) {
+    a.sum = v;
+  }
+}
+__device__ __forceinline__ void top2_merge(LogAcc& a, const LogAcc& b) {
+  if (b.max > a.max) {
+    a.sum = fmax(a.max, b.sum);
+    a.max = b.max;
+  } else {
+    a.sum = fmax(a.sum, b.max);
+  }
+}
+
+__device__ __forceinline__ void acc_merge(int a, LogAcc& x, const LogAcc& y) {
+  if (a == kAccTop2) top2_merge(x, y);
+  else lacc_combine(x, y);
+}
+
+__device__ __forceinline__ LogAcc shfl_xor_acc(const LogAcc& v, int m, unsigned mask = 0xffffffffu) {
+  return LogAcc{__shfl_xor_sync(mask, v.max, m), __shfl_xor_sync(mask, v.sum, m)};
+}
+
+// Deterministic exp for x <= 0 from +,-,* only: identical bits to
+// oracle/restate.c:exp_det.  The __d*_rn intrinsics are never contracted into
+// FMA, so the result does not depend on -fmad.  Used for the resampling CDF so
+// the ancestor search is reproducible bit for bit on the host.
+__device__ __forceinline__ double exp_det(double x) {
+  if (x == -__builtin_huge_val() || x < -745.2) return 0.0;
+  const double kLn2Hi = 6.93147180369123816490e-01;
+  const double kLn2Lo = 1.90821492927058770002e-10;
+  const double kInvLn2 = 1.44269504088896338700e+00;
+  double kf = __dmul_rn(x, kInvLn2);
+  kf = kf < 0.0 ? (double)(long long)__dsub_rn(kf, 0.5) : (double)(long long)__dadd_rn(kf, 0.5);
+  const double r = __dsub_rn(__dsub_rn(x, __dmul_rn(kf, kLn2Hi)), __dmul_rn(kf, kLn2Lo));
+  const double c[13] = {1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0,
+                        1.0 / 40320.0,     1.0 / 5040.0,     1.0 / 720.0,     1.0 / 120.0,
+                        1.0 / 24.0,        1.0 / 6.0,        0.5,             1.0,
+                        1.0};
+  double p = 1.0 / 6227020800.0;
+#pragma unroll
+  for (int i = 0; i < 13; ++i) p = __dadd_rn(__dmul_rn(p, r), c[i]);
+  int k = (int)kf;
+  if (k < -1000) {
+    p = __dmul_rn(p, 0x1.0p-1000);
+    k += 1000;
+  }
+  const double s = __longlong_as_double((long long)(k + 1023) << 52);
+  return __dmul_rn(p, s);
+}
+
+// Error word: the first failing particle records its code (ASMC_ERR_*).
+__device__ __forceinline__ void raise_error(int* err, int code) {
+  if (err) atomicCAS(err, 0, code);
+}
+
+}  // namespace asmcdev

@@ -1,0 +1,59 @@
+// One (precision, target) slice of the particle-pass instantiations; the
+// Makefile compiles this file six times (-DASMC_PREC=64|32 -DASMC_TGT=0|1|2)
+// so the heavy template instantiations build in parallel.  The fp64 slices
+// are compiled with -fmad=false (reference operation order, no contraction).
+#include "dispatch.h"
+
+#ifndef ASMC_PREC
+#error "ASMC_PREC must be 64 or 32"
+#endif
+#ifndef ASMC_TGT
+#error "ASMC_TGT must be a target kind"
+#endif
+
+namespace asmcdev {
+
+#if ASMC_TGT == ASMC_TARGET_GAUSSIAN_SHIFT
+using Tgt = TgtGaussShift;
+#elif ASMC_TGT == ASMC_TARGET_MIXTURE
+using Tgt = TgtMixture;
+#elif ASMC_TGT == ASMC_TARGET_SCALE_GAUSSIAN
+using Tgt = TgtScale;
+#endif
+
+template <int RNG, typename Real, int G, int K>
+static cudaError_t go(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
+  pass_kernel<Tgt, RNG, Real, G, K><<<(unsigned)blocks, kBlock, 0, s>>>(A);
+  return cudaGetLastError();
+}
+
+#define CAT_(a, b, c) a##b##_##c
+#define CAT(a, b, c) CAT_(a, b, c)
+
+cudaError_t CAT(launch_pass_fp, ASMC_PREC, ASMC_TGT)(int rng, Layout L, const PassArgs& A,
+                                                     uint64_t blocks, cudaStream_t s) {
+#if ASMC_PREC == 64
+  if (L.lanes != 1) return cudaErrorInvalidValue;
+  if (rng == ASMC_RNG_XOSHIRO) {
+    if (L.kmax == 16) return go<ASMC_RNG_XOSHIRO, double, 1, 16>(A, blocks, s);
+    if (L.kmax == 1024) return go<ASMC_RNG_XOSHIRO, double, 1, 1024>(A, blocks, s);
+  } else {
+    if (L.kmax == 16) return go<ASMC_RNG_PHILOX, double, 1, 16>(A, blocks, s);
+    if (L.kmax == 1024) return go<ASMC_RNG_PHILOX, double, 1, 1024>(A, blocks, s);
+  }
+#else
+  if (rng == ASMC_RNG_XOSHIRO) {
+    if (L.lanes != 1) return cudaErrorInvalidValue;
+    if (L.kmax == 16) return go<ASMC_RNG_XOSHIRO, float, 1, 16>(A, blocks, s);
+    if (L.kmax == 1024) return go<ASMC_RNG_XOSHIRO, float, 1, 1024>(A, blocks, s);
+    return cudaErrorInvalidValue;
+  }
+  if (L.lanes == 1 && L.kmax == 16) return go<ASMC_RNG_PHILOX, float, 1, 16>(A, blocks, s);
+  if (L.lanes == 1 && L.kmax == 1024) return go<ASMC_RNG_PHILOX, float, 1, 1024>(A, blocks, s);
+  if (L.lanes == 4 && L.kmax == 32) return go<ASMC_RNG_PHILOX, float, 4, 32>(A, blocks, s);
+  if (L.lanes == 32 && L.kmax == 32) return go<ASMC_RNG_PHILOX, float, 32, 32>(A, blocks, s);
+#endif
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace asmcdev

@@ -1,0 +1,153 @@
+// Device target plugins: per-coordinate terms of the product-form annealing
+// families  log gamma_beta(x) = log eta(x) + beta V(x).
+//
+// Two arithmetic contracts per target:
+//  * fp64 "reference" terms (lr64, v64, draws) reproduce the reference's
+//    expressions operation for operation (src/target.cpp:16-19, 57-157 and the
+//    config-2 plugin in oracle/ref_harness.cpp).  Logs of parameters are
+//    precomputed on the host with glibc so they are the reference's bits.
+//  * fp32 "fast" terms: the MH log-ratio in difference form
+//    f_beta(x + h) - f_beta(x) (no cancellation of two large absolute log
+//    densities), and the potential's x-dependent part for the weight.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+namespace asmcdev {
+
+constexpr double kLogSqrt2Pi = 0.91893853320467274178;  // src/target.cpp:13
+
+struct TgtParams {
+  int kind;
+  int pad;
+  uint64_t dim;
+  double p[8];
+  double c[8];  // host-precomputed constants (see host make_params)
+};
+
+// target.cpp:16-19 with log(sigma) supplied
+__device__ __forceinline__ double lnpdf64(double x, double mu, double sigma, double log_sigma) {
+  const double s = (x - mu) / sigma;
+  return -0.5 * s * s - log_sigma - kLogSqrt2Pi;
+}
+
+// ------------------------------------------------- GaussianShiftTarget --
+// p = {mu0, mu1, sigma}; c = {log sigma, a, mid, 1/sigma^2}
+struct TgtGaussShift {
+  static constexpr bool kExact = true;
+  __device__ static double lr64(const TgtParams& T, double x) {
+    return lnpdf64(x, T.p[0], T.p[2], T.c[0]);
+  }
+  __device__ static double v64(const TgtParams& T, double x) { return T.c[1] * (x - T.c[2]); }
+  __device__ static double ref_draw(const TgtParams& T, double n) { return T.p[0] + T.p[2] * n; }
+  // target.cpp:107-113: mu computed once, then mu + sigma * normal
+  __device__ static double exact_mu(const TgtParams& T, double beta) {
+    return (1.0 - beta) * T.p[0] + beta * T.p[1];
+  }
+  __device__ static double exact_draw(const TgtParams& T, double mu, double n) {
+    return mu + T.p[2] * n;
+  }
+  // fp32 fast path ----------------------------------------------------
+  struct F32 {
+    float mu0, inv_s2, ba;  // ba = beta * a
+  };
+  __device__ static F32 f32(const TgtParams& T, double beta) {
+    return F32{(float)T.p[0], (float)T.c[3], (float)(beta * T.c[1])};
+  }
+  // f(x+h) - f(x) = h * (beta a - (x - mu0 + h/2) / sigma^2)
+  __device__ static float dlg(const F32& k, float x, float h) {
+    return h * (k.ba - (x - k.mu0 + 0.5f * h) * k.inv_s2);
+  }
+  __device__ static float vpart(const F32&, float x) { return x; }
+  // V = a * (sum x - d * mid)
+  __device__ static double v_from(const TgtParams& T, double s) {
+    return T.c[1] * (s - (double)T.dim * T.c[2]);
+  }
+};
+
+// ------------------------------------------------------ MixtureTarget --
+// p = {ref_sigma, w, mu1, s1, mu2, s2}; c = {log ref_sigma, log w, log1p(-w), log s1, log s2}
+struct TgtMixture {
+  static constexpr bool kExact = false;
+  __device__ static double lr64(const TgtParams& T, double x) {
+    return lnpdf64(x, 0.0, T.p[0], T.c[0]);
+  }
+  // target.cpp:139-152
+  __device__ static double v64(const TgtParams& T, double x) {
+    const double a = T.c[1] + lnpdf64(x, T.p[2], T.p[3], T.c[3]);
+    const double b = T.c[2] + lnpdf64(x, T.p[4], T.p[5], T.c[4]);
+    const double hi = a > b ? a : b;
+    const double lo = a > b ? b : a;
+    const double log_mix = hi + log1p(exp(lo - hi));
+    return log_mix - lnpdf64(x, 0.0, T.p[0], T.c[0]);
+  }
+  __device__ static double ref_draw(const TgtParams& T, double n) { return T.p[0] * n; }
+  __device__ static double exact_mu(const TgtParams&, double) { return 0.0; }
+  __device__ static double exact_draw(const TgtParams&, double, double n) { return n; }
+  // fp32 ----------------------------------------------------------------
+  struct F32 {
+    float beta, inv_r, lw1, mu1, inv_s1, lw2, mu2, inv_s2;
+  };
+  __device__ static F32 f32(const TgtParams& T, double beta) {
+    // log-normal constants folded: log N(x; mu, s) = -0.5((x-mu)/s)^2 - log s - c
+    return F32{(float)beta, (float)(1.0 / T.p[0]),
+               (float)(T.c[1] - T.c[3] + T.c[0]), (float)T.p[2], (float)(1.0 / T.p[3]),
+               (float)(T.c[2] - T.c[4] + T.c[0]), (float)T.p[4], (float)(1.0 / T.p[5])};
+  }
+  // log_mix(x) - log eta(x) with the common -log(sqrt(2 pi)) - log(ref_sigma) folded out
+  __device__ static float vterm(const F32& k, float x) {
+    const float s1 = (x - k.mu1) * k.inv_s1;
+    const float s2 = (x - k.mu2) * k.inv_s2;
+    const float a = k.lw1 - 0.5f * s1 * s1;
+    const float b = k.lw2 - 0.5f * s2 * s2;
+    const float hi = fmaxf(a, b), lo = fminf(a, b);
+    const float sr = x * k.inv_r;
+    return hi + log1pf(expf(lo - hi)) + 0.5f * sr * sr;
+  }
+  // f_beta(x) up to a beta-dependent constant: log eta + beta V
+  __device__ static float f(const F32& k, float x) {
+    const float sr = x * k.inv_r;
+    return -0.5f * sr * sr + k.beta * vterm(k, x);
+  }
+  __device__ static float dlg(const F32& k, float x, float h) { return f(k, x + h) - f(k, x); }
+  __device__ static float vpart(const F32& k, float x) { return vterm(k, x); }
+  __device__ static double v_from(const TgtParams&, double s) { return s; }
+};
+
+// ------------------------------------------------ ScaleGaussianTarget --
+// N(0, s0^2 I) -> N(0, s1^2 I).  p = {s0, s1};
+// c = {log s0, log s1, 1/s0^2, 1/s1^2, 0.5(1/s0^2 - 1/s1^2), log s1 - log s0}
+struct TgtScale {
+  static constexpr bool kExact = true;
+  __device__ static double lr64(const TgtParams& T, double x) {
+    return lnpdf64(x, 0.0, T.p[0], T.c[0]);
+  }
+  __device__ static double v64(const TgtParams& T, double x) {
+    return lnpdf64(x, 0.0, T.p[1], T.c[1]) - lnpdf64(x, 0.0, T.p[0], T.c[0]);
+  }
+  __device__ static double ref_draw(const TgtParams& T, double n) { return T.p[0] * n; }
+  // ref_harness.cpp ScaleGaussianTarget::exact_sample: sd = 1/sqrt(tau), x = sd * normal
+  __device__ static double exact_mu(const TgtParams& T, double beta) {
+    const double tau = (1.0 - beta) / (T.p[0] * T.p[0]) + beta / (T.p[1] * T.p[1]);
+    return 1.0 / sqrt(tau);
+  }
+  __device__ static double exact_draw(const TgtParams&, double sd, double n) { return sd * n; }
+  // fp32 ----------------------------------------------------------------
+  struct F32 {
+    float tau;
+  };
+  __device__ static F32 f32(const TgtParams& T, double beta) {
+    return F32{(float)((1.0 - beta) * T.c[2] + beta * T.c[3])};
+  }
+  // f(x+h) - f(x) = -tau h (x + h/2)
+  __device__ static float dlg(const F32& k, float x, float h) {
+    return -k.tau * h * (x + 0.5f * h);
+  }
+  __device__ static float vpart(const F32&, float x) { return x * x; }
+  __device__ static double v_from(const TgtParams& T, double s) {
+    return T.c[4] * s - (double)T.dim * T.c[5];
+  }
+};
+
+}  // namespace asmcdev
