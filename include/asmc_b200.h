@@ -100,7 +100,8 @@ typedef struct asmc_exec {
   int32_t rng;       /* ASMC_RNG_*  */
   int32_t precision; /* ASMC_PREC_* */
   int32_t device;    /* CUDA ordinal */
-  int32_t lanes;     /* lanes per particle: 0 = auto, else 1/4/8/32 (fp32 + philox only) */
+  int32_t lanes;     /* lanes per particle: 0 = auto, else 1/4/32 (fp32 + philox only) */
+  uint64_t stream;   /* cudaStream_t to enqueue on; 0 = the library's own stream */
 } asmc_exec;
 
 /* LogAccumulator state (include/asmc/logsum.hpp:47-48 / :82-83). */
@@ -221,6 +222,16 @@ int asmc_local_barrier(const double* lambda, const double* beta, int32_t knots, 
                        double* out);
 int asmc_budget(uint64_t n_particles, int32_t steps, uint64_t dim, uint64_t memory_cap_bytes,
                 int32_t mode, uint64_t* n_out, int32_t* steps_out);
+
+/* ---- measurement hooks (bench.py; not part of the reference interface) ---- */
+/* When enabled, every particle-pass launch on the calling thread is bracketed
+ * by CUDA events on its own stream; collect returns per-launch milliseconds
+ * and the algorithmic normal draws each launch had to make. */
+int asmc_profile_enable(int on);
+int asmc_profile_collect(double* ms, double* normals, int max_launches, int* n_launches);
+/* Generator peak: `blocks` CTAs x 256 threads each drawing quads_per_thread
+ * Philox quads (4 fp32 normals) in registers; returns kernel seconds. */
+int asmc_peak_normals(int32_t device, int32_t blocks, uint64_t quads_per_thread, double* seconds);
 
 #ifdef __cplusplus
 }

@@ -52,7 +52,7 @@ class KernelDesc(C.Structure):
 
 class Exec(C.Structure):
     _fields_ = [("rng", C.c_int32), ("precision", C.c_int32), ("device", C.c_int32),
-                ("lanes", C.c_int32)]
+                ("lanes", C.c_int32), ("stream", C.c_uint64)]
 
 
 class LogAcc(C.Structure):
@@ -111,7 +111,7 @@ def kernel(kind=KERNEL_IDEALIZED, step_sizes=(0.1, 1.0, 10.0), sweeps=1):
     return k
 
 
-def execopts(rng=RNG_XOSHIRO, precision=PREC_FP64, device=0, lanes=0):
+def execopts(rng=RNG_XOSHIRO, precision=PREC_FP64, device=0, lanes=0, stream=0):
     e = Exec()
-    e.rng, e.precision, e.device, e.lanes = rng, precision, device, lanes
+    e.rng, e.precision, e.device, e.lanes, e.stream = rng, precision, device, lanes, stream
     return e

@@ -260,10 +260,32 @@ def budget(n, steps, dim, cap, mode):
     return nn.value, tt.value
 
 
+def profile_enable(on=True):
+    _check(lib().asmc_profile_enable(C.c_int(1 if on else 0)))
+
+
+def profile_collect(max_launches=65536):
+    ms = np.zeros(max_launches)
+    nrm = np.zeros(max_launches)
+    cnt = C.c_int()
+    _check(lib().asmc_profile_collect(_arr(ms, C.c_double), _arr(nrm, C.c_double),
+                                      C.c_int(max_launches), C.byref(cnt)))
+    k = min(cnt.value, max_launches)
+    return ms[:k], nrm[:k]
+
+
+def peak_normals(device, blocks, quads_per_thread):
+    s = C.c_double()
+    _check(lib().asmc_peak_normals(C.c_int32(device), C.c_int32(blocks),
+                                   C.c_uint64(quads_per_thread), C.byref(s)))
+    return s.value
+
+
 EXPORTED = [
     "asmc_last_error", "asmc_version", "asmc_device_count", "asmc_launch_count", "asmc_run_smc",
     "asmc_run_sais_single", "asmc_run_rounds", "asmc_fold_chunks", "asmc_sais_partials",
     "asmc_fold_partials", "asmc_rng_u64", "asmc_rng_uniform", "asmc_rng_normal",
     "asmc_trajectories", "asmc_systematic_resample", "asmc_ess", "asmc_barrier_estimate",
-    "asmc_generate_schedule", "asmc_local_barrier", "asmc_budget",
+    "asmc_generate_schedule", "asmc_local_barrier", "asmc_budget", "asmc_profile_enable",
+    "asmc_profile_collect", "asmc_peak_normals",
 ]

@@ -57,7 +57,7 @@ struct DevCtx {
   int sms = 148;
 };
 
-int get_ctx(int device, DevCtx** out) {
+int get_ctx(int device, DevCtx** out, uint64_t user_stream = 0) {
   static thread_local std::map<int, DevCtx> ctxs;
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -72,6 +72,13 @@ int get_ctx(int device, DevCtx** out) {
     CU(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     CU(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, device));
     it = ctxs.emplace(device, c).first;
+  }
+  static thread_local DevCtx user;
+  if (user_stream) {
+    user = it->second;
+    user.stream = reinterpret_cast<cudaStream_t>(user_stream);
+    *out = &user;
+    return 0;
   }
   *out = &it->second;
   return 0;
@@ -153,8 +160,8 @@ int check_target(const asmc_target_desc* t) {
       return fail(ASMC_ERR_CAPABILITY, "target kind %d has no device implementation", t->kind);
   }
   if (t->dim == 0) return fail(ASMC_ERR_INVALID_ARGUMENT, "dim must be at least 1");
-  if (t->dim > 1024)
-    return fail(ASMC_ERR_CAPABILITY, "dim %llu exceeds the device kernels' limit of 1024",
+  if (t->dim > 16384)
+    return fail(ASMC_ERR_CAPABILITY, "dim %llu exceeds the device kernels' limit of 16384",
                 (unsigned long long)t->dim);
   return 0;
 }
@@ -221,10 +228,21 @@ asmc_exec default_exec() {
   e.precision = ASMC_PREC_FP64;
   e.device = 0;
   e.lanes = 0;
+  e.stream = 0;
   return e;
 }
 
-int choose_layout(const asmc_exec& ex, uint64_t d, Layout* L) {
+int check_smem(Layout L, uint64_t d, int rows, int nacc);
+
+int choose_layout_impl(const asmc_exec& ex, uint64_t d, Layout* L);
+
+// rows / nacc: per-launch step rows and accumulators, for the shared-memory budget
+int choose_layout(const asmc_exec& ex, uint64_t d, Layout* L, int rows = 1, int nacc = kNAcc) {
+  TRY(choose_layout_impl(ex, d, L));
+  return check_smem(*L, d, rows, nacc);
+}
+
+int choose_layout_impl(const asmc_exec& ex, uint64_t d, Layout* L) {
   if (ex.rng != ASMC_RNG_XOSHIRO && ex.rng != ASMC_RNG_PHILOX)
     return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown rng %d", ex.rng);
   if (ex.precision != ASMC_PREC_FP64 && ex.precision != ASMC_PREC_FP32)
@@ -233,23 +251,69 @@ int choose_layout(const asmc_exec& ex, uint64_t d, Layout* L) {
   if (seq_only) {
     if (ex.lanes > 1)
       return fail(ASMC_ERR_CAPABILITY, "lanes > 1 needs rng = philox and precision = fp32");
+    if (d > 1024)
+      return fail(ASMC_ERR_CAPABILITY,
+                  "dim %llu > 1024 needs rng = philox, precision = fp32 (shared-memory pass)",
+                  (unsigned long long)d);
     *L = Layout{1, d <= 16 ? 16 : 1024};
     return 0;
   }
   int lanes = ex.lanes;
   if (lanes == 0) lanes = d <= 16 ? 1 : (d <= 128 ? 4 : 32);
-  if (lanes == 1) *L = Layout{1, d <= 16 ? 16 : 1024};
-  else if (lanes == 4 && d <= 128) *L = Layout{4, 32};
-  else if (lanes == 32 && d <= 1024) *L = Layout{32, 32};
+  if (lanes == 1 && d <= 1024) *L = Layout{1, d <= 16 ? 16 : 1024};
+  else if (lanes == 4 || lanes == 32) *L = Layout{lanes, 0};  // shared-memory particle store
   else return fail(ASMC_ERR_CAPABILITY, "lanes %d not available for dim %llu", lanes, (unsigned long long)d);
   return 0;
+}
+
+// shared-memory budget of the many-lanes pass (x quads + per-warp step accumulators)
+int check_smem(Layout L, uint64_t d, int rows, int nacc) {
+  if (L.lanes == 1) return 0;
+  const size_t bytes = smem_pass_bytes(L.lanes, d, rows - 1, nacc);
+  if (bytes > 227 * 1024)
+    return fail(ASMC_ERR_CAPABILITY,
+                "pass needs %zu B of shared memory (dim %llu, %d steps); limit 227 KB", bytes,
+                (unsigned long long)d, rows);
+  return 0;
+}
+
+// Live per-launch timing of the particle pass (bench.py roofline): events on
+// the launching stream around each pass, plus its algorithmic normal draws.
+struct ProfRec {
+  cudaEvent_t a, b;
+  double normals;
+};
+thread_local bool g_prof = false;
+thread_local std::vector<ProfRec> g_prof_recs;
+
+double pass_normals(const PassArgs& A, uint64_t nparticles) {
+  const double d = (double)A.tg.dim;
+  double per_step = 0.0;
+  if (A.kc.kind == ASMC_KERNEL_RWMH) per_step = (double)A.kc.sweeps * A.kc.n_steps * d;
+  else if (A.kc.kind == ASMC_KERNEL_IDEALIZED) per_step = d;
+  const double steps = A.mode == kModeSmcInit ? 0.0 : (double)(A.t_end - A.t_begin + 1);
+  const double init = (A.mode == kModeSmcStep) ? 0.0 : d;
+  return (double)nparticles * (init + steps * per_step);
 }
 
 cudaError_t launch_pass(const asmc_exec& ex, Layout L, const PassArgs& A, uint64_t blocks,
                         cudaStream_t s) {
   if (blocks == 0) return cudaSuccess;
-  if (ex.precision == ASMC_PREC_FP64) return launch_pass_fp64(A.tg.kind, ex.rng, L, A, blocks, s);
-  return launch_pass_fp32(A.tg.kind, ex.rng, L, A, blocks, s);
+  ProfRec rec{};
+  if (g_prof) {
+    cudaEventCreate(&rec.a);
+    cudaEventCreate(&rec.b);
+    cudaEventRecord(rec.a, s);
+  }
+  const cudaError_t e = ex.precision == ASMC_PREC_FP64
+                            ? launch_pass_fp64(A.tg.kind, ex.rng, L, A, blocks, s)
+                            : launch_pass_fp32(A.tg.kind, ex.rng, L, A, blocks, s);
+  if (g_prof) {
+    cudaEventRecord(rec.b, s);
+    rec.normals = pass_normals(A, A.n_local);
+    g_prof_recs.push_back(rec);
+  }
+  return e;
 }
 
 PassArgs base_args(const asmc_target_desc* t, const asmc_kernel_desc* k) {
@@ -467,9 +531,9 @@ int asmc_run_sais_single(const asmc_target_desc* target, const asmc_kernel_desc*
   if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null report");
   const asmc_exec ex = exec ? *exec : default_exec();
   Layout L;
-  TRY(choose_layout(ex, target->dim, &L));
+  TRY(choose_layout(ex, target->dim, &L, T, 4));
   DevCtx* C;
-  TRY(get_ctx(ex.device, &C));
+  TRY(get_ctx(ex.device, &C, ex.stream));
   const double t0 = now_s();
   DBuf<double> d_betas;
   TRY(d_betas.alloc(T + 1, C->stream));
@@ -502,7 +566,7 @@ int asmc_run_smc(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
   Layout L;
   TRY(choose_layout(ex, target->dim, &L));
   DevCtx* C;
-  TRY(get_ctx(ex.device, &C));
+  TRY(get_ctx(ex.device, &C, ex.stream));
   const double t0 = now_s();
   DBuf<double> d_betas;
   TRY(d_betas.alloc(T + 1, C->stream));
@@ -554,7 +618,7 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
   if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null output");
   const asmc_exec ex = exec ? *exec : default_exec();
   Layout L;
-  TRY(choose_layout(ex, target->dim, &L));
+  TRY(choose_layout_impl(ex, target->dim, &L));
   // The (N_k, T_k) plan depends on the budget rule only, so the whole round
   // loop is enqueued up front; only the betas are data-dependent (device).
   std::vector<uint64_t> ns(rounds);
@@ -564,12 +628,13 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
   for (int k = 1; k < rounds; ++k) TRY(asmc_budget(ns[k - 1], ts[k - 1], target->dim, memory_cap, mode, &ns[k], &ts[k]));
   int tmax = 0;
   for (int k = 0; k < rounds; ++k) tmax = ts[k] > tmax ? ts[k] : tmax;
+  TRY(check_smem(L, target->dim, mode == ASMC_MODE_SAIS ? tmax : 1, mode == ASMC_MODE_SAIS ? 4 : kNAcc));
   if (tmax > out->max_steps) return fail(ASMC_ERR_INVALID_ARGUMENT, "max_steps too small (%d needed)", tmax);
   if (mode == ASMC_MODE_SSMC)
     for (int k = 0; k < rounds; ++k)
       if (ns[k] > 0xffffffffull) return fail(ASMC_ERR_CAPABILITY, "ancestor indices are 32-bit");
   DevCtx* C;
-  TRY(get_ctx(ex.device, &C));
+  TRY(get_ctx(ex.device, &C, ex.stream));
   const int stride = out->max_steps + 1;
   std::vector<RoundBufs> R(rounds);
   std::vector<DBuf<double>> betas(rounds);
@@ -664,9 +729,9 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
   if (ex.precision == ASMC_PREC_FP64)
     return fail(ASMC_ERR_CAPABILITY, "sharded partials use the fp32 tree fold; fp64 reference order is single-GPU");
   Layout L;
-  TRY(choose_layout(ex, target->dim, &L));
+  TRY(choose_layout(ex, target->dim, &L, T, 4));
   DevCtx* C;
-  TRY(get_ctx(ex.device, &C));
+  TRY(get_ctx(ex.device, &C, ex.stream));
   const uint64_t nloc = p_end - p_begin, nblk = nblocks(nloc);
   const uint64_t nch = asmc_fold_chunks(p_begin, p_end);
   if (nch == 0) return 0;
@@ -747,9 +812,9 @@ int asmc_trajectories(const asmc_target_desc* target, const asmc_kernel_desc* ke
   TRY(check_pair(target, kernel));
   const asmc_exec ex = exec ? *exec : default_exec();
   Layout L;
-  TRY(choose_layout(ex, target->dim, &L));
+  TRY(choose_layout(ex, target->dim, &L, T, 4));
   DevCtx* C;
-  TRY(get_ctx(ex.device, &C));
+  TRY(get_ctx(ex.device, &C, ex.stream));
   const uint64_t d = target->dim;
   DBuf<double> d_betas, rx, rl;
   DBuf<uint64_t> pids;
@@ -942,6 +1007,51 @@ int asmc_local_barrier(const double* lambda, const double* beta, int32_t knots, 
   CU(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
   CU(cudaStreamSynchronize(C->stream));
   if (herr) return fail(herr, "interpolant abscissae must be strictly increasing");
+  return 0;
+}
+
+int asmc_profile_enable(int on) {
+  g_prof = on != 0;
+  return 0;
+}
+
+int asmc_profile_collect(double* ms, double* normals, int max_launches, int* n_launches) {
+  int i = 0;
+  for (auto& r : g_prof_recs) {
+    CU(cudaEventSynchronize(r.b));
+    if (i < max_launches) {
+      float t = 0.f;
+      CU(cudaEventElapsedTime(&t, r.a, r.b));
+      if (ms) ms[i] = t;
+      if (normals) normals[i] = r.normals;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+    ++i;
+  }
+  if (n_launches) *n_launches = i;
+  g_prof_recs.clear();
+  return 0;
+}
+
+int asmc_peak_normals(int32_t device, int32_t blocks, uint64_t quads_per_thread, double* seconds) {
+  DevCtx* C;
+  TRY(get_ctx(device, &C));
+  DBuf<float> sink;
+  TRY(sink.alloc(1, C->stream));
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  LCH(launch_peak_normals(blocks, quads_per_thread / 8 + 1, sink.p, C->stream));  // warm-up
+  CU(cudaEventRecord(a, C->stream));
+  LCH(launch_peak_normals(blocks, quads_per_thread, sink.p, C->stream));
+  CU(cudaEventRecord(b, C->stream));
+  CU(cudaEventSynchronize(b));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, a, b));
+  *seconds = ms * 1e-3;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
   return 0;
 }
 

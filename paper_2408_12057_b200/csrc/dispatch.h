@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include "pass_kernel.cuh"
+#include "pass_smem.cuh"
 
 namespace asmcdev {
 

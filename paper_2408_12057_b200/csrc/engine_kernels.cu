@@ -660,3 +660,4 @@ cudaError_t launch_ess(const double* lw, uint64_t n, double* out, int* err, cuda
 }
 
 }  // namespace asmcdev
+

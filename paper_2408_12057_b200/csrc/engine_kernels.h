@@ -61,6 +61,7 @@ cudaError_t launch_barrier(const double* g0, const double* g1, const double* g2,
                            double* lambda, int* err, cudaStream_t s);
 cudaError_t launch_rng(int rng, int what, int precision, const uint64_t key[5], uint64_t count,
                        void* out, cudaStream_t s);
+cudaError_t launch_peak_normals(int blocks, uint64_t quads_per_thread, float* sink, cudaStream_t s);
 cudaError_t launch_ess(const double* lw, uint64_t n, double* out, int* err, cudaStream_t s);
 
 }  // namespace asmcdev

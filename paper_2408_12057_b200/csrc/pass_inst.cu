@@ -3,6 +3,7 @@
 // so the heavy template instantiations build in parallel.  The fp64 slices
 // are compiled with -fmad=false (reference operation order, no contraction).
 #include "dispatch.h"
+#include "pass_smem.cuh"
 
 #ifndef ASMC_PREC
 #error "ASMC_PREC must be 64 or 32"
@@ -27,6 +28,24 @@ static cudaError_t go(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+#if ASMC_PREC == 32
+template <int G>
+static cudaError_t go_smem(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
+  const int nacc = A.mode == kModeSmcStep ? kNAcc : 4;
+  const int rows = A.t_end - A.t_begin + 1 > 0 ? A.t_end - A.t_begin + 1 : 1;
+  const size_t bytes = smem_pass_bytes(G, A.tg.dim, rows - 1, nacc);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(pass_smem_kernel<Tgt, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  pass_smem_kernel<Tgt, G><<<(unsigned)blocks, kBlock, bytes, s>>>(A);
+  return cudaGetLastError();
+}
+#endif
+
 #define CAT_(a, b, c) a##b##_##c
 #define CAT(a, b, c) CAT_(a, b, c)
 
@@ -50,8 +69,8 @@ cudaError_t CAT(launch_pass_fp, ASMC_PREC, ASMC_TGT)(int rng, Layout L, const Pa
   }
   if (L.lanes == 1 && L.kmax == 16) return go<ASMC_RNG_PHILOX, float, 1, 16>(A, blocks, s);
   if (L.lanes == 1 && L.kmax == 1024) return go<ASMC_RNG_PHILOX, float, 1, 1024>(A, blocks, s);
-  if (L.lanes == 4 && L.kmax == 32) return go<ASMC_RNG_PHILOX, float, 4, 32>(A, blocks, s);
-  if (L.lanes == 32 && L.kmax == 32) return go<ASMC_RNG_PHILOX, float, 32, 32>(A, blocks, s);
+  if (L.lanes == 4) return go_smem<4>(A, blocks, s);
+  if (L.lanes == 32) return go_smem<32>(A, blocks, s);
 #endif
   return cudaErrorInvalidValue;
 }

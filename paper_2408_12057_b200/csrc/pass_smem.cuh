@@ -1,0 +1,309 @@
+// Fused particle pass, many-lanes-per-particle variant (fp32, Philox streams).
+//
+// G lanes (4 or 32) share one particle whose coordinates live in SHARED memory
+// as float4 quads (quad q of the particle sits at xq[q]; lane l owns quads
+// l, l+G, ...: consecutive lanes hit consecutive 16-byte words, so every
+// LDS.128/STS.128 is conflict-free).  Keeping x out of registers lets the quad
+// loop stay a real loop (small code, no I-cache thrash), keeps the register
+// count low (high occupancy), and lifts the dimension limit to the shared
+// memory budget instead of a compile-time register array.
+//
+// Reductions are per warp: after each (particle, step) a warp folds its groups'
+// (log w, lg) pairs with a fixed xor tree and lane 0 adds the result to the
+// warp's running accumulator for that step (shared memory).  Warps never wait
+// on each other inside the pass; the block partial is formed once at the end
+// by folding the 8 warp accumulators in warp order -- a fixed, GPU-count
+// independent tree.
+#pragma once
+
+#include "pass_kernel.cuh"
+
+namespace asmcdev {
+
+constexpr int kWarps = kBlock / 32;
+
+// dynamic shared memory: [groups][nquads] float4 (x), then [kWarps][T+1][nacc] LogAcc
+__host__ __device__ inline size_t smem_pass_bytes(int G, uint64_t d, int T, int nacc) {
+  const size_t nq = (size_t)((d + 3) / 4);
+  return (size_t)(kBlock / G) * nq * 16 + (size_t)kWarps * (T + 1) * nacc * sizeof(LogAcc);
+}
+
+template <class Tgt, int G>
+struct SmemOps {
+  // normals 4q .. 4q+3 of the draw set based at `base`
+  __device__ static void quad(const PhiloxKey& k, uint64_t base, int q, float z[4]) {
+    const uint64_t j0 = base + 4 * (uint64_t)q;
+    if ((base & 3) == 0) k.template normals4<float>((uint32_t)(j0 >> 2), z);
+    else k.template normals4_at<float>(j0, z);
+  }
+
+  __device__ static void init(const TgtParams& T, int lane, int d, float4* xq, const PhiloxKey& k) {
+    const int nq = (d + 3) >> 2;
+    for (int q = lane; q < nq; q += G) {
+      float z[4];
+      quad(k, 0, q, z);
+      float v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = (4 * q + e < d) ? (float)Tgt::ref_draw(T, (double)z[e]) : 0.f;
+      xq[q] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  }
+
+  __device__ static double weight(const TgtParams& T, int lane, int d, double b0, double b1,
+                                  const float4* xq) {
+    const typename Tgt::F32 kf = Tgt::f32(T, b1);
+    const int nq = (d + 3) >> 2;
+    float s = 0.f;
+    for (int q = lane; q < nq; q += G) {
+      const float4 x = xq[q];
+      const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e < d) s += Tgt::vpart(kf, xv[e]);
+    }
+    return (b1 - b0) * Tgt::v_from(T, group_sum<G>((double)s));
+  }
+
+  __device__ static void move(const TgtParams& T, const KernelCfg& kc, int lane, int d,
+                              double beta, float4* xq, const PhiloxKey& k) {
+    const int nq = (d + 3) >> 2;
+    if (kc.kind == ASMC_KERNEL_IDEALIZED) {
+      const double mu = Tgt::exact_mu(T, beta);
+      for (int q = lane; q < nq; q += G) {
+        float z[4];
+        quad(k, 0, q, z);
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (4 * q + e < d) ? (float)Tgt::exact_draw(T, mu, (double)z[e]) : 0.f;
+        xq[q] = make_float4(v[0], v[1], v[2], v[3]);
+      }
+      return;
+    }
+    if (kc.kind != ASMC_KERNEL_RWMH) return;
+    const typename Tgt::F32 kf = Tgt::f32(T, beta);
+    const int nprop = kc.sweeps * kc.n_steps;
+    double lu_pre = 0.0;  // lane l holds log u of proposal (q0 + l)
+    const int gbase = (int)(threadIdx.x & 31) & ~(G - 1);
+    // d % 4 == 0: every proposal's draw set starts on a Philox block, so the
+    // hot loops use the one-block path with no tail checks (one copy of the
+    // generator per loop: the loop body stays inside the L0 I-cache).
+    const bool aligned = (d & 3) == 0;
+    for (int p = 0; p < nprop; ++p) {
+      const float s = (float)kc.steps[p % kc.n_steps];
+      const uint64_t base = (uint64_t)p * (uint64_t)d;
+      if ((p % G) == 0) {
+        const int pp = p + lane;
+        lu_pre = pp < nprop ? log(k.uniform((uint32_t)pp)) : 0.0;
+      }
+      const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq)
+                               : delta_pass<false>(kf, k, lane, d, nq, base, s, xq);
+      const double delta = group_sum<G>((double)dl);
+      const double log_u = __shfl_sync(0xffffffffu, lu_pre, gbase + (p % G));
+      if (log_u < delta) {  // kernel.cpp:35: accept -> regenerate the proposal's normals
+        if (aligned) accept_pass<true>(k, lane, nq, base, s, xq);
+        else accept_pass<false>(k, lane, nq, base, s, xq);
+      }
+    }
+  }
+
+  // sum over this lane's quads of f_beta(x + s z) - f_beta(x)
+  template <bool kAligned>
+  __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane,
+                                     int d, int nq, uint64_t base, float s, const float4* xq) {
+    float dl = 0.f;
+#pragma unroll 1
+    for (int q = lane; q < nq; q += G) {
+      float z[4];
+      if (kAligned) k.template normals4<float>((uint32_t)(base >> 2) + (uint32_t)q, z);
+      else k.template normals4_at<float>(base + 4 * (uint64_t)q, z);
+      const float4 x = xq[q];
+      const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (kAligned || 4 * q + e < d) dl += Tgt::dlg(kf, xv[e], s * z[e]);
+    }
+    return dl;
+  }
+
+  template <bool kAligned>
+  __device__ static void accept_pass(const PhiloxKey& k, int lane, int nq, uint64_t base, float s,
+                                     float4* xq) {
+#pragma unroll 1
+    for (int q = lane; q < nq; q += G) {
+      float z[4];
+      if (kAligned) k.template normals4<float>((uint32_t)(base >> 2) + (uint32_t)q, z);
+      else k.template normals4_at<float>(base + 4 * (uint64_t)q, z);
+      float4 x = xq[q];
+      x.x += s * z[0];
+      x.y += s * z[1];
+      x.z += s * z[2];
+      x.w += s * z[3];
+      xq[q] = x;
+    }
+  }
+};
+
+// per-warp fold of this warp's groups for one (particle iteration, step), added
+// into the warp's running accumulators acc[a] (lane 0 holds the result)
+template <int G>
+__device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_post, bool active,
+                                          int nacc, LogAcc* acc) {
+  const int ln = threadIdx.x & 31;
+  if (G == 32) {
+    // one particle per warp: lane a owns accumulator a (no tree, no serial chain)
+    if (ln < nacc && active) {
+      LogAcc v = acc[ln];
+      switch (ln) {
+        case kAccG0: lacc_add(v, lw_pre); break;
+        case kAccG1: lacc_add(v, lw_pre + lg); break;
+        case kAccG2: lacc_add(v, lw_pre + 2.0 * lg); break;
+        case kAccElbo:
+          if (lg != 0.0) sacc_add(v, lw_pre + log(fabs(lg)), lg > 0.0 ? 1.0 : -1.0);
+          break;
+        case kAccSq: lacc_add(v, 2.0 * lw_post); break;
+        default: top2_add(v, lw_post); break;
+      }
+      acc[ln] = v;
+    }
+    return;
+  }
+  const bool leader = (ln % G) == 0;
+  for (int a = 0; a < nacc; ++a) {
+    LogAcc v = (a == kAccTop2) ? LogAcc{-__builtin_huge_val(), -__builtin_huge_val()} : lacc_empty();
+    if (leader && active) {
+      switch (a) {
+        case kAccG0: lacc_add(v, lw_pre); break;
+        case kAccG1: lacc_add(v, lw_pre + lg); break;
+        case kAccG2: lacc_add(v, lw_pre + 2.0 * lg); break;
+        case kAccElbo:
+          if (lg != 0.0) sacc_add(v, lw_pre + log(fabs(lg)), lg > 0.0 ? 1.0 : -1.0);
+          break;
+        case kAccSq: lacc_add(v, 2.0 * lw_post); break;
+        default: top2_add(v, lw_post); break;
+      }
+    }
+#pragma unroll
+    for (int m = G; m < 32; m <<= 1) {
+      const LogAcc o = shfl_xor_acc(v, m);
+      if (a == kAccTop2) top2_merge(v, o);
+      else lacc_combine(v, o);
+    }
+    if (ln == 0) acc_merge(a, acc[a], v);
+  }
+}
+
+template <class Tgt, int G>
+__global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant__ PassArgs A) {
+  constexpr int NG = kBlock / G;
+  const int tid = threadIdx.x, g = tid / G, lane = tid % G, warp = tid >> 5;
+  const int d = (int)A.tg.dim;
+  const int nq = (d + 3) >> 2;
+  const uint64_t blk = blockIdx.x;
+  const int nacc = (A.mode == kModeSmcStep) ? kNAcc : 4;
+  if (A.err && *(volatile int*)A.err) return;
+
+  extern __shared__ __align__(16) unsigned char smem[];
+  float4* xq = reinterpret_cast<float4*>(smem) + (size_t)g * nq;
+  LogAcc* wacc = reinterpret_cast<LogAcc*>(smem + (size_t)NG * nq * 16);
+  const int rows = A.t_end - A.t_begin + 1;
+  LogAcc* myacc = wacc + (size_t)warp * rows * nacc;  // [row][a] of this warp
+  if ((tid & 31) == 0)
+    for (int i = 0; i < rows * nacc; ++i)
+      myacc[i] = (i % nacc == kAccTop2) ? LogAcc{-__builtin_huge_val(), -__builtin_huge_val()}
+                                         : lacc_empty();
+  using Ops = SmemOps<Tgt, G>;
+
+  for (int r = 0; r < G; ++r) {
+    const uint64_t local = blk * kBlock + (uint64_t)r * NG + g;
+    const bool active = local < A.n_local;
+    const uint64_t pid = A.mode == kModeTraj ? (active ? A.pids[local] : 0) : A.p_begin + local;
+    double lw = 0.0;
+    if (A.mode == kModeSmcStep) {
+      const float4* src = reinterpret_cast<const float4*>(
+          reinterpret_cast<const float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d);
+      const bool vec = (d & 3) == 0;
+      for (int q = lane; q < nq; q += G) {
+        if (!active) {
+          xq[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else if (vec) {
+          xq[q] = src[q];
+        } else {
+          const float* s = reinterpret_cast<const float*>(src);
+          float v[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[e] = 4 * q + e < d ? s[4 * q + e] : 0.f;
+          xq[q] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+      }
+      lw = active ? A.lw[local] : 0.0;
+    } else {
+      PhiloxKey k;
+      k.init(A.seed, A.round, pid, 0, 0);
+      Ops::init(A.tg, lane, d, xq, k);
+    }
+    __syncwarp();
+    if (A.mode == kModeSmcInit) {
+      if (active) {
+        float* dst = reinterpret_cast<float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d;
+        for (int q = lane; q < nq; q += G) {
+          const float4 x = xq[q];
+          const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * q + e < d) dst[4 * q + e] = xv[e];
+        }
+        if (lane == 0) A.lw[local] = 0.0;
+      }
+      __syncwarp();
+      continue;
+    }
+    if (A.mode == kModeTraj && active) {
+      double* rx = A.rec_x + (local * (uint64_t)(A.T + 1)) * d;
+      for (int i = lane; i < d; i += G) rx[i] = (double)reinterpret_cast<const float*>(xq)[i];
+      if (lane == 0) A.rec_lw[local * (uint64_t)(A.T + 1)] = 0.0;
+    }
+    for (int t = A.t_begin; t <= A.t_end; ++t) {
+      const double b0 = A.betas[t - 1], b1 = A.betas[t];
+      const double lg = Ops::weight(A.tg, lane, d, b0, b1, xq);
+      PhiloxKey k;
+      k.init(A.seed, A.round, pid, (uint64_t)t, 1);
+      __syncwarp();
+      Ops::move(A.tg, A.kc, lane, d, b1, xq, k);
+      __syncwarp();
+      const double pre = lw;
+      lw += lg;
+      if (A.mode == kModeTraj) {
+        if (active) {
+          double* rx = A.rec_x + (local * (uint64_t)(A.T + 1) + t) * d;
+          for (int i = lane; i < d; i += G) rx[i] = (double)reinterpret_cast<const float*>(xq)[i];
+          if (lane == 0) A.rec_lw[local * (uint64_t)(A.T + 1) + t] = lw;
+        }
+        continue;
+      }
+      warp_fold<G>(pre, lg, lw, active, nacc, myacc + (size_t)(t - A.t_begin) * nacc);
+    }
+    if (A.mode == kModeSmcStep && active) {
+      float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(A.xbuf[*A.xcur]) +
+                                              local * (uint64_t)d);
+      if ((d & 3) == 0) {
+        for (int q = lane; q < nq; q += G) dst[q] = xq[q];
+      } else {
+        float* df = reinterpret_cast<float*>(dst);
+        for (int i = lane; i < d; i += G) df[i] = reinterpret_cast<const float*>(xq)[i];
+      }
+      if (lane == 0) A.lw[local] = lw;
+    }
+    __syncwarp();
+  }
+  if (A.mode == kModeTraj || A.mode == kModeSmcInit) return;
+  __syncthreads();
+  // block partial = warps folded in order (fixed tree)
+  for (int i = tid; i < rows * nacc; i += blockDim.x) {
+    const int row = i / nacc, a = i % nacc;
+    LogAcc acc = wacc[(size_t)row * nacc + a];
+    for (int w = 1; w < kWarps; ++w) acc_merge(a, acc, wacc[((size_t)w * rows + row) * nacc + a]);
+    A.part[((size_t)(A.t_begin + row - A.row_base) * kNAcc + a) * A.part_stride + blk] = acc;
+  }
+}
+
+}  // namespace asmcdev

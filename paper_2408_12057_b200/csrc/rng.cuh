@@ -79,36 +79,86 @@ struct XoStream {
 };
 
 // ----------------------------------------------------------------- philox --
+// 32x32 -> 64 multiply as one IMAD.WIDE.U32; hi/lo are the register pair halves.
+__device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t& lo, uint32_t& hi) {
+  uint64_t p;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(p));
+}
+
 __device__ __forceinline__ uint4 philox10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
-    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
-    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k0, (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ k1,
-                   (uint32_t)p0);
+    uint32_t lo0, hi0, lo1, hi1;
+    mulwide(0xD2511F53u, c.x, lo0, hi0);
+    mulwide(0xCD9E8D57u, c.z, lo1, hi1);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
   return c;
 }
 
-// Box-Muller pair in fp32 from two 32-bit words, matching the double formula
-// of the shadow stream (u1 = (a+1) 2^-32, u2 = b 2^-32) to fp32 accuracy:
-// log(u1) is taken of the exactly-rounded head plus a first-order tail so
-// u1 -> 1 keeps full relative accuracy (plain (float)u1 would not).
+// ln(s) for normal s in [2^-32, 1]: Cephes-style logf without the special
+// cases the library logf carries (denormals, 0, inf, NaN cannot occur here).
+// s = 2^e m, m in [sqrt(1/2), sqrt(2)), log1p(m - 1) by a degree-8 polynomial.
+__device__ __forceinline__ float log_unit(float s) {
+  const int i = __float_as_int(s);
+  const int e = (i - 0x3f3504f3) >> 23;
+  const float m = __int_as_float(i - (e << 23));
+  const float t = m - 1.0f;
+  const float z = t * t;
+  float y = 7.0376836292E-2f;
+  y = fmaf(y, t, -1.1514610310E-1f);
+  y = fmaf(y, t, 1.1676998740E-1f);
+  y = fmaf(y, t, -1.2420140846E-1f);
+  y = fmaf(y, t, 1.4249322787E-1f);
+  y = fmaf(y, t, -1.6668057665E-1f);
+  y = fmaf(y, t, 2.0000714765E-1f);
+  y = fmaf(y, t, -2.4999993993E-1f);
+  y = fmaf(y, t, 3.3333331174E-1f);
+  y = (y * t) * z;
+  const float ef = (float)e;
+  y = fmaf(ef, -2.12194440e-4f, y);
+  y = fmaf(-0.5f, z, y);
+  return fmaf(ef, 0.693359375f, t + y);
+}
+
+// Box-Muller pair in fp32 from two 32-bit words -- the shadow stream's
+// u1 = (a+1) 2^-32, u2 = b 2^-32, r = sqrt(-2 ln u1), angle 2 pi u2
+// (oracle/shadow/asmc/rng.hpp) to fp32 accuracy:
+//  * ln u1 of the exactly rounded head plus a first-order tail, so u1 -> 1
+//    keeps full relative accuracy;
+//  * the angle's quadrant comes from the top two bits of b, the remaining 30
+//    bits give phi in [-pi/4, pi/4) where short sin/cos polynomials are exact
+//    to an ulp; the quadrant rotation is two selects and two sign flips, and
+//    the 1/sqrt(2) of the rotation is folded into r = sqrt(-ln u1) * sqrt(2)/sqrt(2).
 __device__ __forceinline__ void bm_pair_f32(uint32_t a, uint32_t b, float& n_cos, float& n_sin) {
   const float fa = __uint2float_rz(a);
   const uint32_t resid = a - __float2uint_rz(fa);          // 0..255, exact
   const float A = fa * 0x1.0p-32f;                          // exact
   const float E = __uint2float_rn(resid + 1u) * 0x1.0p-32f; // exact
   const float s = A + E;
-  const float corr = E - (s - A);                           // Fast2Sum tail
-  const float lnu = logf(s) + __fdividef(corr, s);
-  const float r = sqrtf(-2.0f * lnu);
-  float sn, cs;
-  sincospif(__uint2float_rn(b) * 0x1.0p-31f, &sn, &cs);
-  n_cos = r * cs;
-  n_sin = r * sn;
+  const float corr = E - (s - A);                           // Fast2Sum tail of u1
+  const float lnu = log_unit(s) + fmaf(-s, corr, 2.0f * corr);  // ~ ln s + corr / s
+  const float v = -lnu;
+  const float rk = v * rsqrtf(fmaxf(v, 1e-30f));           // sqrt(-ln u1) = r / sqrt(2)
+  const float phi = fmaf(__uint2float_rn(b & 0x3FFFFFFFu), 1.46291807926715968e-09f,
+                         -0.785398163397448310f);          // (pi/2)(f 2^-30 - 1/2)
+  const float z = phi * phi;
+  const float sp = fmaf(fmaf(-1.9515295891E-4f, z, 8.3321608736E-3f), z, -1.6666654611E-1f);
+  const float sn = fmaf(sp * z, phi, phi);
+  const float cp = fmaf(fmaf(2.443315711809948E-5f, z, -1.388731625493765E-3f), z,
+                        4.166664568298827E-2f);
+  const float cs = fmaf(cp * z, z, fmaf(-0.5f, z, 1.0f));
+  // angle = pi/4 + q pi/2 + phi, q = b >> 30
+  const float ap = cs + sn, bm = cs - sn;
+  const bool odd = (b >> 30) & 1u;
+  const float sv = odd ? bm : ap, cv = odd ? ap : bm;
+  const uint32_t ssgn = b & 0x80000000u;
+  const uint32_t csgn = (b ^ (b << 1)) & 0x80000000u;
+  n_sin = __int_as_float(__float_as_int(rk) ^ ssgn) * sv;
+  n_cos = __int_as_float(__float_as_int(rk) ^ csgn) * cv;
 }
 
 __device__ __forceinline__ void bm_pair_f64(uint32_t a, uint32_t b, double& n_cos, double& n_sin) {
