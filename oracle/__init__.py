@@ -80,7 +80,7 @@ class Oracle:
     @staticmethod
     def _finish(rep, bufs):
         out = dict(bufs)
-        out["resample_times"] = list(bufs["resample_times"][: rep.n_resample_times])
+        out["resample_times"] = [int(v) for v in bufs["resample_times"][: rep.n_resample_times]]
         out.update(log_z_hat=rep.log_z_hat, elbo_hat=rep.elbo_hat,
                    kernel_applications=rep.kernel_applications, wall_seconds=rep.wall_seconds)
         return out
