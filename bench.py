@@ -123,7 +123,7 @@ def cpu_reference_run(n1, dim, rounds, workers):
 
 def cpu_sample_n1(budget_s, dim, rounds, workers):
     """Largest power-of-two N_1 whose 4-round run fits ~budget_s of wall time."""
-    n1 = 256
+    n1 = 1024
     ka, dt = cpu_reference_run(n1, dim, rounds, workers)
     rate = ka / dt
     per_n1 = psteps(1 << 20, rounds, dim) / float(1 << 20)
@@ -180,7 +180,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n1", type=int, default=N1_PER_GPU, help="round-1 particles per GPU")
     ap.add_argument("--dim", type=int, default=D)
-    ap.add_argument("--cpu-budget", type=float, default=6.0, help="seconds per CPU sample")
+    ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds per CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -294,7 +294,7 @@ def main():
                     "d2h_bytes_per_step": d2h,
                     "path": "C-ABI asmc_run_rounds (run_sais) with host outputs, per step"},
             "roofline": {
-                "bound": "issue", "kernel": "pass_kernel<TgtScale, philox, float, 32, 32>",
+                "bound": "issue", "kernel": "pass_smem_kernel<TgtScale, 32> (fused init+weight+RWMH pass)",
                 "achieved": achieved / 1e9, "peak": peak_normals / 1e9, "unit": "Gnormal/s",
                 "frac": achieved / peak_normals,
                 "peak_source": "asmc_peak_normals: same Philox4x32-10 + fp32 Box-Muller, registers only, measured live",
