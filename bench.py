@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--dim", type=int, default=D)
     ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds per CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU chunk-partial round loop even at one rank")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -204,7 +206,7 @@ def main():
     total_psteps = psteps(n1, ROUNDS, args.dim)
 
     def one_step():
-        if world == 1:
+        if world == 1 and not args.sharded:
             return capi.run_rounds(tg, kern, abi.MODE_SAIS, n1, ROUNDS, seed=SEED, exec_=ex)
         return distributed.run_sais(tg, kern, n1, ROUNDS, SEED, ex, rank, world)
 

@@ -168,3 +168,21 @@ def test_ssmc_fp32_lanes_close_to_reference(lanes):
                      seed=5, round=1, exec_=abi.execopts(PH, F32, lanes=lanes))
     assert a["resample_times"] == b["resample_times"]
     assert abs(a["log_z_hat"] - b["log_z_hat"]) < 0.02
+
+
+def test_sharded_round_loop_matches_device_round_loop():
+    """distributed.run_sais (chunk partials + fold + device schedule, the multi-GPU
+    path) at one rank reproduces asmc_run_rounds bit for bit."""
+    from paper_2408_12057_b200 import distributed
+    tg = abi.scale_gaussian(1.0, 2.0, 200)
+    k = abi.kernel(abi.KERNEL_RWMH)
+    ex = abi.execopts(PH, F32)
+    n1 = abi.FOLD_CHUNK + 999
+    a = capi.run_rounds(tg, k, abi.MODE_SAIS, n1, 3, seed=6, exec_=ex)
+    b = distributed.run_sais(tg, k, n1, 3, 6, ex, 0, 1)
+    for r in range(3):
+        T = int(a["steps"][r])
+        assert b["steps"][r] == T and b["n_particles"][r] == int(a["n_particles"][r])
+        assert np.array_equal(np.asarray(b["betas"][r]), a["betas"][r][: T + 1])
+        assert np.array_equal(np.asarray(b["log_g1"][r]), a["log_g1"][r][: T + 1])
+        assert b["log_z_hat"][r] == a["log_z_hat"][r]
