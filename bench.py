@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--dim", type=int, default=D)
     ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds per CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-target measurement")
+    ap.add_argument("--ttt-seeds", type=int, default=1000)
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU chunk-partial round loop even at one rank")
     args = ap.parse_args()
@@ -314,6 +316,13 @@ def main():
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if world == 1 and not args.no_ttt:
+            try:
+                sys.path.insert(0, os.path.join(ROOT, "tools"))
+                import time_to_target
+                line["time_to_target"] = time_to_target.measure(n_seeds=args.ttt_seeds)
+            except Exception as exc:  # reported, never required
+                line["time_to_target"] = {"unavailable": str(exc)}
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -13,7 +13,7 @@ import numpy as np
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libasmc_b200.so")
+LIB_PATH = os.environ.get("ASMC_B200_LIB", os.path.join(HERE, "libasmc_b200.so"))
 
 _P = C.POINTER
 

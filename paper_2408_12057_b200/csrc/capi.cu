@@ -71,6 +71,12 @@ int get_ctx(int device, DevCtx** out, uint64_t user_stream = 0) {
     DevCtx c;
     CU(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     CU(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, device));
+    // keep freed stream-ordered allocations reserved: every round re-allocates
+    // its partial buffers, which must not go back to the OS at each sync
+    cudaMemPool_t pool;
+    CU(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = ~0ull;
+    CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     it = ctxs.emplace(device, c).first;
   }
   static thread_local DevCtx user;
@@ -269,7 +275,7 @@ int choose_layout_impl(const asmc_exec& ex, uint64_t d, Layout* L) {
 // shared-memory budget of the many-lanes pass (x quads + per-warp step accumulators)
 int check_smem(Layout L, uint64_t d, int rows, int nacc) {
   if (L.lanes == 1) return 0;
-  const size_t bytes = smem_pass_bytes(L.lanes, d, rows - 1, nacc);
+  const size_t bytes = smem_pass_bytes(L.lanes, d, rows - 1, nacc, 2);  // conservative: cached-v targets
   if (bytes > 227 * 1024)
     return fail(ASMC_ERR_CAPABILITY,
                 "pass needs %zu B of shared memory (dim %llu, %d steps); limit 227 KB", bytes,

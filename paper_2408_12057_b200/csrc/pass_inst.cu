@@ -33,7 +33,7 @@ template <int G>
 static cudaError_t go_smem(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
   const int nacc = A.mode == kModeSmcStep ? kNAcc : 4;
   const int rows = A.t_end - A.t_begin + 1 > 0 ? A.t_end - A.t_begin + 1 : 1;
-  const size_t bytes = smem_pass_bytes(G, A.tg.dim, rows - 1, nacc);
+  const size_t bytes = smem_pass_bytes(G, A.tg.dim, rows - 1, nacc, CacheWords<Tgt>::value);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(pass_smem_kernel<Tgt, G>,

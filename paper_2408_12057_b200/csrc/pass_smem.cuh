@@ -22,19 +22,41 @@ namespace asmcdev {
 
 constexpr int kWarps = kBlock / 32;
 
-// dynamic shared memory: [groups][nquads] float4 (x), then [kWarps][T+1][nacc] LogAcc
-__host__ __device__ inline size_t smem_pass_bytes(int G, uint64_t d, int T, int nacc) {
+// dynamic shared memory: [groups][words][nquads] float4 (x, and vterm(x) for targets
+// that cache it), then [kWarps][T+1][nacc] LogAcc
+__host__ __device__ inline size_t smem_pass_bytes(int G, uint64_t d, int T, int nacc, int words = 1) {
   const size_t nq = (size_t)((d + 3) / 4);
-  return (size_t)(kBlock / G) * nq * 16 + (size_t)kWarps * (T + 1) * nacc * sizeof(LogAcc);
+  return (size_t)(kBlock / G) * nq * 16 * words + (size_t)kWarps * (T + 1) * nacc * sizeof(LogAcc);
 }
+
+template <class Tgt>
+struct CacheWords {
+  static constexpr int value = Tgt::kCacheV ? 2 : 1;
+};
 
 template <class Tgt, int G>
 struct SmemOps {
+  static constexpr bool kCache = Tgt::kCacheV;
+
   // normals 4q .. 4q+3 of the draw set based at `base`
   __device__ static void quad(const PhiloxKey& k, uint64_t base, int q, float z[4]) {
     const uint64_t j0 = base + 4 * (uint64_t)q;
     if ((base & 3) == 0) k.template normals4<float>((uint32_t)(j0 >> 2), z);
     else k.template normals4_at<float>(j0, z);
+  }
+
+  __device__ static float4 vquad(const typename Tgt::F32& kf, float4 x) {
+    return make_float4(Tgt::vpart(kf, x.x), Tgt::vpart(kf, x.y), Tgt::vpart(kf, x.z),
+                       Tgt::vpart(kf, x.w));
+  }
+
+  // vq[q] = vterm(x) for the cached-potential targets (after a load or a redraw)
+  __device__ static void refresh_v(const TgtParams& T, int lane, int d, float4* xq) {
+    if constexpr (kCache) {
+      const int nq = (d + 3) >> 2;
+      const typename Tgt::F32 kf = Tgt::f32(T, 0.0);
+      for (int q = lane; q < nq; q += G) xq[nq + q] = vquad(kf, xq[q]);
+    }
   }
 
   __device__ static void init(const TgtParams& T, int lane, int d, float4* xq, const PhiloxKey& k) {
@@ -47,6 +69,7 @@ struct SmemOps {
       for (int e = 0; e < 4; ++e) v[e] = (4 * q + e < d) ? (float)Tgt::ref_draw(T, (double)z[e]) : 0.f;
       xq[q] = make_float4(v[0], v[1], v[2], v[3]);
     }
+    refresh_v(T, lane, d, xq);
   }
 
   __device__ static double weight(const TgtParams& T, int lane, int d, double b0, double b1,
@@ -55,11 +78,18 @@ struct SmemOps {
     const int nq = (d + 3) >> 2;
     float s = 0.f;
     for (int q = lane; q < nq; q += G) {
-      const float4 x = xq[q];
-      const float xv[4] = {x.x, x.y, x.z, x.w};
+      float xv[4];
+      if constexpr (kCache) {
+        const float4 v = xq[nq + q];
+        xv[0] = v.x; xv[1] = v.y; xv[2] = v.z; xv[3] = v.w;
+      } else {
+        const float4 x = xq[q];
+        xv[0] = Tgt::vpart(kf, x.x); xv[1] = Tgt::vpart(kf, x.y);
+        xv[2] = Tgt::vpart(kf, x.z); xv[3] = Tgt::vpart(kf, x.w);
+      }
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        if (4 * q + e < d) s += Tgt::vpart(kf, xv[e]);
+        if (4 * q + e < d) s += xv[e];
     }
     return (b1 - b0) * Tgt::v_from(T, group_sum<G>((double)s));
   }
@@ -100,8 +130,8 @@ struct SmemOps {
       const double delta = group_sum<G>((double)dl);
       const double log_u = __shfl_sync(0xffffffffu, lu_pre, gbase + (p % G));
       if (log_u < delta) {  // kernel.cpp:35: accept -> regenerate the proposal's normals
-        if (aligned) accept_pass<true>(k, lane, nq, base, s, xq);
-        else accept_pass<false>(k, lane, nq, base, s, xq);
+        if (aligned) accept_pass<true>(kf, k, lane, nq, base, s, xq);
+        else accept_pass<false>(kf, k, lane, nq, base, s, xq);
       }
     }
   }
@@ -118,27 +148,36 @@ struct SmemOps {
       else k.template normals4_at<float>(base + 4 * (uint64_t)q, z);
       const float4 x = xq[q];
       const float xv[4] = {x.x, x.y, x.z, x.w};
+      if constexpr (kCache) {
+        const float4 v = xq[nq + q];
+        const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (kAligned || 4 * q + e < d) dl += Tgt::dlg(kf, xv[e], s * z[e]);
+        for (int e = 0; e < 4; ++e)
+          if (kAligned || 4 * q + e < d) dl += Tgt::dlg_cached(kf, xv[e], vv[e], fmaf(s, z[e], xv[e]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (kAligned || 4 * q + e < d) dl += Tgt::dlg(kf, xv[e], s * z[e]);
+      }
     }
     return dl;
   }
 
   template <bool kAligned>
-  __device__ static void accept_pass(const PhiloxKey& k, int lane, int nq, uint64_t base, float s,
-                                     float4* xq) {
+  __device__ static void accept_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane,
+                                     int nq, uint64_t base, float s, float4* xq) {
 #pragma unroll 1
     for (int q = lane; q < nq; q += G) {
       float z[4];
       if (kAligned) k.template normals4<float>((uint32_t)(base >> 2) + (uint32_t)q, z);
       else k.template normals4_at<float>(base + 4 * (uint64_t)q, z);
       float4 x = xq[q];
-      x.x += s * z[0];
-      x.y += s * z[1];
-      x.z += s * z[2];
-      x.w += s * z[3];
+      x.x = fmaf(s, z[0], x.x);
+      x.y = fmaf(s, z[1], x.y);
+      x.z = fmaf(s, z[2], x.z);
+      x.w = fmaf(s, z[3], x.w);
       xq[q] = x;
+      if constexpr (kCache) xq[nq + q] = vquad(kf, x);
     }
   }
 };
@@ -203,8 +242,9 @@ __global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant
   if (A.err && *(volatile int*)A.err) return;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  float4* xq = reinterpret_cast<float4*>(smem) + (size_t)g * nq;
-  LogAcc* wacc = reinterpret_cast<LogAcc*>(smem + (size_t)NG * nq * 16);
+  constexpr int kWords = CacheWords<Tgt>::value;
+  float4* xq = reinterpret_cast<float4*>(smem) + (size_t)g * nq * kWords;
+  LogAcc* wacc = reinterpret_cast<LogAcc*>(smem + (size_t)NG * nq * 16 * kWords);
   const int rows = A.t_end - A.t_begin + 1;
   LogAcc* myacc = wacc + (size_t)warp * rows * nacc;  // [row][a] of this warp
   if ((tid & 31) == 0)
@@ -236,6 +276,8 @@ __global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant
         }
       }
       lw = active ? A.lw[local] : 0.0;
+      __syncwarp();
+      Ops::refresh_v(A.tg, lane, d, xq);
     } else {
       PhiloxKey k;
       k.init(A.seed, A.round, pid, 0, 0);

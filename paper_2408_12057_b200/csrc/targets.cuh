@@ -36,6 +36,7 @@ __device__ __forceinline__ double lnpdf64(double x, double mu, double sigma, dou
 // p = {mu0, mu1, sigma}; c = {log sigma, a, mid, 1/sigma^2}
 struct TgtGaussShift {
   static constexpr bool kExact = true;
+  static constexpr bool kCacheV = false;
   __device__ static double lr64(const TgtParams& T, double x) {
     return lnpdf64(x, T.p[0], T.p[2], T.c[0]);
   }
@@ -70,6 +71,7 @@ struct TgtGaussShift {
 // p = {ref_sigma, w, mu1, s1, mu2, s2}; c = {log ref_sigma, log w, log1p(-w), log s1, log s2}
 struct TgtMixture {
   static constexpr bool kExact = false;
+  static constexpr bool kCacheV = true;  // smem pass keeps vterm(x_i) beside x_i
   __device__ static double lr64(const TgtParams& T, double x) {
     return lnpdf64(x, 0.0, T.p[0], T.c[0]);
   }
@@ -95,7 +97,9 @@ struct TgtMixture {
                (float)(T.c[1] - T.c[3] + T.c[0]), (float)T.p[2], (float)(1.0 / T.p[3]),
                (float)(T.c[2] - T.c[4] + T.c[0]), (float)T.p[4], (float)(1.0 / T.p[5])};
   }
-  // log_mix(x) - log eta(x) with the common -log(sqrt(2 pi)) - log(ref_sigma) folded out
+  // log_mix(x) - log eta(x) with the common -log(sqrt(2 pi)) - log(ref_sigma) folded out.
+  // log1p(e^{lo-hi}) with lo <= hi: the MUFU ex2/lg2 pair is accurate to ~2e-7
+  // absolute on (0, ln 2] (no cancellation: the argument of lg2 is in [1, 2]).
   __device__ static float vterm(const F32& k, float x) {
     const float s1 = (x - k.mu1) * k.inv_s1;
     const float s2 = (x - k.mu2) * k.inv_s2;
@@ -103,7 +107,18 @@ struct TgtMixture {
     const float b = k.lw2 - 0.5f * s2 * s2;
     const float hi = fmaxf(a, b), lo = fminf(a, b);
     const float sr = x * k.inv_r;
-    return hi + log1pf(expf(lo - hi)) + 0.5f * sr * sr;
+    const float e = exp2f_approx((lo - hi) * 1.4426950408889634f);
+    return hi + lg2f_approx(1.0f + e) * 0.69314718055994531f + 0.5f * sr * sr;
+  }
+  __device__ static float exp2f_approx(float v) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+  }
+  __device__ static float lg2f_approx(float v) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
   }
   // f_beta(x) up to a beta-dependent constant: log eta + beta V
   __device__ static float f(const F32& k, float x) {
@@ -111,6 +126,11 @@ struct TgtMixture {
     return -0.5f * sr * sr + k.beta * vterm(k, x);
   }
   __device__ static float dlg(const F32& k, float x, float h) { return f(k, x + h) - f(k, x); }
+  // difference form with the cached potential term v = vterm(x): one evaluation
+  __device__ static float dlg_cached(const F32& k, float x, float v, float p) {
+    const float sx = x * k.inv_r, sp = p * k.inv_r;
+    return fmaf(k.beta, vterm(k, p) - v, 0.5f * (sx - sp) * (sx + sp));
+  }
   __device__ static float vpart(const F32& k, float x) { return vterm(k, x); }
   __device__ static double v_from(const TgtParams&, double s) { return s; }
 };
@@ -120,6 +140,7 @@ struct TgtMixture {
 // c = {log s0, log s1, 1/s0^2, 1/s1^2, 0.5(1/s0^2 - 1/s1^2), log s1 - log s0}
 struct TgtScale {
   static constexpr bool kExact = true;
+  static constexpr bool kCacheV = false;
   __device__ static double lr64(const TgtParams& T, double x) {
     return lnpdf64(x, 0.0, T.p[0], T.c[0]);
   }
