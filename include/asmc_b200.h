@@ -63,6 +63,10 @@ extern "C" {
 #define ASMC_KERNEL_IDEALIZED 0
 #define ASMC_KERNEL_RWMH 1
 #define ASMC_KERNEL_IDENTITY 2
+/* new: Hamiltonian Monte Carlo cycling through step_sizes as the leapfrog
+ * epsilon (one trajectory of `leapfrog` steps per step size per sweep; unit
+ * mass; momentum = the trajectory's d normals, accept uniform after them) */
+#define ASMC_KERNEL_HMC 3
 #define ASMC_MAX_STEP_SIZES 16
 
 /* ---- resampling policies (include/asmc/engine.hpp:22) ---- */
@@ -92,7 +96,7 @@ typedef struct asmc_kernel_desc {
   int32_t kind;
   int32_t n_step_sizes;
   int32_t sweeps;
-  int32_t reserved;
+  int32_t leapfrog; /* HMC leapfrog steps per trajectory */
   double step_sizes[ASMC_MAX_STEP_SIZES];
 } asmc_kernel_desc;
 

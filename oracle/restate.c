@@ -310,6 +310,12 @@ static int validate_kernel(const asmc_kernel_desc* k) {
     for (int i = 0; i < k->n_step_sizes; ++i)
       if (!(k->step_sizes[i] > 0.0)) FAIL(ASMC_ERR_INVALID_ARGUMENT, "rwmh step sizes must be positive");
     if (k->sweeps < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "rwmh sweeps must be at least 1");
+  } else if (k->kind == ASMC_KERNEL_HMC) {
+    if (k->n_step_sizes < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "hmc requires at least one step size");
+    for (int i = 0; i < k->n_step_sizes; ++i)
+      if (!(k->step_sizes[i] > 0.0)) FAIL(ASMC_ERR_INVALID_ARGUMENT, "hmc step sizes must be positive");
+    if (k->sweeps < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "hmc sweeps must be at least 1");
+    if (k->leapfrog < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "hmc leapfrog steps must be at least 1");
   } else if (k->kind != ASMC_KERNEL_IDEALIZED && k->kind != ASMC_KERNEL_IDENTITY) {
     FAIL(ASMC_ERR_INVALID_ARGUMENT, "unknown kernel kind");
   }
@@ -335,12 +341,71 @@ static void rwmh_cycle_move(const asmc_target_desc* t, const asmc_kernel_desc* k
   }
 }
 
-/* kernel.cpp:46-63 */
+/* d/dx_i log gamma_beta(x), per coordinate (product-form targets).  NEW -- the
+ * reference has no gradient-based kernel; the device's HMC uses these exact
+ * expressions (csrc/targets.cuh grad64). */
+static double grad_log_gamma(const asmc_target_desc* t, double beta, double xi) {
+  const double* p = t->p;
+  if (t->kind == ASMC_TARGET_GAUSSIAN_SHIFT) {
+    const double a = (p[1] - p[0]) / (p[2] * p[2]);
+    return -(xi - p[0]) / (p[2] * p[2]) + beta * a;
+  }
+  if (t->kind == ASMC_TARGET_SCALE_GAUSSIAN) {
+    const double tau = (1.0 - beta) / (p[0] * p[0]) + beta / (p[1] * p[1]);
+    return -tau * xi;
+  }
+  /* mixture: grad log eta + beta * grad V, V = log_mix - log eta */
+  const double a = log(p[1]) + log_normal_pdf(xi, p[2], p[3]);
+  const double b = log1p(-p[1]) + log_normal_pdf(xi, p[4], p[5]);
+  const double r1 = 1.0 / (1.0 + exp(b - a));
+  const double glm = -(r1 * (xi - p[2]) / (p[3] * p[3]) + (1.0 - r1) * (xi - p[4]) / (p[5] * p[5]));
+  const double gref = -xi / (p[0] * p[0]);
+  return gref + beta * (glm - gref);
+}
+
+/* NEW kernel (no reference code): HMC cycling through the step sizes as the
+ * leapfrog epsilon, unit mass, `leapfrog` steps per trajectory.  Draw order per
+ * trajectory: d momentum normals, then one uniform (as RWMH: kernel.cpp:31-36).
+ * Accept iff log u < (log g(x') - log g(x)) + (|p0|^2 - |p1|^2) / 2. */
+static void hmc_cycle_move(const asmc_target_desc* t, const asmc_kernel_desc* k, double beta,
+                           double* x, double* scratch, stream_t* st) {
+  const uint64_t d = t->dim;
+  double* xp = scratch;
+  double* pm = scratch + d;
+  double log_gamma_x = log_gamma(t, beta, x);
+  for (int sweep = 0; sweep < k->sweeps; ++sweep) {
+    for (int si = 0; si < k->n_step_sizes; ++si) {
+      const double eps = k->step_sizes[si];
+      double k0 = 0.0;
+      for (uint64_t i = 0; i < d; ++i) {
+        pm[i] = normal(st);
+        k0 += pm[i] * pm[i];
+      }
+      for (uint64_t i = 0; i < d; ++i) xp[i] = x[i];
+      for (int l = 0; l < k->leapfrog; ++l) {
+        for (uint64_t i = 0; i < d; ++i) pm[i] += 0.5 * eps * grad_log_gamma(t, beta, xp[i]);
+        for (uint64_t i = 0; i < d; ++i) xp[i] += eps * pm[i];
+        for (uint64_t i = 0; i < d; ++i) pm[i] += 0.5 * eps * grad_log_gamma(t, beta, xp[i]);
+      }
+      double k1 = 0.0;
+      for (uint64_t i = 0; i < d; ++i) k1 += pm[i] * pm[i];
+      const double log_gamma_p = log_gamma(t, beta, xp);
+      const double log_u = log(uniform(st));
+      if (log_u < (log_gamma_p - log_gamma_x) + 0.5 * (k0 - k1)) {
+        for (uint64_t i = 0; i < d; ++i) x[i] = xp[i];
+        log_gamma_x = log_gamma_p;
+      }
+    }
+  }
+}
+
+/* kernel.cpp:46-63 (+ the new HMC branch) */
 static int propagate(const asmc_target_desc* t, const asmc_kernel_desc* k, double beta, double* x,
                      double* scratch, stream_t* st) {
   switch (k->kind) {
     case ASMC_KERNEL_IDEALIZED: return exact_sample(t, beta, st, x);
     case ASMC_KERNEL_RWMH: rwmh_cycle_move(t, k, beta, x, scratch, st); return 0;
+    case ASMC_KERNEL_HMC: hmc_cycle_move(t, k, beta, x, scratch, st); return 0;
     default: return 0;
   }
 }
@@ -519,7 +584,7 @@ static int run_smc_impl(const asmc_target_desc* tg, const asmc_kernel_desc* k, c
   double* xs = calloc(n * d, sizeof(double));
   double* xb = calloc(n * d, sizeof(double));
   double* lw = calloc(n, sizeof(double));
-  double* scratch = calloc(d, sizeof(double));
+  double* scratch = calloc(2 * d, sizeof(double));  /* proposal / HMC (x', p) */
   uint32_t* anc = calloc(n, sizeof(uint32_t));
   int rc = 0;
   /* engine_detail.hpp:91-100 */
@@ -642,7 +707,7 @@ int ora_run_sais_single(const asmc_target_desc* tg, const asmc_kernel_desc* k, c
   step_acc_t* glob = malloc((size_t)(T + 1) * sizeof(step_acc_t));
   step_acc_t* blk = malloc((size_t)(T + 1) * sizeof(step_acc_t));
   double* x = calloc(d, sizeof(double));
-  double* scratch = calloc(d, sizeof(double));
+  double* scratch = calloc(2 * d, sizeof(double));  /* proposal / HMC (x', p) */
   for (int t = 0; t <= T; ++t) step_acc_init(&glob[t]);
   int rc = 0;
   const uint64_t nb = block_count(n);
@@ -703,7 +768,7 @@ int ora_trajectory(const asmc_target_desc* tg, const asmc_kernel_desc* k, const 
   TRY(validate_kernel(k));
   TRY(check_target(tg));
   const uint64_t d = tg->dim;
-  double* scratch = calloc(d, sizeof(double));
+  double* scratch = calloc(2 * d, sizeof(double));  /* proposal / HMC (x', p) */
   stream_t si;
   stream_init(&si, seed, round, particle, 0, 0);
   sample_reference(tg, &si, x_out);

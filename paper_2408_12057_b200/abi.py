@@ -21,6 +21,7 @@ TARGET_SCALE_GAUSSIAN = 2
 KERNEL_IDEALIZED = 0
 KERNEL_RWMH = 1
 KERNEL_IDENTITY = 2
+KERNEL_HMC = 3
 MAX_STEP_SIZES = 16
 
 POLICY_NEVER = 0
@@ -47,7 +48,7 @@ class TargetDesc(C.Structure):
 
 class KernelDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n_step_sizes", C.c_int32), ("sweeps", C.c_int32),
-                ("reserved", C.c_int32), ("step_sizes", C.c_double * MAX_STEP_SIZES)]
+                ("leapfrog", C.c_int32), ("step_sizes", C.c_double * MAX_STEP_SIZES)]
 
 
 class Exec(C.Structure):
@@ -101,11 +102,12 @@ def scale_gaussian(sigma0, sigma1, dim=1):
     return target(TARGET_SCALE_GAUSSIAN, dim, sigma0, sigma1)
 
 
-def kernel(kind=KERNEL_IDEALIZED, step_sizes=(0.1, 1.0, 10.0), sweeps=1):
+def kernel(kind=KERNEL_IDEALIZED, step_sizes=(0.1, 1.0, 10.0), sweeps=1, leapfrog=10):
     k = KernelDesc()
     k.kind = kind
     k.n_step_sizes = len(step_sizes)
     k.sweeps = sweeps
+    k.leapfrog = leapfrog
     for i, s in enumerate(step_sizes):
         k.step_sizes[i] = float(s)
     return k

@@ -138,6 +138,14 @@ int check_kernel(const asmc_kernel_desc* k) {
       if (!(k->step_sizes[i] > 0.0))
         return fail(ASMC_ERR_INVALID_ARGUMENT, "rwmh step sizes must be positive");
     if (k->sweeps < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "rwmh sweeps must be at least 1");
+  } else if (k->kind == ASMC_KERNEL_HMC) {  // new kernel; same checks as oracle/restate.c
+    if (k->n_step_sizes < 1 || k->n_step_sizes > ASMC_MAX_STEP_SIZES)
+      return fail(ASMC_ERR_INVALID_ARGUMENT, "hmc requires 1..16 step sizes");
+    for (int i = 0; i < k->n_step_sizes; ++i)
+      if (!(k->step_sizes[i] > 0.0))
+        return fail(ASMC_ERR_INVALID_ARGUMENT, "hmc step sizes must be positive");
+    if (k->sweeps < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "hmc sweeps must be at least 1");
+    if (k->leapfrog < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "hmc leapfrog steps must be at least 1");
   } else if (k->kind != ASMC_KERNEL_IDEALIZED && k->kind != ASMC_KERNEL_IDENTITY) {
     return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown kernel kind");
   }
@@ -220,8 +228,9 @@ KernelCfg make_kcfg(const asmc_kernel_desc* k) {
   c.kind = k->kind;
   c.n_steps = k->n_step_sizes;
   c.sweeps = k->sweeps;
+  c.leapfrog = k->leapfrog;
   for (int i = 0; i < k->n_step_sizes && i < ASMC_MAX_STEP_SIZES; ++i) c.steps[i] = k->step_sizes[i];
-  if (c.kind != ASMC_KERNEL_RWMH) {
+  if (c.kind != ASMC_KERNEL_RWMH && c.kind != ASMC_KERNEL_HMC) {
     c.n_steps = 1;
     c.sweeps = 1;
   }
@@ -295,7 +304,8 @@ thread_local std::vector<ProfRec> g_prof_recs;
 double pass_normals(const PassArgs& A, uint64_t nparticles) {
   const double d = (double)A.tg.dim;
   double per_step = 0.0;
-  if (A.kc.kind == ASMC_KERNEL_RWMH) per_step = (double)A.kc.sweeps * A.kc.n_steps * d;
+  if (A.kc.kind == ASMC_KERNEL_RWMH || A.kc.kind == ASMC_KERNEL_HMC)
+    per_step = (double)A.kc.sweeps * A.kc.n_steps * d;
   else if (A.kc.kind == ASMC_KERNEL_IDEALIZED) per_step = d;
   const double steps = A.mode == kModeSmcInit ? 0.0 : (double)(A.t_end - A.t_begin + 1);
   const double init = (A.mode == kModeSmcStep) ? 0.0 : d;

@@ -46,6 +46,7 @@ asmc_kernel_desc kernel_desc(const Kernel& k) {
     throw capability_error("at most 16 rwmh step sizes are supported on the device");
   d.n_step_sizes = static_cast<int32_t>(k.step_sizes.size());
   d.sweeps = k.sweeps;
+  d.leapfrog = k.leapfrog;
   for (std::size_t i = 0; i < k.step_sizes.size(); ++i) d.step_sizes[i] = k.step_sizes[i];
   return d;
 }
@@ -256,6 +257,13 @@ bool ScaleGaussianTarget::device_descriptor(asmc_target_desc* o) const {
 
 // ---- kernel / engine ------------------------------------------------------
 void validate_kernel(const Kernel& k) {  // kernel.cpp:12-22
+  if (k.kind == KernelKind::hmc) {
+    if (k.step_sizes.empty()) throw std::invalid_argument("hmc requires at least one step size");
+    for (double s : k.step_sizes)
+      if (!(s > 0.0)) throw std::invalid_argument("hmc step sizes must be positive");
+    if (k.sweeps < 1) throw std::invalid_argument("hmc sweeps must be at least 1");
+    if (k.leapfrog < 1) throw std::invalid_argument("hmc leapfrog steps must be at least 1");
+  }
   if (k.kind == KernelKind::rwmh_cycle) {
     if (k.step_sizes.empty()) throw std::invalid_argument("rwmh_cycle requires at least one step size");
     for (double s : k.step_sizes)

@@ -123,12 +123,14 @@ class ScaleGaussianTarget final : public AnnealedTarget {
 double log_normal_pdf(double x, double mu, double sigma);
 
 // ---- kernel.hpp -----------------------------------------------------------
-enum class KernelKind { idealized_exact, rwmh_cycle, identity };
+// hmc (new): Hamiltonian Monte Carlo cycling through step_sizes as epsilon
+enum class KernelKind { idealized_exact, rwmh_cycle, identity, hmc };
 
 struct Kernel {
   KernelKind kind = KernelKind::idealized_exact;
   std::vector<double> step_sizes = {0.1, 1.0, 10.0};
   int sweeps = 1;
+  int leapfrog = 10;  // new: HMC leapfrog steps per trajectory
 };
 
 void validate_kernel(const Kernel& kernel);

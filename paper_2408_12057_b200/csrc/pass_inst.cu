@@ -29,20 +29,25 @@ static cudaError_t go(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
 }
 
 #if ASMC_PREC == 32
-template <int G>
-static cudaError_t go_smem(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
+template <int G, bool kHmc>
+static cudaError_t go_smem_k(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
   const int nacc = A.mode == kModeSmcStep ? kNAcc : 4;
   const int rows = A.t_end - A.t_begin + 1 > 0 ? A.t_end - A.t_begin + 1 : 1;
   const size_t bytes = smem_pass_bytes(G, A.tg.dim, rows - 1, nacc, CacheWords<Tgt>::value);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(pass_smem_kernel<Tgt, G>,
+    cudaError_t e = cudaFuncSetAttribute(pass_smem_kernel<Tgt, G, kHmc>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  pass_smem_kernel<Tgt, G><<<(unsigned)blocks, kBlock, bytes, s>>>(A);
+  pass_smem_kernel<Tgt, G, kHmc><<<(unsigned)blocks, kBlock, bytes, s>>>(A);
   return cudaGetLastError();
+}
+// HMC gets its own instantiation so the RWMH pass keeps its lean register allocation
+template <int G>
+static cudaError_t go_smem(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
+  return A.kc.kind == ASMC_KERNEL_HMC ? go_smem_k<G, true>(A, blocks, s) : go_smem_k<G, false>(A, blocks, s);
 }
 #endif
 

@@ -35,7 +35,7 @@ struct KernelCfg {
   int kind;  // ASMC_KERNEL_*
   int n_steps;
   int sweeps;
-  int pad;
+  int leapfrog;  // HMC
   double steps[ASMC_MAX_STEP_SIZES];
 };
 
@@ -122,6 +122,44 @@ struct Exact {
 #pragma unroll(KMAX <= 64 ? KMAX : 1)
       for (int k = 0; k < KMAX; ++k)
         if (k < d) x[k] = Tgt::exact_draw(T, mu, (double)st.normal());
+      return;
+    }
+    if (kc.kind == ASMC_KERNEL_HMC) {
+      // oracle/restate.c:hmc_cycle_move; product targets are separable, so each
+      // coordinate's trajectory runs to completion before the next is drawn
+      // (same draws, same per-coordinate arithmetic, same summation order).
+      double lgx = log_gamma(T, d, beta, x);
+      for (int sw = 0; sw < kc.sweeps; ++sw) {
+        for (int si = 0; si < kc.n_steps; ++si) {
+          const double eps = kc.steps[si];
+          double k0 = 0.0, k1 = 0.0;
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+          for (int k = 0; k < KMAX; ++k) {
+            if (k < d) {
+              double p = (double)st.normal();
+              k0 += p * p;
+              double xx = x[k];
+              double g = Tgt::grad64(T, beta, xx);
+              for (int l = 0; l < kc.leapfrog; ++l) {
+                p += 0.5 * eps * g;
+                xx += eps * p;
+                g = Tgt::grad64(T, beta, xx);
+                p += 0.5 * eps * g;
+              }
+              k1 += p * p;
+              prop[k] = xx;
+            }
+          }
+          const double lgp = log_gamma(T, d, beta, prop);
+          const double log_u = log(st.uniform());
+          if (log_u < (lgp - lgx) + 0.5 * (k0 - k1)) {
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+            for (int k = 0; k < KMAX; ++k)
+              if (k < d) x[k] = prop[k];
+            lgx = lgp;
+          }
+        }
+      }
       return;
     }
     if (kc.kind != ASMC_KERNEL_RWMH) return;
@@ -220,6 +258,39 @@ struct Fast {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (valid(lane, 4 * m + e, d)) x[4 * m + e] = (float)Tgt::exact_draw(T, mu, (double)q[e]);
+        }
+      }
+      return;
+    }
+    if (kc.kind == ASMC_KERNEL_HMC) {  // one lane per particle (G > 1 runs pass_smem)
+      if constexpr (kSeq) {
+        const typename Tgt::F32 kf = Tgt::f32(T, beta);
+        for (int sw = 0; sw < kc.sweeps; ++sw) {
+          for (int si = 0; si < kc.n_steps; ++si) {
+            const float eps = (float)kc.steps[si], he = 0.5f * eps;
+            float prop[KMAX];
+            float dl = 0.0f;
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+            for (int k = 0; k < KMAX; ++k) {
+              if (k < d) {
+                const float p0 = src.seq.normal();
+                float p = p0, xx = x[k], g = Tgt::grad32(kf, xx);
+                for (int l = 0; l < kc.leapfrog; ++l) {
+                  p = fmaf(he, g, p);
+                  xx = fmaf(eps, p, xx);
+                  g = Tgt::grad32(kf, xx);
+                  p = fmaf(he, g, p);
+                }
+                dl += Tgt::dlg(kf, x[k], xx - x[k]) + 0.5f * (p0 - p) * (p0 + p);
+                prop[k] = xx;
+              }
+            }
+            if (log(src.seq.uniform()) < (double)dl) {
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+              for (int k = 0; k < KMAX; ++k)
+                if (k < d) x[k] = prop[k];
+            }
+          }
         }
       }
       return;

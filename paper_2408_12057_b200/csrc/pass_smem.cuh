@@ -34,7 +34,7 @@ struct CacheWords {
   static constexpr int value = Tgt::kCacheV ? 2 : 1;
 };
 
-template <class Tgt, int G>
+template <class Tgt, int G, bool kHmc = false>
 struct SmemOps {
   static constexpr bool kCache = Tgt::kCacheV;
 
@@ -109,11 +109,34 @@ struct SmemOps {
       }
       return;
     }
-    if (kc.kind != ASMC_KERNEL_RWMH) return;
+    if (kc.kind != (kHmc ? ASMC_KERNEL_HMC : ASMC_KERNEL_RWMH)) return;
     const typename Tgt::F32 kf = Tgt::f32(T, beta);
     const int nprop = kc.sweeps * kc.n_steps;
     double lu_pre = 0.0;  // lane l holds log u of proposal (q0 + l)
     const int gbase = (int)(threadIdx.x & 31) & ~(G - 1);
+    if constexpr (kHmc) {
+      // oracle/restate.c:hmc_cycle_move, coordinate-separable: each lane integrates
+      // its coordinates' trajectories, the energy difference is reduced over the
+      // group, and an accepted trajectory is re-integrated from regenerated momenta.
+      const bool aligned = (d & 3) == 0;
+      for (int p = 0; p < nprop; ++p) {
+        const float eps = (float)kc.steps[p % kc.n_steps];
+        const uint64_t base = (uint64_t)p * (uint64_t)d;
+        if ((p % G) == 0) {
+          const int pp = p + lane;
+          lu_pre = pp < nprop ? log(k.uniform((uint32_t)pp)) : 0.0;
+        }
+        const float dl = aligned ? hmc_pass<true, false>(kf, k, lane, d, nq, base, eps, kc.leapfrog, xq)
+                                 : hmc_pass<false, false>(kf, k, lane, d, nq, base, eps, kc.leapfrog, xq);
+        const double delta = group_sum<G>((double)dl);
+        const double log_u = __shfl_sync(0xffffffffu, lu_pre, gbase + (p % G));
+        if (log_u < delta) {
+          if (aligned) hmc_pass<true, true>(kf, k, lane, d, nq, base, eps, kc.leapfrog, xq);
+          else hmc_pass<false, true>(kf, k, lane, d, nq, base, eps, kc.leapfrog, xq);
+        }
+      }
+      return;
+    }
     // d % 4 == 0: every proposal's draw set starts on a Philox block, so the
     // hot loops use the one-block path with no tail checks (one copy of the
     // generator per loop: the loop body stays inside the L0 I-cache).
@@ -134,6 +157,62 @@ struct SmemOps {
         else accept_pass<false>(kf, k, lane, nq, base, s, xq);
       }
     }
+  }
+
+  // one coordinate's leapfrog trajectory from (x, p); returns x', sets p'
+  __device__ static float trajectory(const typename Tgt::F32& kf, float x, float p, float eps, int L,
+                                     float& pend) {
+    const float he = 0.5f * eps;
+    float g = Tgt::grad32(kf, x);
+    for (int l = 0; l < L; ++l) {
+      p = fmaf(he, g, p);
+      x = fmaf(eps, p, x);
+      g = Tgt::grad32(kf, x);
+      p = fmaf(he, g, p);
+    }
+    pend = p;
+    return x;
+  }
+
+  // HMC over this lane's quads: kWrite = false -> energy difference
+  // H(x,p0) - H(x',p'); kWrite = true -> store the accepted x' (and vterm)
+  template <bool kAligned, bool kWrite>
+  __device__ static float hmc_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane, int d,
+                                   int nq, uint64_t base, float eps, int L, float4* xq) {
+    float dl = 0.f;
+#pragma unroll 1
+    for (int q = lane; q < nq; q += G) {
+      float z[4];
+      if (kAligned) k.template normals4<float>((uint32_t)(base >> 2) + (uint32_t)q, z);
+      else k.template normals4_at<float>(base + 4 * (uint64_t)q, z);
+      const float4 x4 = xq[q];
+      float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+      float vv[4] = {0.f, 0.f, 0.f, 0.f};
+      if constexpr (kCache && !kWrite) {
+        const float4 v = xq[nq + q];
+        vv[0] = v.x; vv[1] = v.y; vv[2] = v.z; vv[3] = v.w;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (!kAligned && 4 * q + e >= d) continue;
+        float pend;
+        const float xx = trajectory(kf, xv[e], z[e], eps, L, pend);
+        if (kWrite) {
+          xv[e] = xx;
+        } else {
+          float dlg;
+          if constexpr (kCache) dlg = Tgt::dlg_cached(kf, xv[e], vv[e], xx);
+          else dlg = Tgt::dlg(kf, xv[e], xx - xv[e]);
+          dl += dlg + 0.5f * (z[e] - pend) * (z[e] + pend);
+        }
+      }
+      if (kWrite) {
+        const float4 xn = make_float4(xv[0], xv[1], xv[2], xv[3]);
+        xq[q] = xn;
+        if constexpr (kCache) xq[nq + q] = vquad(kf, xn);
+      }
+    }
+    return dl;
   }
 
   // sum over this lane's quads of f_beta(x + s z) - f_beta(x)
@@ -231,7 +310,7 @@ __device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_po
   }
 }
 
-template <class Tgt, int G>
+template <class Tgt, int G, bool kHmc = false>
 __global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant__ PassArgs A) {
   constexpr int NG = kBlock / G;
   const int tid = threadIdx.x, g = tid / G, lane = tid % G, warp = tid >> 5;
@@ -251,7 +330,7 @@ __global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant
     for (int i = 0; i < rows * nacc; ++i)
       myacc[i] = (i % nacc == kAccTop2) ? LogAcc{-__builtin_huge_val(), -__builtin_huge_val()}
                                          : lacc_empty();
-  using Ops = SmemOps<Tgt, G>;
+  using Ops = SmemOps<Tgt, G, kHmc>;
 
   for (int r = 0; r < G; ++r) {
     const uint64_t local = blk * kBlock + (uint64_t)r * NG + g;

@@ -60,6 +60,11 @@ struct TgtGaussShift {
   __device__ static float dlg(const F32& k, float x, float h) {
     return h * (k.ba - (x - k.mu0 + 0.5f * h) * k.inv_s2);
   }
+  // d/dx log gamma_beta (oracle/restate.c:grad_log_gamma)
+  __device__ static double grad64(const TgtParams& T, double beta, double x) {
+    return -(x - T.p[0]) / (T.p[2] * T.p[2]) + beta * T.c[1];
+  }
+  __device__ static float grad32(const F32& k, float x) { return fmaf(-(x - k.mu0), k.inv_s2, k.ba); }
   __device__ static float vpart(const F32&, float x) { return x; }
   // V = a * (sum x - d * mid)
   __device__ static double v_from(const TgtParams& T, double s) {
@@ -126,6 +131,26 @@ struct TgtMixture {
     return -0.5f * sr * sr + k.beta * vterm(k, x);
   }
   __device__ static float dlg(const F32& k, float x, float h) { return f(k, x + h) - f(k, x); }
+  // gradient: grad log eta + beta (grad log_mix - grad log eta), responsibilities r1, 1 - r1
+  __device__ static double grad64(const TgtParams& T, double beta, double x) {
+    const double a = T.c[1] + lnpdf64(x, T.p[2], T.p[3], T.c[3]);
+    const double b = T.c[2] + lnpdf64(x, T.p[4], T.p[5], T.c[4]);
+    const double r1 = 1.0 / (1.0 + exp(b - a));
+    const double glm = -(r1 * (x - T.p[2]) / (T.p[3] * T.p[3]) +
+                         (1.0 - r1) * (x - T.p[4]) / (T.p[5] * T.p[5]));
+    const double gref = -x / (T.p[0] * T.p[0]);
+    return gref + beta * (glm - gref);
+  }
+  __device__ static float grad32(const F32& k, float x) {
+    const float s1 = (x - k.mu1) * k.inv_s1;
+    const float s2 = (x - k.mu2) * k.inv_s2;
+    const float a = k.lw1 - 0.5f * s1 * s1;
+    const float b = k.lw2 - 0.5f * s2 * s2;
+    const float r1 = __frcp_rn(1.0f + exp2f_approx((b - a) * 1.4426950408889634f));
+    const float glm = -(r1 * s1 * k.inv_s1 + (1.0f - r1) * s2 * k.inv_s2);
+    const float gref = -x * k.inv_r * k.inv_r;
+    return fmaf(k.beta, glm - gref, gref);
+  }
   // difference form with the cached potential term v = vterm(x): one evaluation
   __device__ static float dlg_cached(const F32& k, float x, float v, float p) {
     const float sx = x * k.inv_r, sp = p * k.inv_r;
@@ -165,6 +190,11 @@ struct TgtScale {
   __device__ static float dlg(const F32& k, float x, float h) {
     return -k.tau * h * (x + 0.5f * h);
   }
+  __device__ static double grad64(const TgtParams& T, double beta, double x) {
+    const double tau = (1.0 - beta) / (T.p[0] * T.p[0]) + beta / (T.p[1] * T.p[1]);
+    return -tau * x;
+  }
+  __device__ static float grad32(const F32& k, float x) { return -k.tau * x; }
   __device__ static float vpart(const F32&, float x) { return x * x; }
   __device__ static double v_from(const TgtParams& T, double s) {
     return T.c[4] * s - (double)T.dim * T.c[5];

@@ -181,3 +181,45 @@ def test_sais_fp32_philox_close_to_reference():
     a = ref.run_sais_single(tg, RWMH, betas, 4096, seed=1, round=1)
     b = capi.run_sais_single(tg, RWMH, betas, 4096, seed=1, round=1, exec_=abi.execopts(PH, F32))
     assert abs(a["log_z_hat"] - b["log_z_hat"]) < 2e-3 * max(1, abs(a["log_z_hat"]))
+
+
+# ---- HMC (new kernel; the oracle restatement defines it: oracle/restate.c) --------------
+HMC = abi.kernel(abi.KERNEL_HMC, (0.05, 0.2), 1, leapfrog=6)
+
+
+@pytest.mark.parametrize("name,tg", targets())
+def test_hmc_trajectories_fp64_match_oracle(name, tg):
+    betas = np.linspace(0.0, 1.0, 5)
+    for rng in (XO, PH):
+        rs = oracle.load("restate", rng)
+        pids = [0, 7, 300, 99999]
+        x, lw = capi.trajectories(tg, HMC, betas, 4, 1, pids, abi.execopts(rng, F64))
+        for i, p in enumerate(pids):
+            rx, rlw, _ = rs.trajectory(tg, HMC, betas, 4, 1, p)
+            assert np.max(np.abs(x[i] - rx)) < 1e-11, (name, rng, p)
+            assert rel(lw[i], rlw) < 1e-11
+
+
+@pytest.mark.parametrize("name,tg", targets())
+def test_hmc_trajectories_fp32_close_to_oracle(name, tg):
+    betas = np.linspace(0.0, 1.0, 5)
+    rs = oracle.load("restate", PH)
+    pids = np.arange(48)
+    for lanes in (1, 4, 32):
+        if lanes == 1 and tg.dim > 16:
+            continue
+        x, lw = capi.trajectories(tg, HMC, betas, 4, 1, pids, abi.execopts(PH, F32, lanes=lanes))
+        ok = 0
+        for i, p in enumerate(pids):
+            rx, rlw, _ = rs.trajectory(tg, HMC, betas, 4, 1, int(p))
+            if np.max(np.abs(x[i] - rx)) < 5e-4 * max(1.0, np.max(np.abs(rx))):
+                ok += 1
+        assert ok >= len(pids) - 1, (name, lanes, ok)
+
+
+def test_hmc_sais_log_z_on_device():
+    for tg in (abi.scale_gaussian(1.0, 2.0, 100), abi.gaussian_shift(0.0, 0.5, 1.0, 100)):
+        r = capi.run_sais_single(tg, abi.kernel(abi.KERNEL_HMC, (0.05, 0.15), 1, leapfrog=10),
+                                 np.linspace(0, 1, 65), 1 << 15, seed=9, round=1,
+                                 exec_=abi.execopts(PH, F32))
+        assert abs(r["log_z_hat"]) < 0.1, r["log_z_hat"]

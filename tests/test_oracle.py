@@ -267,6 +267,30 @@ def test_degenerate_weights_abort():  # test_engine.cpp:286-311 (SpreadTarget an
     assert e.value.code == abi.ERR_DEGENERATE and "degenerate" in e.value.msg
 
 
+# ------------------------- new kernel (no reference code): HMC in the oracle --
+@pytest.mark.parametrize("tag", ["xoshiro", "philox"])
+@pytest.mark.parametrize("tname", ["gauss10", "mix5", "scale7"])
+def test_hmc_oracle_log_z_unbiased_enough(tag, tname):
+    """HMC leaves pi_beta invariant, so SAIS with HMC moves estimates log Z(1) = 0
+    for these normalized families within Monte-Carlo error."""
+    rs = oracle.load("restate", RNGS[tag])
+    k = abi.kernel(abi.KERNEL_HMC, (0.05, 0.2), 1, leapfrog=8)
+    r = rs.run_sais_single(TARGETS[tname], k, np.linspace(0, 1, 33), 1 << 13, seed=3, round=1)
+    assert abs(r["log_z_hat"]) < 0.1, r["log_z_hat"]
+
+
+def test_hmc_oracle_converges_to_pi_beta():
+    """A long HMC chain at beta = 1 started from eta = N(0, 1) reaches pi_1 = N(2, 0.7^2)
+    (stationarity of the new kernel; test_kernel.cpp:119-146 analogue)."""
+    rs = oracle.load("restate")
+    tg = abi.gaussian_shift(0.0, 2.0, 0.7, 1)
+    k = abi.kernel(abi.KERNEL_HMC, (0.3,), 40, leapfrog=5)
+    xs = np.array([rs.trajectory(tg, k, [0.0, 1.0], 13, 0, p)[0][1, 0] for p in range(3000)])
+    se = 0.7 / math.sqrt(len(xs))
+    assert abs(xs.mean() - 2.0) < 5 * se
+    assert abs(xs.var() - 0.49) < 0.05
+
+
 # ------------------------------------- streams (test_rng.cpp, both families) --
 @pytest.mark.parametrize("tag", ["xoshiro", "philox"])
 def test_stream_identity_and_sensitivity(tag):  # test_rng.cpp:15-34
