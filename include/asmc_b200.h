@@ -58,6 +58,10 @@ extern "C" {
 #define ASMC_TARGET_GAUSSIAN_SHIFT 0 /* p = {mu0, mu1, sigma}                       target.cpp:57-113  */
 #define ASMC_TARGET_MIXTURE 1        /* p = {ref_sigma, weight, mu1, s1, mu2, s2}   target.cpp:115-157 */
 #define ASMC_TARGET_SCALE_GAUSSIAN 2 /* p = {sigma0, sigma1}: N(0,s0^2 I) -> N(0,s1^2 I), config 2 (new) */
+/* Bayesian logistic regression, config 4 (new): eta = N(0, sigma_p^2 I), V(theta) =
+ * sum_i y_i x_i.theta - softplus(x_i.theta); p = {sigma_p, n}; data = X (n x dim), y (n).
+ * Device path: rng = philox, precision = fp32, likelihood on tcgen05 (split-bf16). */
+#define ASMC_TARGET_LOGISTIC 3
 
 /* ---- forward kernels (include/asmc/kernel.hpp:11-27) ---- */
 #define ASMC_KERNEL_IDEALIZED 0
@@ -90,6 +94,10 @@ typedef struct asmc_target_desc {
   int32_t reserved;
   uint64_t dim;
   double p[8];
+  /* host data of data-backed plugins (LOGISTIC: X row-major n x dim float32,
+   * then y[n] float32 in {0,1}); copied to the device per call */
+  const void* data;
+  uint64_t data_bytes;
 } asmc_target_desc;
 
 typedef struct asmc_kernel_desc {

@@ -98,6 +98,43 @@ class ScaleGaussianTarget final : public asmc::AnnealedTarget {
   std::size_t dim_;
 };
 
+// Config-4 plugin: Bayesian logistic regression posterior, eta = N(0, sp^2 I),
+// gamma = eta * prod_j sigmoid(x_j.theta)^y_j (1 - sigmoid)^(1 - y_j).
+class LogisticTarget final : public asmc::AnnealedTarget {
+ public:
+  LogisticTarget(double sp, std::size_t n, std::size_t dim, const float* data)
+      : sp_(sp), n_(n), dim_(dim), X_(data), y_(data + n * dim) {
+    if (!(sp > 0.0)) throw std::invalid_argument("prior sigma must be positive");
+    if (dim == 0 || n == 0 || !data) throw std::invalid_argument("logistic target needs data");
+  }
+  std::size_t dim() const override { return dim_; }
+  double log_reference(std::span<const double> x) const override {
+    double acc = 0.0;
+    for (double xi : x) acc += asmc::log_normal_pdf(xi, 0.0, sp_);
+    return acc;
+  }
+  double potential(std::span<const double> th) const override {
+    double acc = 0.0;
+    for (std::size_t j = 0; j < n_; ++j) {
+      double l = 0.0;
+      for (std::size_t i = 0; i < dim_; ++i) l += static_cast<double>(X_[j * dim_ + i]) * th[i];
+      const double sp = l > 0.0 ? l + std::log1p(std::exp(-l)) : std::log1p(std::exp(l));
+      acc += static_cast<double>(y_[j]) * l - sp;
+    }
+    return acc;
+  }
+  void sample_reference(asmc::rng::Stream& stream, std::span<double> out) const override {
+    check_point(out);
+    for (double& xi : out) xi = sp_ * stream.normal();
+  }
+
+ private:
+  double sp_;
+  std::size_t n_, dim_;
+  const float* X_;
+  const float* y_;
+};
+
 std::unique_ptr<asmc::AnnealedTarget> make_target(const asmc_target_desc* t) {
   if (!t) throw std::invalid_argument("null target descriptor");
   const double* p = t->p;
@@ -108,6 +145,9 @@ std::unique_ptr<asmc::AnnealedTarget> make_target(const asmc_target_desc* t) {
       return std::make_unique<asmc::MixtureTarget>(p[0], p[1], p[2], p[3], p[4], p[5], t->dim);
     case ASMC_TARGET_SCALE_GAUSSIAN:
       return std::make_unique<ScaleGaussianTarget>(p[0], p[1], t->dim);
+    case ASMC_TARGET_LOGISTIC:
+      return std::make_unique<LogisticTarget>(p[0], static_cast<std::size_t>(p[1]), t->dim,
+                                              static_cast<const float*>(t->data));
   }
   throw asmc::capability_error("unknown target kind " + std::to_string(t->kind));
 }

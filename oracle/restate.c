@@ -225,6 +225,11 @@ static int check_target(const asmc_target_desc* t) {
     case ASMC_TARGET_SCALE_GAUSSIAN:
       if (!(p[0] > 0.0 && p[1] > 0.0)) FAIL(ASMC_ERR_INVALID_ARGUMENT, "scale sigmas must be positive");
       break;
+    case ASMC_TARGET_LOGISTIC:
+      if (!(p[0] > 0.0)) FAIL(ASMC_ERR_INVALID_ARGUMENT, "prior sigma must be positive");
+      if (!t->data || t->data_bytes < (uint64_t)p[1] * (t->dim + 1) * sizeof(float))
+        FAIL(ASMC_ERR_INVALID_ARGUMENT, "logistic target needs X (n x dim) and y (n) data");
+      break;
     default:
       FAIL(ASMC_ERR_CAPABILITY, "unknown target kind %d", t->kind);
   }
@@ -232,12 +237,28 @@ static int check_target(const asmc_target_desc* t) {
   return 0;
 }
 
-/* target.cpp:65-69, 133-137 and the scale plugin (oracle/ref_harness.cpp) */
+/* NEW plugin (config 4): Bayesian logistic regression, V = sum_j y_j l_j - softplus(l_j),
+ * l_j = x_j . theta, accumulated in double in row then column order. */
+static double logistic_potential(const asmc_target_desc* t, const double* th) {
+  const uint64_t d = t->dim, n = (uint64_t)t->p[1];
+  const float* X = (const float*)t->data;
+  const float* y = X + n * d;
+  double acc = 0.0;
+  for (uint64_t j = 0; j < n; ++j) {
+    double l = 0.0;
+    for (uint64_t i = 0; i < d; ++i) l += (double)X[j * d + i] * th[i];
+    const double sp = l > 0.0 ? l + log1p(exp(-l)) : log1p(exp(l));
+    acc += (double)y[j] * l - sp;
+  }
+  return acc;
+}
+
+/* target.cpp:65-69, 133-137 and the scale / logistic plugins (oracle/ref_harness.cpp) */
 static double log_reference(const asmc_target_desc* t, const double* x) {
   double acc = 0.0;
   const double* p = t->p;
   const double mu = t->kind == ASMC_TARGET_GAUSSIAN_SHIFT ? p[0] : 0.0;
-  const double sg = t->kind == ASMC_TARGET_SCALE_GAUSSIAN ? p[0] : (t->kind == ASMC_TARGET_MIXTURE ? p[0] : p[2]);
+  const double sg = t->kind == ASMC_TARGET_GAUSSIAN_SHIFT ? p[2] : p[0];
   for (uint64_t i = 0; i < t->dim; ++i) acc += log_normal_pdf(x[i], mu, sg);
   return acc;
 }
@@ -246,6 +267,7 @@ static double log_reference(const asmc_target_desc* t, const double* x) {
 static double potential(const asmc_target_desc* t, const double* x) {
   const double* p = t->p;
   double acc = 0.0;
+  if (t->kind == ASMC_TARGET_LOGISTIC) return logistic_potential(t, x);
   if (t->kind == ASMC_TARGET_GAUSSIAN_SHIFT) {
     const double a = (p[1] - p[0]) / (p[2] * p[2]);
     const double mid = 0.5 * (p[0] + p[1]);

@@ -17,6 +17,7 @@ ERR_INTERNAL = 7
 TARGET_GAUSSIAN_SHIFT = 0
 TARGET_MIXTURE = 1
 TARGET_SCALE_GAUSSIAN = 2
+TARGET_LOGISTIC = 3
 
 KERNEL_IDEALIZED = 0
 KERNEL_RWMH = 1
@@ -43,7 +44,7 @@ BLOCK = 256  # kReductionBlock, include/asmc/logsum.hpp:15
 
 class TargetDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("dim", C.c_uint64),
-                ("p", C.c_double * 8)]
+                ("p", C.c_double * 8), ("data", C.c_void_p), ("data_bytes", C.c_uint64)]
 
 
 class KernelDesc(C.Structure):
@@ -100,6 +101,44 @@ def mixture(ref_sigma, weight, mu1, sigma1, mu2, sigma2, dim=1):
 
 def scale_gaussian(sigma0, sigma1, dim=1):
     return target(TARGET_SCALE_GAUSSIAN, dim, sigma0, sigma1)
+
+
+def _bf16_round(a):
+    """round-to-nearest-even float32 -> bfloat16, returned as float32"""
+    import numpy as np
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
+def logistic_data(n=100000, d=256, seed=0):
+    """Config-4 synthetic data: X ~ N(0, 1/d) rounded to values exactly representable as a
+    bf16 hi + bf16 lo pair (so the device's split-bf16 operand is exact), theta* ~ N(0, I),
+    y ~ Bernoulli(sigmoid(X theta*)).  Deterministic in `seed` (numpy PCG64)."""
+    import numpy as np
+    g = np.random.default_rng(seed)
+    x = (g.standard_normal((n, d)) / np.sqrt(d)).astype(np.float32)
+    hi = _bf16_round(x)
+    lo = _bf16_round(x - hi)
+    X = (hi + lo).astype(np.float32)
+    theta = g.standard_normal(d)
+    p = 1.0 / (1.0 + np.exp(-(X.astype(np.float64) @ theta)))
+    y = (g.uniform(size=n) < p).astype(np.float32)
+    return X, y
+
+
+def logistic(X, y, sigma_p=1.0):
+    """Descriptor of the logistic-regression posterior; keeps the packed data alive."""
+    import numpy as np
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    n, d = X.shape
+    buf = np.concatenate([X.ravel(), y])
+    t = target(TARGET_LOGISTIC, d, sigma_p, float(n))
+    t.data = buf.ctypes.data
+    t.data_bytes = buf.nbytes
+    t._keep = buf
+    return t
 
 
 def kernel(kind=KERNEL_IDEALIZED, step_sizes=(0.1, 1.0, 10.0), sweeps=1, leapfrog=10):

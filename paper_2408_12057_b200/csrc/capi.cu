@@ -16,6 +16,7 @@
 #include "asmc_b200.h"
 #include "dispatch.h"
 #include "engine_kernels.h"
+#include "logistic.h"
 
 using namespace asmcdev;
 
@@ -169,6 +170,12 @@ int check_target(const asmc_target_desc* t) {
     case ASMC_TARGET_SCALE_GAUSSIAN:
       if (!(p[0] > 0.0 && p[1] > 0.0))
         return fail(ASMC_ERR_INVALID_ARGUMENT, "scale sigmas must be positive");
+      break;
+    case ASMC_TARGET_LOGISTIC:
+      if (!(p[0] > 0.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "prior sigma must be positive");
+      if (!(p[1] >= 1.0) || !t->data ||
+          t->data_bytes < (uint64_t)p[1] * (t->dim + 1) * sizeof(float))
+        return fail(ASMC_ERR_INVALID_ARGUMENT, "logistic target needs X (n x dim) and y (n) data");
       break;
     default:
       return fail(ASMC_ERR_CAPABILITY, "target kind %d has no device implementation", t->kind);
@@ -484,6 +491,149 @@ int enqueue_smc_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs& 
   return 0;
 }
 
+// ------------------------------------------------- config 4: logistic --
+// Data-backed target: X and y uploaded once per call, X split into bf16 hi/lo
+// rows padded to the 128-row MMA tile, TMA descriptors over both halves.
+struct LgData {
+  DBuf<float> raw;  // X (n x d) then y (n), fp32 as given
+  DBuf<uint16_t> hi, lo;
+  CUtensorMap mhi, mlo;
+  uint64_t n = 0, n_pad = 0;
+  int d = 0;
+};
+
+int lg_check(const asmc_target_desc* t, const asmc_kernel_desc* k, const asmc_exec& ex) {
+  if (ex.rng != ASMC_RNG_PHILOX || ex.precision != ASMC_PREC_FP32)
+    return fail(ASMC_ERR_CAPABILITY,
+                "the logistic-regression target runs on the tensor-core path: rng = philox, precision = fp32");
+  if (t->dim % 64 != 0 || t->dim > 256)
+    return fail(ASMC_ERR_CAPABILITY, "logistic target needs dim a multiple of 64, at most 256");
+  if (k->kind != ASMC_KERNEL_RWMH && k->kind != ASMC_KERNEL_IDENTITY)
+    return fail(ASMC_ERR_CAPABILITY, "logistic target supports the rwmh_cycle and identity kernels");
+  return 0;
+}
+
+int lg_upload(DevCtx* C, const asmc_target_desc* t, LgData& D) {
+  D.d = (int)t->dim;
+  D.n = (uint64_t)t->p[1];
+  D.n_pad = (D.n + 127) / 128 * 128;
+  TRY(D.raw.alloc(D.n * (D.d + 1), C->stream));
+  CU(cudaMemcpyAsync(D.raw.p, t->data, D.n * (D.d + 1) * sizeof(float), cudaMemcpyHostToDevice, C->stream));
+  TRY(D.hi.alloc(D.n_pad * D.d, C->stream));
+  TRY(D.lo.alloc(D.n_pad * D.d, C->stream));
+  LCH(launch_lg_split(D.raw.p, D.n, D.d, D.n_pad, D.hi.p, D.lo.p, C->stream));
+  CU(make_x_maps(D.hi.p, D.lo.p, D.n_pad, D.d, &D.mhi, &D.mlo));
+  return 0;
+}
+
+struct LgWork {
+  DBuf<float> sa, sb;
+  DBuf<float*> sbuf;
+  DBuf<int> xcur;
+  DBuf<double> lw, cum, btot;
+  DBuf<uint32_t> anc;
+  DBuf<LogAcc> part, chunk, tot;
+};
+
+// one likelihood evaluation launch, timed like the particle pass when profiling
+int lg_eval(DevCtx* C, const LgData& D, const LgArgs& A, int mode, const double* betas, float step, int q) {
+  ProfRec rec{};
+  if (g_prof) {
+    cudaEventCreate(&rec.a);
+    cudaEventCreate(&rec.b);
+    cudaEventRecord(rec.a, C->stream);
+  }
+  LCH(launch_lg_eval(D.mhi, D.mlo, A, mode, betas, step, q, C->stream));
+  if (g_prof) {
+    cudaEventRecord(rec.b, C->stream);
+    rec.normals = 2.0 * (double)D.n * D.d * (double)A.n_local;  // algorithmic flops of X theta'
+    g_prof_recs.push_back(rec);
+  }
+  return 0;
+}
+
+// run_smc (engine.cpp:97-188) for the logistic target: step-outer because the
+// likelihood of all particles is one GEMM per proposal (SAIS = policy never).
+int enqueue_lg_round(DevCtx* C, const LgData& D, const asmc_target_desc* t, const asmc_kernel_desc* k,
+                     const double* d_betas, int T, uint64_t n, int policy, double rho, uint64_t seed,
+                     uint64_t round, RoundDev* d_rd, SmcState* d_st, LgWork& W) {
+  const int d = D.d, row = d + 4;
+  const uint64_t nblk = nblocks(n), nchunks = (nblk + kChunkBlocks - 1) / kChunkBlocks;
+  TRY(W.sa.alloc(n * row, C->stream));
+  TRY(W.sb.alloc(n * row, C->stream));
+  TRY(W.sbuf.alloc(2, C->stream));
+  TRY(W.xcur.alloc(1, C->stream));
+  TRY(W.lw.alloc(n, C->stream));
+  TRY(W.cum.alloc(n, C->stream));
+  TRY(W.btot.alloc(nblk, C->stream));
+  TRY(W.anc.alloc(n, C->stream));
+  TRY(W.part.alloc((size_t)kNAcc * nblk, C->stream));
+  TRY(W.chunk.alloc((size_t)kNAcc * nchunks, C->stream));
+  TRY(W.tot.alloc(kNAcc, C->stream));
+  float* ptrs[2] = {W.sa.p, W.sb.p};
+  CU(cudaMemcpyAsync(W.sbuf.p, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemsetAsync(W.xcur.p, 0, sizeof(int), C->stream));
+  CU(cudaMemsetAsync(W.lw.p, 0, n * sizeof(double), C->stream));
+  LgArgs A;
+  std::memset(&A, 0, sizeof A);
+  A.state = W.sbuf.p;
+  A.xcur = W.xcur.p;
+  A.lw = W.lw.p;
+  A.y = D.raw.p + D.n * (uint64_t)d;
+  A.n = D.n;
+  A.n_local = n;
+  A.d = d;
+  A.row = row;
+  A.seed = seed;
+  A.round = round;
+  A.sigma_p = t->p[0];
+  A.err = &d_st->err;
+  LCH(launch_lg_init(A, C->stream));        // engine_detail.hpp:91-100
+  TRY(lg_eval(C, D, A, 0, d_betas, 0.f, 0));  // V(theta_0)
+  const int nprop = k->kind == ASMC_KERNEL_RWMH ? k->sweeps * k->n_step_sizes : 0;
+  for (int s = 1; s <= T; ++s) {
+    A.t = s;
+    LCH(launch_lg_weight(A, d_betas, s, W.part.p, nblk, C->stream));
+    LCH(launch_fold(false, W.part.p, nblk, nblk, 0, 1, kNAcc, W.chunk.p, W.tot.p, C->stream));
+    LCH(launch_smc_decide(W.tot.p, s, T, n, policy, rho, seed, round, ASMC_RNG_PHILOX, d_rd, C->stream));
+    for (int q = 0; q < nprop; ++q)  // kernel.cpp:31-40 at beta_t
+      TRY(lg_eval(C, D, A, 1, d_betas, (float)k->step_sizes[q % k->n_step_sizes], q));
+    LCH(launch_resample(W.lw.p, n, d_st, W.cum.p, W.btot.p, W.anc.p, C->stream));
+    g_launches += 3;
+    LCH(launch_gather(W.anc.p, n, (uint64_t)row * sizeof(float), reinterpret_cast<void* const*>(W.sbuf.p),
+                      W.xcur.p, W.lw.p, d_st, C->sms, C->stream));
+    g_launches += 1;
+  }
+  return 0;
+}
+
+int copy_round(cudaStream_t s, RoundBufs& R, int T, bool smc, asmc_report* out, SmcState* st);
+
+// asmc_run_smc / asmc_run_sais_single body for the logistic target
+int run_lg_single(const asmc_target_desc* target, const asmc_kernel_desc* kernel, const double* betas, int T,
+                  uint64_t n, int policy, double rho, uint64_t seed, uint64_t round, const asmc_exec& ex,
+                  asmc_report* out, bool smc) {
+  TRY(lg_check(target, kernel, ex));
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C, ex.stream));
+  const double t0 = now_s();
+  DBuf<double> d_betas;
+  TRY(d_betas.alloc(T + 1, C->stream));
+  CU(cudaMemcpyAsync(d_betas.p, betas, sizeof(double) * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  RoundBufs R;
+  TRY(R.alloc(T, C->stream));
+  LgData D;
+  TRY(lg_upload(C, target, D));
+  LgWork W;
+  TRY(enqueue_lg_round(C, D, target, kernel, d_betas.p, T, n, policy, rho, seed, round, R.rd.p, R.st.p, W));
+  SmcState st;
+  TRY(copy_round(C->stream, R, T, smc, out, &st));
+  TRY(device_error(st.err, st.err_step, st.err_val));
+  out->kernel_applications = n * (uint64_t)T;
+  out->wall_seconds = now_s() - t0;
+  return 0;
+}
+
 int copy_round(cudaStream_t s, RoundBufs& R, int T, bool smc, asmc_report* out, SmcState* st) {
   std::vector<double> tmp(T + 1);
   auto get = [&](const double* src, double* dst) -> int {
@@ -546,6 +696,8 @@ int asmc_run_sais_single(const asmc_target_desc* target, const asmc_kernel_desc*
   TRY(check_pair(target, kernel));
   if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null report");
   const asmc_exec ex = exec ? *exec : default_exec();
+  if (target->kind == ASMC_TARGET_LOGISTIC)  // SAIS == run_smc(never) (drivers.hpp:80-86)
+    return run_lg_single(target, kernel, betas, T, n, ASMC_POLICY_NEVER, 0.5, seed, round, ex, out, false);
   Layout L;
   TRY(choose_layout(ex, target->dim, &L, T, 4));
   DevCtx* C;
@@ -579,6 +731,8 @@ int asmc_run_smc(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
   if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null report");
   if (n > 0xffffffffull) return fail(ASMC_ERR_CAPABILITY, "ancestor indices are 32-bit");
   const asmc_exec ex = exec ? *exec : default_exec();
+  if (target->kind == ASMC_TARGET_LOGISTIC)
+    return run_lg_single(target, kernel, betas, T, n, policy, rho, seed, round, ex, out, true);
   Layout L;
   TRY(choose_layout(ex, target->dim, &L));
   DevCtx* C;
@@ -634,7 +788,13 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
   if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null output");
   const asmc_exec ex = exec ? *exec : default_exec();
   Layout L;
-  TRY(choose_layout_impl(ex, target->dim, &L));
+  const bool lg = target->kind == ASMC_TARGET_LOGISTIC;
+  if (lg) {
+    TRY(lg_check(target, kernel, ex));
+    L = Layout{1, 0};
+  } else {
+    TRY(choose_layout_impl(ex, target->dim, &L));
+  }
   // The (N_k, T_k) plan depends on the budget rule only, so the whole round
   // loop is enqueued up front; only the betas are data-dependent (device).
   std::vector<uint64_t> ns(rounds);
@@ -651,6 +811,8 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
       if (ns[k] > 0xffffffffull) return fail(ASMC_ERR_CAPABILITY, "ancestor indices are 32-bit");
   DevCtx* C;
   TRY(get_ctx(ex.device, &C, ex.stream));
+  LgData lgd;
+  if (lg) TRY(lg_upload(C, target, lgd));
   const int stride = out->max_steps + 1;
   std::vector<RoundBufs> R(rounds);
   std::vector<DBuf<double>> betas(rounds);
@@ -670,7 +832,12 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
   for (auto& e : ev) CU(cudaEventCreate(&e));
   CU(cudaEventRecord(ev[0], C->stream));
   for (int k = 0; k < rounds; ++k) {
-    if (mode == ASMC_MODE_SAIS) {
+    if (lg) {  // config 4: step-outer tensor-core engine (SAIS = policy never)
+      LgWork w;
+      TRY(enqueue_lg_round(C, lgd, target, kernel, betas[k].p, ts[k], ns[k],
+                           mode == ASMC_MODE_SAIS ? ASMC_POLICY_NEVER : policy, rho, seed,
+                           (uint64_t)(k + 1), R[k].rd.p, R[k].st.p, w));
+    } else if (mode == ASMC_MODE_SAIS) {
       SaisWork w;  // stream-ordered: freed after this round's kernels retire
       TRY(enqueue_sais_round(C, ex, L, base, betas[k].p, ts[k], ns[k], seed, (uint64_t)(k + 1),
                              R[k].rd.p, gerr.p, w));
