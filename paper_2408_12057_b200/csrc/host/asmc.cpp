@@ -255,6 +255,38 @@ bool ScaleGaussianTarget::device_descriptor(asmc_target_desc* o) const {
   return true;
 }
 
+LogisticTarget::LogisticTarget(std::vector<float> X, std::vector<float> y, std::size_t dim, double sp)
+    : y_(std::move(y)), dim_(dim), sp_(sp) {
+  if (!(sp > 0.0)) throw std::invalid_argument("prior sigma must be positive");
+  if (dim == 0 || y_.empty() || X.size() != y_.size() * dim)
+    throw std::invalid_argument("logistic target needs X (n x dim) and y (n)");
+  data_ = std::move(X);
+  data_.insert(data_.end(), y_.begin(), y_.end());
+}
+double LogisticTarget::log_reference(std::span<const double> x) const {
+  double s = 0.0;
+  for (double v : x) s += log_normal_pdf(v, 0.0, sp_);
+  return s;
+}
+double LogisticTarget::potential(std::span<const double> th) const {
+  double acc = 0.0;
+  for (std::size_t j = 0; j < y_.size(); ++j) {
+    double l = 0.0;
+    for (std::size_t i = 0; i < dim_; ++i) l += static_cast<double>(data_[j * dim_ + i]) * th[i];
+    acc += y_[j] * l - (l > 0.0 ? l + std::log1p(std::exp(-l)) : std::log1p(std::exp(l)));
+  }
+  return acc;
+}
+bool LogisticTarget::device_descriptor(asmc_target_desc* o) const {
+  o->kind = ASMC_TARGET_LOGISTIC;
+  o->dim = dim_;
+  o->p[0] = sp_;
+  o->p[1] = static_cast<double>(y_.size());
+  o->data = data_.data();
+  o->data_bytes = data_.size() * sizeof(float);
+  return true;
+}
+
 // ---- kernel / engine ------------------------------------------------------
 void validate_kernel(const Kernel& k) {  // kernel.cpp:12-22
   if (k.kind == KernelKind::hmc) {

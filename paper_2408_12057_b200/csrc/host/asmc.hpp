@@ -120,6 +120,24 @@ class ScaleGaussianTarget final : public AnnealedTarget {
   std::size_t dim_;
 };
 
+// Config-4 plugin (new): Bayesian logistic regression posterior; X is n x dim
+// row-major, y in {0, 1}; prior N(0, sigma_p^2 I).  Sampled on the tcgen05 path.
+class LogisticTarget final : public AnnealedTarget {
+ public:
+  LogisticTarget(std::vector<float> X, std::vector<float> y, std::size_t dim, double sigma_p);
+  std::size_t dim() const override { return dim_; }
+  double log_reference(std::span<const double> x) const override;
+  double potential(std::span<const double> x) const override;
+  bool device_descriptor(asmc_target_desc* out) const override;
+  std::size_t n_data() const { return y_.size(); }
+
+ private:
+  std::vector<float> data_;  // X then y, the C-ABI's packed layout
+  std::vector<float> y_;
+  std::size_t dim_;
+  double sp_;
+};
+
 double log_normal_pdf(double x, double mu, double sigma);
 
 // ---- kernel.hpp -----------------------------------------------------------

@@ -1,0 +1,96 @@
+"""Config 4: Bayesian logistic regression with the likelihood on the tensor cores.
+
+Oracle: the unmodified reference engine (oracle/_ref, Philox shadow streams) running
+the LogisticTarget plugin of oracle/ref_harness.cpp (double precision), and the
+restatement's identical plugin.  Tolerances: the split-bf16 tensor-core likelihood
+(3 MMAs, fp32 accumulate, fp64 row sums) reproduces V(theta) to ~1e-7 relative, so
+increment statistics must agree to 1e-6 relative (identity kernel) and 1e-5
+(RWMH, where a near-boundary MH decision may differ), log Z likewise.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2408_12057_b200 import abi, capi
+
+PH, F32 = abi.RNG_PHILOX, abi.PREC_FP32
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ref():
+    return oracle.load("ref", PH) if oracle.available("ref", PH) else oracle.load("restate", PH)
+
+
+def test_synthetic_data_is_split_bf16_exact():
+    X, y = abi.logistic_data(500, 64, 3)
+    hi = abi._bf16_round(X)
+    lo = abi._bf16_round(X - hi)
+    assert np.array_equal(hi + lo, X)  # the device's split operand is exact
+    assert set(np.unique(y)) <= {0.0, 1.0}
+
+
+def test_restatement_plugin_matches_reference_plugin():
+    if not oracle.available("ref", PH):
+        pytest.skip("reference not built here")
+    X, y = abi.logistic_data(400, 64, 1)
+    tg = abi.logistic(X, y, 1.0)
+    k = abi.kernel(abi.KERNEL_RWMH, (0.01, 0.05), 1)
+    a = oracle.load("ref", PH).run_smc(tg, k, np.linspace(0, 1, 4), 64, policy=abi.POLICY_ALWAYS, seed=4)
+    b = oracle.load("restate", PH).run_smc(tg, k, np.linspace(0, 1, 4), 64, policy=abi.POLICY_ALWAYS, seed=4)
+    assert a["log_z_hat"] == b["log_z_hat"] and np.array_equal(a["log_g2"], b["log_g2"])
+
+
+def test_tensor_core_kernel_in_sass():
+    so = os.path.join(ROOT, "paper_2408_12057_b200", "libasmc_b200.so")
+    elf = subprocess.run(["cuobjdump", "-elf", so], capture_output=True, text=True)
+    if elf.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    import re
+    name = sorted(set(re.findall(r"_ZN7asmcdev14lg_eval_kernel\w*?fi\b", elf.stdout)))[0]
+    out = subprocess.run(["cuobjdump", "-sass", "-fun", name, so], capture_output=True, text=True)
+    assert "UTCHMMA" in out.stdout and "UTMALDG" in out.stdout and "LDTM" in out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kname", ["identity", "rwmh"])
+def test_logistic_sais_matches_reference(kname):
+    X, y = abi.logistic_data(3000, 64, 0)
+    tg = abi.logistic(X, y, 1.0)
+    k = abi.kernel(abi.KERNEL_IDENTITY) if kname == "identity" else \
+        abi.kernel(abi.KERNEL_RWMH, (0.01, 0.03, 0.1), 1)
+    betas = np.linspace(0, 1, 5)
+    a = _ref().run_sais_single(tg, k, betas, 384, seed=2, round=1)
+    b = capi.run_sais_single(tg, k, betas, 384, seed=2, round=1, exec_=abi.execopts(PH, F32))
+    tol = 1e-6 if kname == "identity" else 1e-5
+    for g in ("log_g0", "log_g1", "log_g2"):
+        assert np.max(np.abs(a[g][1:] - b[g][1:]) / np.abs(a[g][1:]).clip(1)) < tol, g
+    assert abs(a["log_z_hat"] - b["log_z_hat"]) < tol * abs(a["log_z_hat"])
+
+
+@pytest.mark.gpu
+def test_logistic_ssmc_and_rounds_run():
+    X, y = abi.logistic_data(2000, 128, 5)
+    tg = abi.logistic(X, y, 1.0)
+    k = abi.kernel(abi.KERNEL_RWMH, (0.01, 0.02), 1)
+    ref = _ref()
+    betas = np.linspace(0, 1, 7)
+    a = ref.run_smc(tg, k, betas, 300, policy=abi.POLICY_ADAPTIVE_ESS, seed=3, round=1)
+    b = capi.run_smc(tg, k, betas, 300, policy=abi.POLICY_ADAPTIVE_ESS, seed=3, round=1,
+                     exec_=abi.execopts(PH, F32))
+    assert a["resample_times"] == b["resample_times"]
+    assert abs(a["log_z_hat"] - b["log_z_hat"]) < 1e-4 * abs(a["log_z_hat"])
+    r = capi.run_rounds(tg, k, abi.MODE_SAIS, 256, 3, seed=1, exec_=abi.execopts(PH, F32))
+    assert list(r["steps"]) == [1, 2, 3] and np.all(np.isfinite(r["log_z_hat"]))
+
+
+@pytest.mark.gpu
+def test_logistic_rejects_unsupported_modes():
+    X, y = abi.logistic_data(100, 64, 0)
+    tg = abi.logistic(X, y, 1.0)
+    with pytest.raises(capi.AsmcError) as e:
+        capi.run_sais_single(tg, abi.kernel(abi.KERNEL_RWMH), [0.0, 1.0], 16,
+                             exec_=abi.execopts(abi.RNG_XOSHIRO, abi.PREC_FP64))
+    assert e.value.code == abi.ERR_CAPABILITY
