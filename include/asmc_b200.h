@@ -17,6 +17,9 @@
  *   asmc_sais_partials    <- the per-wave block fold of run_sais_single, src/drivers.cpp:113-146
  *                            (one particle range per GPU; see asmc_fold_partials)
  *   asmc_fold_partials    <- the ordered fold + report tail, src/drivers.cpp:137-176
+ *   asmc_smc_shard_*      <- asmc::run_smc split per GPU: step_pass (src/engine_detail.hpp:113-156),
+ *                            ess/decide (src/engine.cpp:46-59,82-95,140-160), systematic
+ *                            resample + gather (src/engine.cpp:61-80,161-173)
  *   asmc_systematic_resample <- asmc::systematic_resample  src/engine.cpp:61-80
  *   asmc_ess              <- asmc::ess                src/engine.cpp:46-59
  *   asmc_barrier_estimate <- asmc::barrier_estimate   src/schedule.cpp:41-56
@@ -202,6 +205,51 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
  * tail of run_sais_single (drivers.cpp:148-176). Host-side scalar code. */
 int asmc_fold_partials(const asmc_logacc* partials, uint64_t chunks, int32_t steps,
                        uint64_t n_particles, asmc_report* out);
+
+/* Multi-GPU SSMC: run_smc (src/engine.cpp:97-188) with the particles of one round
+ * split into contiguous shards, one per GPU, each shard starting at a multiple of
+ * ASMC_FOLD_CHUNK.  The caller owns the communication (NCCL/gloo through
+ * torch.distributed, or anything else) and passes DEVICE buffers; the library
+ * never syncs except where a host decision is needed (decide, plan).  Every rank
+ * computes the same totals, decisions and ancestors as a single-GPU asmc_run_smc
+ * with rng = philox, precision = fp32 (bit-identical report).  Per step t:
+ *   1. asmc_smc_shard_step    pass + local fold -> this shard's chunk partials,
+ *                             chunk-major: partials[c * ASMC_SHARD_NACC + a]
+ *   2. caller all-gathers the partials of all shards in rank order
+ *   3. asmc_smc_shard_decide  fold + ESS + policy (engine.cpp:82-95,140-160);
+ *                             if *resample, writes this shard's block CDF totals
+ *                             (asmc_smc_shard_blocks entries) to block_totals
+ *   4. (resample) caller all-gathers the block totals in rank order
+ *   5. asmc_smc_shard_plan    global CDF offsets (scanned IN PLACE in the gathered
+ *                             totals buffer, which this rank must own); slot_begin[r] (host, world+1)
+ *                             = first output slot whose ancestor lies in shard r
+ *   6. asmc_smc_shard_pack    rows of the ancestors of slots [slot_begin[me],
+ *                             slot_begin[me+1]) in slot order (row_bytes each)
+ *   7. caller all-to-all: shard r's packed rows for slots in shard q go to q
+ *   8. asmc_smc_shard_accept  the received rows (this shard's slots, in order)
+ *                             become the particles; log-weights reset to 0
+ * asmc_smc_shard_report after step T fills the (replicated) run_smc report. */
+#define ASMC_SHARD_NACC 6 /* accumulators per chunk partial: g0 g1 g2 elbo sq top2 */
+typedef struct asmc_smc_shard asmc_smc_shard;
+int asmc_smc_shard_create(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                          const double* betas, int32_t steps, uint64_t n_particles,
+                          uint64_t p_begin, uint64_t p_end, int32_t policy, double rho,
+                          uint64_t seed, uint64_t round, const asmc_exec* exec,
+                          asmc_smc_shard** out);
+void asmc_smc_shard_destroy(asmc_smc_shard* shard);
+uint64_t asmc_smc_shard_chunks(const asmc_smc_shard* shard);
+uint64_t asmc_smc_shard_blocks(const asmc_smc_shard* shard);
+uint64_t asmc_smc_shard_row_bytes(const asmc_smc_shard* shard);
+int asmc_smc_shard_step(asmc_smc_shard* shard, int32_t t, asmc_logacc* partials_dev);
+int asmc_smc_shard_decide(asmc_smc_shard* shard, int32_t t, const asmc_logacc* all_partials_dev,
+                          uint64_t all_chunks, double* block_totals_dev, int32_t* resample);
+int asmc_smc_shard_plan(asmc_smc_shard* shard, double* all_block_totals_dev, uint64_t all_blocks,
+                        int32_t world, const uint64_t* shard_p_begin, uint64_t* slot_begin);
+int asmc_smc_shard_pack(asmc_smc_shard* shard, void* rows_dev);
+int asmc_smc_shard_accept(asmc_smc_shard* shard, const void* rows_dev);
+int asmc_smc_shard_report(asmc_smc_shard* shard, asmc_report* out);
+/* parity hook: copy this shard's particles (row-major, row_bytes each) and log-weights */
+int asmc_smc_shard_state(asmc_smc_shard* shard, void* rows_host, double* log_w_host);
 
 /* ---- parity hooks ---- */
 /* key = {seed, round, particle, step, substep} (rng.hpp:11-17) */

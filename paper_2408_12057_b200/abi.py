@@ -40,6 +40,7 @@ PREC_FP32 = 1
 
 FOLD_CHUNK = 262144
 BLOCK = 256  # kReductionBlock, include/asmc/logsum.hpp:15
+SHARD_NACC = 6  # ASMC_SHARD_NACC: g0 g1 g2 elbo sq top2 per chunk partial
 
 
 class TargetDesc(C.Structure):

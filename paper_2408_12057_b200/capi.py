@@ -281,11 +281,90 @@ def peak_normals(device, blocks, quads_per_thread):
     return s.value
 
 
+class SmcShard:
+    """One GPU's particle shard of a multi-GPU run_smc (asmc_smc_shard_* in
+    include/asmc_b200.h).  Buffers passed to the methods are DEVICE addresses
+    (ints, e.g. ``tensor.data_ptr()``) on ``exec_.device``; the caller owns them
+    and the collectives between the calls (paper_2408_12057_b200/distributed.py)."""
+
+    def __init__(self, target, kernel, betas, n, p_begin, p_end, policy=abi.POLICY_ADAPTIVE_ESS,
+                 rho=0.5, seed=0, round=0, exec_=None):
+        L = lib()
+        self._lib = L
+        for f in ("asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes"):
+            getattr(L, f).restype = C.c_uint64
+            getattr(L, f).argtypes = [C.c_void_p]
+        L.asmc_smc_shard_destroy.argtypes = [C.c_void_p]
+        L.asmc_smc_shard_destroy.restype = None
+        betas = np.ascontiguousarray(betas, dtype=np.float64)
+        self.T = len(betas) - 1
+        self.n, self.p_begin, self.p_end = n, p_begin, p_end
+        self.exec_ = exec_ or abi.execopts(abi.RNG_PHILOX, abi.PREC_FP32)
+        self._target = target  # keeps a data-backed target's buffer alive
+        h = C.c_void_p()
+        _check(L.asmc_smc_shard_create(C.byref(target), C.byref(kernel), _arr(betas, C.c_double),
+                                       C.c_int32(self.T), C.c_uint64(n), C.c_uint64(p_begin),
+                                       C.c_uint64(p_end), C.c_int32(policy), C.c_double(rho),
+                                       C.c_uint64(seed), C.c_uint64(round), C.byref(self.exec_),
+                                       C.byref(h)))
+        self._h = h
+        self.chunks = L.asmc_smc_shard_chunks(h)
+        self.blocks = L.asmc_smc_shard_blocks(h)
+        self.row_bytes = L.asmc_smc_shard_row_bytes(h)
+
+    def step(self, t, partials_ptr):
+        _check(self._lib.asmc_smc_shard_step(self._h, C.c_int32(t), C.c_void_p(partials_ptr)))
+
+    def decide(self, t, all_partials_ptr, all_chunks, block_totals_ptr):
+        flag = C.c_int32(0)
+        _check(self._lib.asmc_smc_shard_decide(self._h, C.c_int32(t), C.c_void_p(all_partials_ptr),
+                                                C.c_uint64(all_chunks), C.c_void_p(block_totals_ptr),
+                                                C.byref(flag)))
+        return bool(flag.value)
+
+    def plan(self, all_block_totals_ptr, all_blocks, shard_p_begin):
+        b = np.ascontiguousarray(shard_p_begin, dtype=np.uint64)
+        out = np.zeros(len(b), np.uint64)
+        _check(self._lib.asmc_smc_shard_plan(self._h, C.c_void_p(all_block_totals_ptr),
+                                              C.c_uint64(all_blocks), C.c_int32(len(b) - 1),
+                                              _arr(b, C.c_uint64), _arr(out, C.c_uint64)))
+        return [int(v) for v in out]
+
+    def pack(self, rows_ptr):
+        _check(self._lib.asmc_smc_shard_pack(self._h, C.c_void_p(rows_ptr)))
+
+    def accept(self, rows_ptr):
+        _check(self._lib.asmc_smc_shard_accept(self._h, C.c_void_p(rows_ptr)))
+
+    def report(self):
+        rep, bufs = _report(self.T)
+        _check(self._lib.asmc_smc_shard_report(self._h, C.byref(rep)))
+        return _finish(rep, bufs, True)
+
+    def state(self):
+        nl = self.p_end - self.p_begin
+        rows = np.zeros(nl * self.row_bytes, np.uint8)
+        lw = np.zeros(nl)
+        _check(self._lib.asmc_smc_shard_state(self._h, _arr(rows, C.c_uint8), _arr(lw, C.c_double)))
+        return rows.view(np.float32).reshape(nl, -1), lw
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.asmc_smc_shard_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
 EXPORTED = [
     "asmc_last_error", "asmc_version", "asmc_device_count", "asmc_launch_count", "asmc_run_smc",
     "asmc_run_sais_single", "asmc_run_rounds", "asmc_fold_chunks", "asmc_sais_partials",
     "asmc_fold_partials", "asmc_rng_u64", "asmc_rng_uniform", "asmc_rng_normal",
     "asmc_trajectories", "asmc_systematic_resample", "asmc_ess", "asmc_barrier_estimate",
     "asmc_generate_schedule", "asmc_local_barrier", "asmc_budget", "asmc_profile_enable",
-    "asmc_profile_collect", "asmc_peak_normals",
+    "asmc_profile_collect", "asmc_peak_normals", "asmc_smc_shard_create", "asmc_smc_shard_destroy",
+    "asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes",
+    "asmc_smc_shard_step", "asmc_smc_shard_decide", "asmc_smc_shard_plan", "asmc_smc_shard_pack",
+    "asmc_smc_shard_accept", "asmc_smc_shard_report", "asmc_smc_shard_state",
 ]

@@ -1239,3 +1239,252 @@ int asmc_peak_normals(int32_t device, int32_t blocks, uint64_t quads_per_thread,
 }
 
 }  // extern "C"
+
+// ============================================================ sharded SSMC
+// One particle shard of a multi-GPU run_smc (include/asmc_b200.h).  The state,
+// log-weights and block CDF stay on this GPU; what crosses GPUs is the chunk
+// partials (ASMC_SHARD_NACC x 16 B per 262144 particles per step), the block CDF
+// totals (8 B per 256 particles per resampling event) and the resampled rows.
+struct asmc_smc_shard {
+  DevCtx C;
+  asmc_exec ex;
+  Layout L;
+  PassArgs A;
+  int T = 0, policy = 0, t_done = 0, me = -1, resampling = 0;
+  double rho = 0.5;
+  uint64_t n = 0, p_begin = 0, n_local = 0, seed = 0, round = 0;
+  uint64_t nblk = 0, nch = 0, row_bytes = 0, anc_cap = 0;
+  DBuf<double> betas, lw, cum;
+  DBuf<char> x;
+  DBuf<void*> xbuf;
+  DBuf<int> xcur;
+  DBuf<uint32_t> anc;
+  DBuf<LogAcc> part, chunk, tot;
+  DBuf<uint64_t> rank_blk, slot_dev;
+  RoundBufs R;
+  std::vector<uint64_t> slots;
+};
+
+extern "C" {
+
+int asmc_smc_shard_create(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                          const double* betas, int32_t T, uint64_t n, uint64_t p_begin, uint64_t p_end,
+                          int32_t policy, double rho, uint64_t seed, uint64_t round,
+                          const asmc_exec* exec, asmc_smc_shard** out) {
+  if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null shard handle");
+  *out = nullptr;
+  TRY(check_schedule(betas, T));
+  if (n < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "n_particles must be at least 1");
+  if (!(rho >= 0.0 && rho <= 1.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "rho must lie in [0, 1]");
+  if (policy < ASMC_POLICY_NEVER || policy > ASMC_POLICY_STABILIZED)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown resampling policy");
+  TRY(check_pair(target, kernel));
+  if (n > 0xffffffffull) return fail(ASMC_ERR_CAPABILITY, "ancestor indices are 32-bit");
+  if (p_begin % ASMC_FOLD_CHUNK != 0)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "p_begin must be a multiple of ASMC_FOLD_CHUNK");
+  if (p_end > n || p_end <= p_begin) return fail(ASMC_ERR_INVALID_ARGUMENT, "bad particle range");
+  if (p_end != n && p_end % ASMC_FOLD_CHUNK != 0)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "p_end must be n_particles or a multiple of ASMC_FOLD_CHUNK");
+  const asmc_exec ex = exec ? *exec : default_exec();
+  if (ex.precision == ASMC_PREC_FP64 || ex.rng != ASMC_RNG_PHILOX)
+    return fail(ASMC_ERR_CAPABILITY,
+                "sharded SSMC uses the fp32 tree fold (rng = philox, precision = fp32); the fp64 reference order is single-GPU");
+  if (target->kind == ASMC_TARGET_LOGISTIC)
+    return fail(ASMC_ERR_CAPABILITY, "sharded SSMC does not support the logistic target yet");
+  auto* h = new asmc_smc_shard;
+  auto drop = [&](int rc) { delete h; return rc; };
+  int rc = choose_layout(ex, target->dim, &h->L);
+  if (rc) return drop(rc);
+  DevCtx* C;
+  if ((rc = get_ctx(ex.device, &C, ex.stream))) return drop(rc);
+  h->C = *C;
+  h->ex = ex;
+  h->T = T;
+  h->policy = policy;
+  h->rho = rho;
+  h->n = n;
+  h->p_begin = p_begin;
+  h->n_local = p_end - p_begin;
+  h->seed = seed;
+  h->round = round;
+  h->nblk = nblocks(h->n_local);
+  h->nch = asmc_fold_chunks(p_begin, p_end);
+  h->row_bytes = target->dim * sizeof(float);
+  cudaStream_t s = h->C.stream;
+  const uint64_t nl = h->n_local;
+  rc = [&]() -> int {
+    TRY(h->betas.alloc(T + 1, s));
+    CU(cudaMemcpyAsync(h->betas.p, betas, sizeof(double) * (T + 1), cudaMemcpyHostToDevice, s));
+    TRY(h->x.alloc(nl * h->row_bytes, s));
+    TRY(h->xbuf.alloc(2, s));
+    TRY(h->xcur.alloc(1, s));
+    TRY(h->lw.alloc(nl, s));
+    TRY(h->cum.alloc(nl, s));
+    TRY(h->part.alloc((size_t)kNAcc * h->nblk, s));
+    TRY(h->chunk.alloc((size_t)kNAcc * h->nch, s));
+    TRY(h->tot.alloc(kNAcc, s));
+    TRY(h->R.alloc(T, s));
+    void* ptrs[2] = {h->x.p, h->x.p};  // in-place state: resampled rows arrive via accept
+    CU(cudaMemcpyAsync(h->xbuf.p, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, s));
+    CU(cudaMemsetAsync(h->xcur.p, 0, sizeof(int), s));
+    PassArgs& A = h->A;
+    A = base_args(target, kernel);
+    A.betas = h->betas.p;
+    A.T = T;
+    A.n = n;
+    A.p_begin = p_begin;
+    A.n_local = nl;
+    A.seed = seed;
+    A.round = round;
+    A.xbuf = h->xbuf.p;
+    A.xcur = h->xcur.p;
+    A.lw = h->lw.p;
+    A.part = h->part.p;
+    A.part_stride = h->nblk;
+    A.err = &h->R.st.p->err;
+    A.mode = kModeSmcInit;  // engine_detail.hpp:91-100, global particle ids
+    LCH(launch_pass(h->ex, h->L, A, h->nblk, s));
+    return 0;
+  }();
+  if (rc) return drop(rc);
+  *out = h;
+  return 0;
+}
+
+void asmc_smc_shard_destroy(asmc_smc_shard* h) {
+  if (!h) return;
+  cudaStreamSynchronize(h->C.stream);
+  delete h;
+}
+
+uint64_t asmc_smc_shard_chunks(const asmc_smc_shard* h) { return h ? h->nch : 0; }
+uint64_t asmc_smc_shard_blocks(const asmc_smc_shard* h) { return h ? h->nblk : 0; }
+uint64_t asmc_smc_shard_row_bytes(const asmc_smc_shard* h) { return h ? h->row_bytes : 0; }
+
+int asmc_smc_shard_step(asmc_smc_shard* h, int32_t t, asmc_logacc* partials_dev) {
+  if (!h || !partials_dev) return fail(ASMC_ERR_INVALID_ARGUMENT, "null shard or partials");
+  if (t != h->t_done + 1 || t > h->T || h->resampling)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "shard step %d out of order (last completed %d)", t, h->t_done);
+  cudaStream_t s = h->C.stream;
+  PassArgs A = h->A;
+  A.mode = kModeSmcStep;
+  A.t_begin = A.t_end = t;
+  A.row_base = t;
+  LCH(launch_pass(h->ex, h->L, A, h->nblk, s));
+  LCH(launch_fold_chunks(h->part.p, h->nblk, h->nblk, 0, 1, kNAcc, h->nch, h->chunk.p, s));
+  LCH(launch_chunk_major(h->chunk.p, h->nch, reinterpret_cast<LogAcc*>(partials_dev), s));
+  return 0;
+}
+
+int asmc_smc_shard_decide(asmc_smc_shard* h, int32_t t, const asmc_logacc* all_dev, uint64_t all_chunks,
+                          double* btot_dev, int32_t* resample) {
+  if (!h || !all_dev || !btot_dev || !resample) return fail(ASMC_ERR_INVALID_ARGUMENT, "null argument");
+  if (t != h->t_done + 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "decide for step %d out of order", t);
+  if (all_chunks != asmc_fold_chunks(0, h->n))
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "expected %llu chunk partials, got %llu",
+                (unsigned long long)asmc_fold_chunks(0, h->n), (unsigned long long)all_chunks);
+  cudaStream_t s = h->C.stream;
+  LCH(launch_fold_chunk_major(reinterpret_cast<const LogAcc*>(all_dev), all_chunks, h->tot.p, s));
+  LCH(launch_smc_decide(h->tot.p, t, h->T, h->n, h->policy, h->rho, h->seed, h->round, h->ex.rng,
+                        h->R.rd.p, s));
+  LCH(launch_cdf_blocks(h->lw.p, h->n_local, h->R.st.p, h->cum.p, btot_dev, s));
+  SmcState st;
+  CU(cudaMemcpyAsync(&st, h->R.st.p, sizeof st, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  TRY(device_error(st.err, st.err_step, st.err_val));
+  h->t_done = t;
+  h->resampling = st.resample_now;
+  *resample = st.resample_now;
+  return 0;
+}
+
+int asmc_smc_shard_plan(asmc_smc_shard* h, double* all_btot_dev, uint64_t all_blocks, int32_t world,
+                        const uint64_t* shard_p_begin, uint64_t* slot_begin) {
+  if (!h || !all_btot_dev || !shard_p_begin || !slot_begin)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "null argument");
+  if (!h->resampling) return fail(ASMC_ERR_INVALID_ARGUMENT, "plan without a resampling decision");
+  if (world < 1 || world > 1023) return fail(ASMC_ERR_INVALID_ARGUMENT, "world size must be in [1, 1023]");
+  if (all_blocks != nblocks(h->n))
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "expected %llu block totals, got %llu",
+                (unsigned long long)nblocks(h->n), (unsigned long long)all_blocks);
+  if (shard_p_begin[0] != 0 || shard_p_begin[world] != h->n)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "shard boundaries must span [0, n_particles)");
+  h->me = -1;
+  std::vector<uint64_t> rb(world + 1);
+  for (int r = 0; r <= world; ++r) {
+    if (r < world && (shard_p_begin[r] > shard_p_begin[r + 1] || shard_p_begin[r] % ASMC_FOLD_CHUNK))
+      return fail(ASMC_ERR_INVALID_ARGUMENT, "shard boundaries must be ordered multiples of ASMC_FOLD_CHUNK");
+    rb[r] = nblocks(shard_p_begin[r]);
+    if (r < world && shard_p_begin[r] == h->p_begin && shard_p_begin[r + 1] == h->p_begin + h->n_local) h->me = r;
+  }
+  if (h->me < 0) return fail(ASMC_ERR_INVALID_ARGUMENT, "this shard's range is not among the shard boundaries");
+  cudaStream_t s = h->C.stream;
+  if (!h->rank_blk.p || (int)h->slots.size() != world + 1) {
+    h->rank_blk.~DBuf();
+    new (&h->rank_blk) DBuf<uint64_t>();
+    h->slot_dev.~DBuf();
+    new (&h->slot_dev) DBuf<uint64_t>();
+    TRY(h->rank_blk.alloc(world + 1, s));
+    TRY(h->slot_dev.alloc(world + 1, s));
+    h->slots.assign(world + 1, 0);
+  }
+  CU(cudaMemcpyAsync(h->rank_blk.p, rb.data(), sizeof(uint64_t) * (world + 1), cudaMemcpyHostToDevice, s));
+  LCH(launch_shard_plan(all_btot_dev, all_blocks, h->cum.p, h->n_local, nblocks(h->p_begin), h->rank_blk.p,
+                        world, h->n, h->R.st.p, h->slot_dev.p, s));
+  g_launches += 2;
+  CU(cudaMemcpyAsync(h->slots.data(), h->slot_dev.p, sizeof(uint64_t) * (world + 1), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  std::memcpy(slot_begin, h->slots.data(), sizeof(uint64_t) * (world + 1));
+  return 0;
+}
+
+int asmc_smc_shard_pack(asmc_smc_shard* h, void* rows_dev) {
+  if (!h || h->me < 0 || !h->resampling) return fail(ASMC_ERR_INVALID_ARGUMENT, "pack before plan");
+  const uint64_t lo = h->slots[h->me], count = h->slots[h->me + 1] - lo;
+  if (count && !rows_dev) return fail(ASMC_ERR_INVALID_ARGUMENT, "null row buffer");
+  cudaStream_t s = h->C.stream;
+  if (count > h->anc_cap) {
+    h->anc.~DBuf();
+    new (&h->anc) DBuf<uint32_t>();
+    TRY(h->anc.alloc(count, s));
+    h->anc_cap = count;
+  }
+  LCH(launch_shard_pack(h->cum.p, h->n_local, h->R.st.p, lo, count, h->n, h->anc.p, h->row_bytes, h->x.p,
+                        rows_dev, h->C.sms, s));
+  if (count) g_launches += 1;
+  return 0;
+}
+
+int asmc_smc_shard_accept(asmc_smc_shard* h, const void* rows_dev) {
+  if (!h || !rows_dev || !h->resampling) return fail(ASMC_ERR_INVALID_ARGUMENT, "accept without a resampling step");
+  cudaStream_t s = h->C.stream;
+  CU(cudaMemcpyAsync(h->x.p, rows_dev, h->n_local * h->row_bytes, cudaMemcpyDeviceToDevice, s));
+  CU(cudaMemsetAsync(h->lw.p, 0, h->n_local * sizeof(double), s));  // engine.cpp:170-172
+  CU(cudaMemsetAsync(&h->R.st.p->resample_now, 0, sizeof(int), s));
+  h->resampling = 0;
+  h->me = -1;
+  return 0;
+}
+
+int asmc_smc_shard_report(asmc_smc_shard* h, asmc_report* out) {
+  if (!h || !out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null argument");
+  if (h->t_done != h->T || h->resampling)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "report before step %d completed", h->T);
+  SmcState st;
+  TRY(copy_round(h->C.stream, h->R, h->T, true, out, &st));
+  TRY(device_error(st.err, st.err_step, st.err_val));
+  out->kernel_applications = h->n * (uint64_t)h->T;
+  return 0;
+}
+
+int asmc_smc_shard_state(asmc_smc_shard* h, void* rows_host, double* lw_host) {
+  if (!h) return fail(ASMC_ERR_INVALID_ARGUMENT, "null shard");
+  cudaStream_t s = h->C.stream;
+  if (rows_host)
+    CU(cudaMemcpyAsync(rows_host, h->x.p, h->n_local * h->row_bytes, cudaMemcpyDeviceToHost, s));
+  if (lw_host) CU(cudaMemcpyAsync(lw_host, h->lw.p, h->n_local * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return 0;
+}
+
+}  // extern "C"

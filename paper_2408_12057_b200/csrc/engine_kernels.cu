@@ -659,5 +659,120 @@ cudaError_t launch_ess(const double* lw, uint64_t n, double* out, int* err, cuda
   return LAUNCH_OK();
 }
 
-}  // namespace asmcdev
+// ------------------------------------------------------ sharded SSMC --
+// Exchange layout of the per-step fold partials: chunk-major [c][kNAcc], so the
+// rank-ordered concatenation of every shard's chunks is the global chunk order.
+__global__ void chunk_major_kernel(const LogAcc* in, uint64_t nch, LogAcc* out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nch * kNAcc) return;
+  const uint64_t c = i / kNAcc;
+  const int a = (int)(i % kNAcc);
+  out[i] = in[(size_t)a * nch + c];
+}
 
+// Same merge sequence as fold_chunks_final_kernel (chunks 0..C-1 from empty):
+// the all-gathered partials fold to the single-GPU totals bit for bit.
+__global__ void fold_chunk_major_kernel(const LogAcc* in, uint64_t nch, LogAcc* tot) {
+  const int a = threadIdx.x;
+  if (a >= kNAcc) return;
+  LogAcc acc = (a == kAccTop2) ? LogAcc{kNegInf, kNegInf} : lacc_empty();
+  for (uint64_t c = 0; c < nch; ++c) acc_merge(a, acc, in[c * kNAcc + a]);
+  tot[a] = acc;
+}
+
+// pos_m of engine.cpp:68-70, in the operation order of ancestor_kernel
+__device__ __forceinline__ double slot_pos(uint64_t m, double u, uint64_t n, double total) {
+  return __dmul_rn(__ddiv_rn(__dadd_rn((double)m, u), (double)n), total);
+}
+
+// Output slot m lands in shard r's particles iff cum[p_r - 1] < pos_m <= cum[p_{r+1} - 1];
+// cum[p_r - 1] equals the exclusive block offset boff[rank_blk[r]] (same dadd of the
+// same two operands), so every rank derives the same slot ranges from the scan.
+__global__ void shard_bounds_kernel(const double* boff, uint64_t nblk_all, const uint64_t* rank_blk,
+                                    int world, uint64_t n, const SmcState* st, uint64_t* slot_begin) {
+  const int r = threadIdx.x;
+  if (r > world) return;
+  if (r == 0) { slot_begin[0] = 0; return; }
+  if (r == world) { slot_begin[world] = n; return; }
+  const double total = st->total, u = st->u;
+  const double thr = rank_blk[r] < nblk_all ? boff[rank_blk[r]] : total;
+  uint64_t lo = 0, hi = n;  // first m with pos_m > thr (pos is non-decreasing in m)
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (slot_pos(mid, u, n, total) <= thr) lo = mid + 1;
+    else hi = mid;
+  }
+  slot_begin[r] = lo;
+}
+
+__global__ void shard_ancestor_kernel(const double* cum, uint64_t n_local, const SmcState* st,
+                                      uint64_t slot_lo, uint64_t count, uint64_t n, uint32_t* anc) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double pos = slot_pos(slot_lo + i, st->u, n, st->total);
+  uint64_t lo = 0, hi = n_local;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (cum[mid] < pos) lo = mid + 1;
+    else hi = mid;
+  }
+  anc[i] = (uint32_t)(lo < n_local ? lo : n_local - 1);
+}
+
+__global__ void pack_rows_kernel(const uint32_t* anc, uint64_t count, uint64_t row_bytes,
+                                 const char* src, char* dst) {
+  if (row_bytes % 16 == 0) {
+    const uint64_t vec = row_bytes / 16, total = count * vec;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t m = i / vec, v = i % vec;
+      ((uint4*)(dst + m * row_bytes))[v] = ((const uint4*)(src + (uint64_t)anc[m] * row_bytes))[v];
+    }
+  } else {
+    const uint64_t w4 = row_bytes / 4, total = count * w4;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+      const uint64_t m = i / w4, v = i % w4;
+      ((uint32_t*)(dst + m * row_bytes))[v] = ((const uint32_t*)(src + (uint64_t)anc[m] * row_bytes))[v];
+    }
+  }
+}
+
+cudaError_t launch_chunk_major(const LogAcc* in, uint64_t nch, LogAcc* out, cudaStream_t s) {
+  const uint64_t n = nch * kNAcc;
+  chunk_major_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(in, nch, out);
+  return LAUNCH_OK();
+}
+
+cudaError_t launch_fold_chunk_major(const LogAcc* in, uint64_t nch, LogAcc* tot, cudaStream_t s) {
+  fold_chunk_major_kernel<<<1, 32, 0, s>>>(in, nch, tot);
+  return LAUNCH_OK();
+}
+
+cudaError_t launch_cdf_blocks(const double* lw, uint64_t n, const SmcState* st, double* cum,
+                              double* btot, cudaStream_t s) {
+  cdf_block_kernel<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(lw, n, st, cum, btot);
+  return LAUNCH_OK();
+}
+
+cudaError_t launch_shard_plan(double* btot_all, uint64_t nblk_all, double* cum, uint64_t n_local,
+                              uint64_t blk_begin, const uint64_t* rank_blk, int world, uint64_t n,
+                              SmcState* st, uint64_t* slot_begin, cudaStream_t s) {
+  cdf_scan_kernel<<<1, 1024, 0, s>>>(btot_all, nblk_all, st);
+  if (n_local)
+    cdf_offset_kernel<<<(unsigned)((n_local + 255) / 256), 256, 0, s>>>(cum, btot_all + blk_begin, n_local, st);
+  shard_bounds_kernel<<<1, 1024, 0, s>>>(btot_all, nblk_all, rank_blk, world, n, st, slot_begin);
+  return LAUNCH_OK();
+}
+
+cudaError_t launch_shard_pack(const double* cum, uint64_t n_local, const SmcState* st,
+                              uint64_t slot_lo, uint64_t count, uint64_t n, uint32_t* anc,
+                              uint64_t row_bytes, const void* x, void* dst, int sms, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  shard_ancestor_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(cum, n_local, st, slot_lo,
+                                                                       count, n, anc);
+  pack_rows_kernel<<<sms * 8, 256, 0, s>>>(anc, count, row_bytes, (const char*)x, (char*)dst);
+  return LAUNCH_OK();
+}
+
+}  // namespace asmcdev

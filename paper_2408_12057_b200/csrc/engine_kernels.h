@@ -64,4 +64,24 @@ cudaError_t launch_rng(int rng, int what, int precision, const uint64_t key[5], 
 cudaError_t launch_peak_normals(int blocks, uint64_t quads_per_thread, float* sink, cudaStream_t s);
 cudaError_t launch_ess(const double* lw, uint64_t n, double* out, int* err, cudaStream_t s);
 
+// ---- sharded SSMC (one particle shard per GPU) ----
+// per-shard chunk partials [a][c] -> exchange layout [c][a]
+cudaError_t launch_chunk_major(const LogAcc* in, uint64_t nch, LogAcc* out, cudaStream_t s);
+// sequential fold of [C][a] chunk partials into tot[a] (== fold_chunks_final order)
+cudaError_t launch_fold_chunk_major(const LogAcc* in, uint64_t nch, LogAcc* tot, cudaStream_t s);
+// local block CDF (no-op unless st->resample_now)
+cudaError_t launch_cdf_blocks(const double* lw, uint64_t n, const SmcState* st, double* cum,
+                              double* btot, cudaStream_t s);
+// scan the all-gathered block totals (in place -> exclusive offsets, st->total),
+// shift the local CDF by this shard's offsets, and find every shard's output-slot
+// range: slot_begin[r] = #{m : pos_m <= boff[rank_blk[r]]}
+cudaError_t launch_shard_plan(double* btot_all, uint64_t nblk_all, double* cum, uint64_t n_local,
+                              uint64_t blk_begin, const uint64_t* rank_blk, int world, uint64_t n,
+                              SmcState* st, uint64_t* slot_begin, cudaStream_t s);
+// ancestors of output slots [slot_lo, slot_lo + count) within the local CDF,
+// rows gathered into dst in slot order
+cudaError_t launch_shard_pack(const double* cum, uint64_t n_local, const SmcState* st,
+                              uint64_t slot_lo, uint64_t count, uint64_t n, uint32_t* anc,
+                              uint64_t row_bytes, const void* x, void* dst, int sms, cudaStream_t s);
+
 }  // namespace asmcdev

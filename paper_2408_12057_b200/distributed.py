@@ -112,3 +112,175 @@ def io_bytes(ts):
     h2d = 16 + SIZEOF_ROUNDDEV * len(ts)
     d2h = 4 + sum(6 * 8 * (t + 1) + (t + 1) + 4 * (t + 1) + 16 + SIZEOF_SMCSTATE for t in ts)
     return h2d, d2h
+
+
+# ------------------------------------------------------------------ SSMC
+# Multi-GPU run_smc (engine.cpp:97-188).  Shards are the fold-chunk
+# ranges of chunk_partition.  Per step every shard all-gathers the chunk partials
+# (6 accumulators x 16 B per 262144 particles) and folds them in chunk order, so
+# ESS, the resampling decision and the uniform are the same on every rank and
+# equal to the single-GPU run.  On a resampling event:
+#   * block CDF totals (8 B per 256 particles) are all-gathered and scanned
+#     redundantly, giving each shard the global offset of its CDF;
+#   * output slot m's ancestor lies in shard r iff cum[p_r - 1] < pos_m <= cum[p_{r+1} - 1],
+#     so shard r computes the ancestors of one contiguous slot range and packs their
+#     rows in slot order;
+#   * one all-to-all-v moves each packed row to the shard owning its slot.
+# Weight mass that stays balanced across shards keeps most rows on their GPU
+# (the self part of the all-to-all is a local copy).
+
+class VirtualComm:
+    """All shards in this process (one GPU, or a CPU test): collectives are
+    concatenations and slices, in the same rank order NCCL would use."""
+
+    def __init__(self, world):
+        self.world = world
+
+    def allgather(self, tensors, counts):
+        import torch
+        cat = torch.cat(list(tensors), 0)
+        return [cat] + [cat.clone() for _ in tensors[1:]]  # one buffer per rank, as NCCL delivers
+
+    def alltoall(self, sends, send_splits, recv_splits):
+        import torch
+        offs = [np.concatenate([[0], np.cumsum(s)]).astype(int) for s in send_splits]
+        out = []
+        for q in range(self.world):
+            parts = [sends[r][offs[r][q]:offs[r][q + 1]] for r in range(self.world)]
+            out.append(torch.cat(parts, 0))
+        return out
+
+
+class TorchComm:
+    """One shard per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, rank, world, group=None):
+        self.rank, self.world, self.group = rank, world, group
+
+    def allgather(self, tensors, counts):
+        import torch
+        import torch.distributed as dist
+        (x,) = tensors
+        cmax = max(max(counts), 1)
+        buf = torch.zeros((cmax,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        buf[: x.shape[0]] = x
+        outs = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(outs, buf, group=self.group)
+        return [torch.cat([o[:c] for o, c in zip(outs, counts)], 0)]
+
+    def alltoall(self, sends, send_splits, recv_splits):
+        import torch
+        import torch.distributed as dist
+        (x,), (ss,), (rs,) = sends, send_splits, recv_splits
+        recv = torch.empty((int(sum(rs)),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        dist.all_to_all_single(recv, x, [int(v) for v in rs], [int(v) for v in ss], group=self.group)
+        return [recv]
+
+
+def _overlap(a0, a1, b0, b1):
+    return max(0, min(a1, b1) - max(a0, b0))
+
+
+def exchange_splits(slots, bounds):
+    """send[r][q] = rows shard r packs for shard q: |[slots[r], slots[r+1]) & [bounds[q], bounds[q+1])|."""
+    G = len(bounds) - 1
+    return [[_overlap(slots[r], slots[r + 1], bounds[q], bounds[q + 1]) for q in range(G)]
+            for r in range(G)]
+
+
+class DeviceShard:
+    """Tensor-facing adapter over capi.SmcShard (device buffers by data_ptr)."""
+
+    def __init__(self, shard, device):
+        self.s, self.device = shard, device
+        self.chunks, self.blocks, self.row_bytes = shard.chunks, shard.blocks, shard.row_bytes
+        self.T = shard.T
+
+    def step(self, t, partials):
+        self.s.step(t, partials.data_ptr())
+
+    def decide(self, t, all_partials, block_totals):
+        return self.s.decide(t, all_partials.data_ptr(), all_partials.shape[0], block_totals.data_ptr())
+
+    def plan(self, all_block_totals, bounds):
+        return self.s.plan(all_block_totals.data_ptr(), all_block_totals.shape[0], bounds)
+
+    def pack(self, rows):
+        self.s.pack(rows.data_ptr())
+
+    def accept(self, rows):
+        self.s.accept(rows.data_ptr())
+
+    def report(self):
+        return self.s.report()
+
+
+def run_smc_sharded(shards, ranks, comm, bounds, stats=None, nacc=abi.SHARD_NACC,
+                    chunk=abi.FOLD_CHUNK, block=abi.BLOCK):
+    """Drive local shards (one per process with TorchComm; all of them with
+    VirtualComm) through steps 1..T in lockstep; returns each shard's report.
+
+    shards[i] owns particles [bounds[ranks[i]], bounds[ranks[i]+1]).  `stats`
+    (dict, optional) collects per-step exchange volumes for the bench."""
+    import torch
+    G = len(bounds) - 1
+    T = shards[0].T
+    dev = shards[0].device
+    n_chunks = [chunks_of((bounds[r], bounds[r + 1]), chunk) for r in range(G)]
+    n_blocks = [-(-(bounds[r + 1] - bounds[r]) // block) for r in range(G)]
+    parts = [torch.empty((s.chunks, nacc, 2), dtype=torch.float64, device=dev) for s in shards]
+    btots = [torch.empty((max(s.blocks, 1),), dtype=torch.float64, device=dev) for s in shards]
+    for t in range(1, T + 1):
+        for s, p in zip(shards, parts):
+            s.step(t, p)
+        allp = comm.allgather(parts, n_chunks)
+        flags = [s.decide(t, a, b) for s, a, b in zip(shards, allp, btots)]
+        if not flags[0]:
+            continue
+        allb = comm.allgather([b[: s.blocks] for s, b in zip(shards, btots)], n_blocks)
+        slots = [s.plan(a, bounds) for s, a in zip(shards, allb)]
+        splits = exchange_splits(slots[0], bounds)
+        sends = []
+        for s, r, sl in zip(shards, ranks, slots):
+            rows = torch.empty((sl[r + 1] - sl[r], s.row_bytes), dtype=torch.uint8, device=dev)
+            s.pack(rows)
+            sends.append(rows)
+        recvs = comm.alltoall(sends, [splits[r] for r in ranks],
+                              [[splits[q][r] for q in range(G)] for r in ranks])
+        for s, rows in zip(shards, recvs):
+            s.accept(rows)
+        if stats is not None:
+            moved = sum(splits[r][q] for r in range(G) for q in range(G) if q != r)
+            stats.setdefault("rows_moved", []).append(moved)
+    return [s.report() for s in shards]
+
+
+
+def run_smc_multi(target, kernel, betas, n, policy=abi.POLICY_ADAPTIVE_ESS, rho=0.5, seed=0, round=0,
+                  exec_=None, comm=None, rank=0, world=1, return_state=False, stats=None):
+    """Multi-GPU asmc::run_smc: this process's shard(s) on exec_.device.
+
+    comm = TorchComm(rank, world) drives one shard per process (NCCL on the GPU
+    box); comm = None runs all `world` shards in this process (VirtualComm) --
+    the single-GPU proof that the sharded result is bit-identical to asmc_run_smc.
+    All library work and all torch-side buffers/collectives share one CUDA stream."""
+    import torch
+    from . import capi
+    ex = exec_ or abi.execopts(abi.RNG_PHILOX, abi.PREC_FP32)
+    dev = torch.device("cuda", ex.device)
+    stream = torch.cuda.Stream(device=dev)
+    ex = abi.execopts(ex.rng, ex.precision, ex.device, ex.lanes, stream.cuda_stream)
+    bounds = [b for b, _ in chunk_partition(n, world)] + [n]
+    ranks = list(range(world)) if comm is None else [rank]
+    comm = comm or VirtualComm(world)
+    with torch.cuda.device(dev), torch.cuda.stream(stream):
+        shards = [DeviceShard(capi.SmcShard(target, kernel, betas, n, bounds[r], bounds[r + 1], policy,
+                                            rho, seed, round, ex), dev) for r in ranks]
+        reps = run_smc_sharded(shards, ranks, comm, bounds, stats=stats)
+        if return_state:
+            for rep, s in zip(reps, shards):
+                rep["x"], rep["log_w"] = s.s.state()
+    stream.synchronize()
+    for s in shards:
+        s.s.close()
+    return reps

@@ -1,0 +1,73 @@
+"""Multi-GPU SSMC (asmc_smc_shard_*) on one B200: G shards driven in lockstep by
+paper_2408_12057_b200.distributed with VirtualComm (the collectives become
+concatenations/slices in rank order, exactly what NCCL delivers).  The sharded
+run must be BIT-identical to the single-GPU asmc_run_smc (same fp32/Philox
+execution mode): per-step g0/g1/g2, ESS, resampling times, log Z, ELBO, and the
+final particles themselves for every world size."""
+import numpy as np
+import pytest
+
+from paper_2408_12057_b200 import abi, capi, distributed
+
+pytestmark = pytest.mark.gpu
+
+PH, F32 = abi.RNG_PHILOX, abi.PREC_FP32
+N = 2 * abi.FOLD_CHUNK + 12345
+KEYS = ("log_g0", "log_g1", "log_g2", "ess_trace", "cum_log_z", "resample_times", "resampled")
+
+
+def _same(a, b):
+    for k in KEYS:
+        assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+    assert a["log_z_hat"] == b["log_z_hat"] and a["elbo_hat"] == b["elbo_hat"]
+
+
+@pytest.mark.parametrize("policy", [abi.POLICY_ALWAYS, abi.POLICY_ADAPTIVE_ESS])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_ssmc_bit_identical_to_single_gpu(policy, world):
+    tg = abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 8)
+    k = abi.kernel(abi.KERNEL_RWMH, (0.1, 1.0, 10.0), 1)
+    betas = np.linspace(0, 1, 7)
+    ex = abi.execopts(PH, F32)
+    ref = capi.run_smc(tg, k, betas, N, policy=policy, seed=5, round=2, exec_=ex)
+    reps = distributed.run_smc_multi(tg, k, betas, N, policy=policy, seed=5, round=2, exec_=ex,
+                                     world=world)
+    assert len(ref["resample_times"]) > 0
+    for r in reps:
+        _same(r, ref)
+
+
+def test_sharded_particles_identical_across_world_sizes():
+    tg = abi.scale_gaussian(1.0, 2.0, 20)
+    k = abi.kernel(abi.KERNEL_RWMH, (0.1, 0.5, 1.0), 1)
+    betas = np.linspace(0, 1, 6)
+    ex = abi.execopts(PH, F32)
+    stats = {}
+    one = distributed.run_smc_multi(tg, k, betas, N, policy=abi.POLICY_ALWAYS, seed=3, exec_=ex,
+                                    world=1, return_state=True)
+    three = distributed.run_smc_multi(tg, k, betas, N, policy=abi.POLICY_ALWAYS, seed=3, exec_=ex,
+                                      world=3, return_state=True, stats=stats)
+    x1 = one[0]["x"]
+    x3 = np.concatenate([r["x"] for r in three])
+    assert x1.shape == (N, 20) and np.array_equal(x1, x3)
+    assert np.array_equal(one[0]["log_w"], np.concatenate([r["log_w"] for r in three]))
+    assert len(stats["rows_moved"]) == 5  # one exchange per step (policy always)
+    _same(one[0], three[2])
+
+
+def test_shard_api_rejects_misuse():
+    tg = abi.gaussian_shift(0.0, 1.0, 1.0, 4)
+    k = abi.kernel(abi.KERNEL_RWMH)
+    ex = abi.execopts(PH, F32)
+    with pytest.raises(capi.AsmcError) as e:
+        capi.SmcShard(tg, k, [0.0, 1.0], 1000, 10, 1000, exec_=ex)
+    assert "multiple of ASMC_FOLD_CHUNK" in e.value.msg
+    with pytest.raises(capi.AsmcError) as e:
+        capi.SmcShard(tg, k, [0.0, 1.0], 1000, 0, 1000, exec_=abi.execopts(abi.RNG_XOSHIRO, abi.PREC_FP64))
+    assert e.value.code == abi.ERR_CAPABILITY
+    s = capi.SmcShard(tg, k, [0.0, 0.5, 1.0], 1000, 0, 1000, exec_=ex)
+    with pytest.raises(capi.AsmcError):
+        s.step(2, 0)  # out of order
+    with pytest.raises(capi.AsmcError):
+        s.report()  # before the last step
+    s.close()
