@@ -65,6 +65,13 @@ extern "C" {
  * sum_i y_i x_i.theta - softplus(x_i.theta); p = {sigma_p, n}; data = X (n x dim), y (n).
  * Device path: rng = philox, precision = fp32, likelihood on tcgen05 (split-bf16). */
 #define ASMC_TARGET_LOGISTIC 3
+/* Relaxed Ising model on an L x L torus, config 5 (new): spins marginalised by the
+ * Hubbard-Stratonovich transform, coordinates y in R^{L*L} (i = a L + b), A = delta I +
+ * K (Adj + 4 I), u = A y, log p(y) = sum_i -y_i u_i / 2 + log 2cosh(u_i);
+ * eta = N(0, sigma^2 I), V = log p - log eta; p = {L, K, delta, sigma}, dim = L * L.
+ * Z(1) = (2 pi)^{n/2} |A|^{-1/2} e^{(delta + 4K) n / 2} Z_Ising(K) (Kaufman, exact).
+ * Device path: rng = philox, precision = fp32, L in {8, 16, 32, 64}; rwmh_cycle, hmc, identity. */
+#define ASMC_TARGET_ISING 4
 
 /* ---- forward kernels (include/asmc/kernel.hpp:11-27) ---- */
 #define ASMC_KERNEL_IDEALIZED 0

@@ -135,6 +135,45 @@ class LogisticTarget final : public asmc::AnnealedTarget {
   const float* y_;
 };
 
+// Config-5 plugin: relaxed Ising model on an L x L torus (include/asmc_b200.h,
+// ASMC_TARGET_ISING): y in R^{L^2}, u = A y, A = delta I + K (Adj + 4 I),
+// V = sum_i -y_i u_i / 2 + log 2cosh(u_i) - log N(y_i; 0, sigma).
+class IsingTarget final : public asmc::AnnealedTarget {
+ public:
+  IsingTarget(int L, double K, double delta, double sigma)
+      : L_(L), K_(K), c_(delta + 4.0 * K), sigma_(sigma) {
+    if (L < 3 || !(K >= 0.0) || !(delta > 0.0) || !(sigma > 0.0))
+      throw std::invalid_argument("ising needs L >= 3, K >= 0, delta > 0, sigma > 0");
+  }
+  std::size_t dim() const override { return static_cast<std::size_t>(L_) * L_; }
+  double log_reference(std::span<const double> x) const override {
+    double acc = 0.0;
+    for (double xi : x) acc += asmc::log_normal_pdf(xi, 0.0, sigma_);
+    return acc;
+  }
+  double potential(std::span<const double> y) const override {
+    double acc = 0.0;
+    for (int a = 0; a < L_; ++a)
+      for (int b = 0; b < L_; ++b) {
+        const double nb = (y[((a + L_ - 1) % L_) * L_ + b] + y[((a + 1) % L_) * L_ + b]) +
+                          (y[a * L_ + (b + L_ - 1) % L_] + y[a * L_ + (b + 1) % L_]);
+        const double yi = y[a * L_ + b];
+        const double u = c_ * yi + K_ * nb;
+        const double au = std::fabs(u);
+        acc += -0.5 * yi * u + (au + std::log1p(std::exp(-2.0 * au))) - asmc::log_normal_pdf(yi, 0.0, sigma_);
+      }
+    return acc;
+  }
+  void sample_reference(asmc::rng::Stream& stream, std::span<double> out) const override {
+    check_point(out);
+    for (double& xi : out) xi = sigma_ * stream.normal();
+  }
+
+ private:
+  int L_;
+  double K_, c_, sigma_;
+};
+
 std::unique_ptr<asmc::AnnealedTarget> make_target(const asmc_target_desc* t) {
   if (!t) throw std::invalid_argument("null target descriptor");
   const double* p = t->p;
@@ -148,6 +187,8 @@ std::unique_ptr<asmc::AnnealedTarget> make_target(const asmc_target_desc* t) {
     case ASMC_TARGET_LOGISTIC:
       return std::make_unique<LogisticTarget>(p[0], static_cast<std::size_t>(p[1]), t->dim,
                                               static_cast<const float*>(t->data));
+    case ASMC_TARGET_ISING:
+      return std::make_unique<IsingTarget>(static_cast<int>(p[0]), p[1], p[2], p[3]);
   }
   throw asmc::capability_error("unknown target kind " + std::to_string(t->kind));
 }

@@ -230,6 +230,12 @@ static int check_target(const asmc_target_desc* t) {
       if (!t->data || t->data_bytes < (uint64_t)p[1] * (t->dim + 1) * sizeof(float))
         FAIL(ASMC_ERR_INVALID_ARGUMENT, "logistic target needs X (n x dim) and y (n) data");
       break;
+    case ASMC_TARGET_ISING:
+      if (!(p[0] >= 3.0 && p[0] == floor(p[0]) && t->dim == (uint64_t)p[0] * (uint64_t)p[0]))
+        FAIL(ASMC_ERR_INVALID_ARGUMENT, "ising target needs an integer side L >= 3 and dim = L * L");
+      if (!(p[1] >= 0.0 && p[2] > 0.0 && p[3] > 0.0))
+        FAIL(ASMC_ERR_INVALID_ARGUMENT, "ising needs K >= 0, delta > 0, sigma > 0");
+      break;
     default:
       FAIL(ASMC_ERR_CAPABILITY, "unknown target kind %d", t->kind);
   }
@@ -253,12 +259,53 @@ static double logistic_potential(const asmc_target_desc* t, const double* th) {
   return acc;
 }
 
-/* target.cpp:65-69, 133-137 and the scale / logistic plugins (oracle/ref_harness.cpp) */
+/* NEW plugin (config 5): relaxed Ising on an L x L torus (include/asmc_b200.h).
+ * u = A y with A = delta I + K (Adj + 4 I), neighbour sum grouped (a-1 + a+1) + (b-1 + b+1). */
+static void ising_stencil(const asmc_target_desc* t, const double* y, double* u) {
+  const int L = (int)t->p[0];
+  const double K = t->p[1], c = t->p[2] + 4.0 * t->p[1];
+  for (int a = 0; a < L; ++a)
+    for (int b = 0; b < L; ++b) {
+      const double nb = (y[((a + L - 1) % L) * L + b] + y[((a + 1) % L) * L + b]) +
+                        (y[a * L + (b + L - 1) % L] + y[a * L + (b + 1) % L]);
+      u[a * L + b] = c * y[a * L + b] + K * nb;
+    }
+}
+
+static double log2cosh(double u) {
+  const double a = fabs(u);
+  return a + log1p(exp(-2.0 * a));
+}
+
+/* V = sum_i -y_i u_i / 2 + log 2cosh(u_i) - log N(y_i; 0, sigma) */
+static double ising_potential(const asmc_target_desc* t, const double* y) {
+  const uint64_t n = t->dim;
+  double* u = malloc(n * sizeof(double));
+  ising_stencil(t, y, u);
+  double acc = 0.0;
+  for (uint64_t i = 0; i < n; ++i) acc += -0.5 * y[i] * u[i] + log2cosh(u[i]) - log_normal_pdf(y[i], 0.0, t->p[3]);
+  free(u);
+  return acc;
+}
+
+/* grad log gamma_beta = beta A (tanh(u) - y) - (1 - beta) y / sigma^2;  work: 2 n doubles */
+static void ising_grad(const asmc_target_desc* t, double beta, const double* y, double* g, double* work) {
+  const uint64_t n = t->dim;
+  double* u = work;
+  double* v = work + n;
+  ising_stencil(t, y, u);
+  for (uint64_t i = 0; i < n; ++i) v[i] = tanh(u[i]) - y[i];
+  ising_stencil(t, v, g);
+  const double is2 = 1.0 / (t->p[3] * t->p[3]);
+  for (uint64_t i = 0; i < n; ++i) g[i] = beta * g[i] - (1.0 - beta) * is2 * y[i];
+}
+
+/* target.cpp:65-69, 133-137 and the scale / logistic / ising plugins (oracle/ref_harness.cpp) */
 static double log_reference(const asmc_target_desc* t, const double* x) {
   double acc = 0.0;
   const double* p = t->p;
   const double mu = t->kind == ASMC_TARGET_GAUSSIAN_SHIFT ? p[0] : 0.0;
-  const double sg = t->kind == ASMC_TARGET_GAUSSIAN_SHIFT ? p[2] : p[0];
+  const double sg = t->kind == ASMC_TARGET_GAUSSIAN_SHIFT ? p[2] : t->kind == ASMC_TARGET_ISING ? p[3] : p[0];
   for (uint64_t i = 0; i < t->dim; ++i) acc += log_normal_pdf(x[i], mu, sg);
   return acc;
 }
@@ -268,6 +315,7 @@ static double potential(const asmc_target_desc* t, const double* x) {
   const double* p = t->p;
   double acc = 0.0;
   if (t->kind == ASMC_TARGET_LOGISTIC) return logistic_potential(t, x);
+  if (t->kind == ASMC_TARGET_ISING) return ising_potential(t, x);
   if (t->kind == ASMC_TARGET_GAUSSIAN_SHIFT) {
     const double a = (p[1] - p[0]) / (p[2] * p[2]);
     const double mid = 0.5 * (p[0] + p[1]);
@@ -302,6 +350,7 @@ static void sample_reference(const asmc_target_desc* t, stream_t* st, double* ou
   const double* p = t->p;
   for (uint64_t i = 0; i < t->dim; ++i) {
     if (t->kind == ASMC_TARGET_GAUSSIAN_SHIFT) out[i] = p[0] + p[2] * normal(st);
+    else if (t->kind == ASMC_TARGET_ISING) out[i] = p[3] * normal(st);
     else out[i] = p[0] * normal(st);
   }
 }
@@ -385,6 +434,15 @@ static double grad_log_gamma(const asmc_target_desc* t, double beta, double xi) 
   return gref + beta * (glm - gref);
 }
 
+/* whole-vector gradient (work: 2 d doubles); separable targets per coordinate */
+static void grad_vec(const asmc_target_desc* t, double beta, const double* x, double* g, double* work) {
+  if (t->kind == ASMC_TARGET_ISING) {
+    ising_grad(t, beta, x, g, work);
+    return;
+  }
+  for (uint64_t i = 0; i < t->dim; ++i) g[i] = grad_log_gamma(t, beta, x[i]);
+}
+
 /* NEW kernel (no reference code): HMC cycling through the step sizes as the
  * leapfrog epsilon, unit mass, `leapfrog` steps per trajectory.  Draw order per
  * trajectory: d momentum normals, then one uniform (as RWMH: kernel.cpp:31-36).
@@ -394,6 +452,8 @@ static void hmc_cycle_move(const asmc_target_desc* t, const asmc_kernel_desc* k,
   const uint64_t d = t->dim;
   double* xp = scratch;
   double* pm = scratch + d;
+  double* g = scratch + 2 * d;
+  double* work = scratch + 3 * d;  /* 2 d */
   double log_gamma_x = log_gamma(t, beta, x);
   for (int sweep = 0; sweep < k->sweeps; ++sweep) {
     for (int si = 0; si < k->n_step_sizes; ++si) {
@@ -405,9 +465,11 @@ static void hmc_cycle_move(const asmc_target_desc* t, const asmc_kernel_desc* k,
       }
       for (uint64_t i = 0; i < d; ++i) xp[i] = x[i];
       for (int l = 0; l < k->leapfrog; ++l) {
-        for (uint64_t i = 0; i < d; ++i) pm[i] += 0.5 * eps * grad_log_gamma(t, beta, xp[i]);
+        grad_vec(t, beta, xp, g, work);
+        for (uint64_t i = 0; i < d; ++i) pm[i] += 0.5 * eps * g[i];
         for (uint64_t i = 0; i < d; ++i) xp[i] += eps * pm[i];
-        for (uint64_t i = 0; i < d; ++i) pm[i] += 0.5 * eps * grad_log_gamma(t, beta, xp[i]);
+        grad_vec(t, beta, xp, g, work);
+        for (uint64_t i = 0; i < d; ++i) pm[i] += 0.5 * eps * g[i];
       }
       double k1 = 0.0;
       for (uint64_t i = 0; i < d; ++i) k1 += pm[i] * pm[i];
@@ -606,7 +668,7 @@ static int run_smc_impl(const asmc_target_desc* tg, const asmc_kernel_desc* k, c
   double* xs = calloc(n * d, sizeof(double));
   double* xb = calloc(n * d, sizeof(double));
   double* lw = calloc(n, sizeof(double));
-  double* scratch = calloc(2 * d, sizeof(double));  /* proposal / HMC (x', p) */
+  double* scratch = calloc(5 * d, sizeof(double));  /* proposal / HMC (x', p, g, work) */
   uint32_t* anc = calloc(n, sizeof(uint32_t));
   int rc = 0;
   /* engine_detail.hpp:91-100 */
@@ -729,7 +791,7 @@ int ora_run_sais_single(const asmc_target_desc* tg, const asmc_kernel_desc* k, c
   step_acc_t* glob = malloc((size_t)(T + 1) * sizeof(step_acc_t));
   step_acc_t* blk = malloc((size_t)(T + 1) * sizeof(step_acc_t));
   double* x = calloc(d, sizeof(double));
-  double* scratch = calloc(2 * d, sizeof(double));  /* proposal / HMC (x', p) */
+  double* scratch = calloc(5 * d, sizeof(double));  /* proposal / HMC (x', p, g, work) */
   for (int t = 0; t <= T; ++t) step_acc_init(&glob[t]);
   int rc = 0;
   const uint64_t nb = block_count(n);
@@ -790,7 +852,7 @@ int ora_trajectory(const asmc_target_desc* tg, const asmc_kernel_desc* k, const 
   TRY(validate_kernel(k));
   TRY(check_target(tg));
   const uint64_t d = tg->dim;
-  double* scratch = calloc(2 * d, sizeof(double));  /* proposal / HMC (x', p) */
+  double* scratch = calloc(5 * d, sizeof(double));  /* proposal / HMC (x', p, g, work) */
   stream_t si;
   stream_init(&si, seed, round, particle, 0, 0);
   sample_reference(tg, &si, x_out);

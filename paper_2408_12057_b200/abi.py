@@ -18,6 +18,7 @@ TARGET_GAUSSIAN_SHIFT = 0
 TARGET_MIXTURE = 1
 TARGET_SCALE_GAUSSIAN = 2
 TARGET_LOGISTIC = 3
+TARGET_ISING = 4
 
 KERNEL_IDEALIZED = 0
 KERNEL_RWMH = 1
@@ -102,6 +103,11 @@ def mixture(ref_sigma, weight, mu1, sigma1, mu2, sigma2, dim=1):
 
 def scale_gaussian(sigma0, sigma1, dim=1):
     return target(TARGET_SCALE_GAUSSIAN, dim, sigma0, sigma1)
+
+
+def ising(L, K, delta=1.0, sigma=1.0):
+    """Config 5: relaxed Ising on an L x L torus (ASMC_TARGET_ISING), coupling K = beta J."""
+    return target(TARGET_ISING, L * L, L, K, delta, sigma)
 
 
 def _bf16_round(a):

@@ -16,6 +16,7 @@
 #include "asmc_b200.h"
 #include "dispatch.h"
 #include "engine_kernels.h"
+#include "ising.h"
 #include "logistic.h"
 
 using namespace asmcdev;
@@ -177,6 +178,15 @@ int check_target(const asmc_target_desc* t) {
           t->data_bytes < (uint64_t)p[1] * (t->dim + 1) * sizeof(float))
         return fail(ASMC_ERR_INVALID_ARGUMENT, "logistic target needs X (n x dim) and y (n) data");
       break;
+    case ASMC_TARGET_ISING: {
+      const int L = (int)p[0];
+      if (!((double)L == p[0] && L >= 3) || t->dim != (uint64_t)L * (uint64_t)L)
+        return fail(ASMC_ERR_INVALID_ARGUMENT, "ising target needs an integer side L >= 3 and dim = L * L");
+      if (!(p[1] >= 0.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "ising coupling must be non-negative");
+      if (!(p[2] > 0.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "ising relaxation delta must be positive");
+      if (!(p[3] > 0.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "reference sigma must be positive");
+      break;
+    }
     default:
       return fail(ASMC_ERR_CAPABILITY, "target kind %d has no device implementation", t->kind);
   }
@@ -190,8 +200,18 @@ int check_target(const asmc_target_desc* t) {
 int check_pair(const asmc_target_desc* t, const asmc_kernel_desc* k) {
   TRY(check_target(t));
   TRY(check_kernel(k));
-  if (k->kind == ASMC_KERNEL_IDEALIZED && t->kind == ASMC_TARGET_MIXTURE)
+  if (k->kind == ASMC_KERNEL_IDEALIZED &&
+      (t->kind == ASMC_TARGET_MIXTURE || t->kind == ASMC_TARGET_ISING || t->kind == ASMC_TARGET_LOGISTIC))
     return fail(ASMC_ERR_CAPABILITY, "idealized_exact kernel requires an exact sampler");
+  return 0;
+}
+
+// entry points built on the fused particle pass only (not the step-outer engines
+// of the data-backed / lattice targets)
+int check_pass_target(const asmc_target_desc* t, const char* what) {
+  if (t->kind == ASMC_TARGET_LOGISTIC || t->kind == ASMC_TARGET_ISING)
+    return fail(ASMC_ERR_CAPABILITY, "%s does not support the %s target yet", what,
+                t->kind == ASMC_TARGET_LOGISTIC ? "logistic" : "ising");
   return 0;
 }
 
@@ -552,6 +572,26 @@ int lg_eval(DevCtx* C, const LgData& D, const LgArgs& A, int mode, const double*
   return 0;
 }
 
+// one lattice-move launch, timed like the particle pass when profiling
+int is_move(DevCtx* C, const IsArgs& A, int mode, const double* betas, int t) {
+  ProfRec rec{};
+  if (g_prof) {
+    cudaEventCreate(&rec.a);
+    cudaEventCreate(&rec.b);
+    cudaEventRecord(rec.a, C->stream);
+  }
+  LCH(launch_is_move(A, mode, betas, t, C->stream));
+  if (g_prof) {
+    cudaEventRecord(rec.b, C->stream);
+    // algorithmic unit: site-gradient evaluations (HMC: leapfrog + 1 per trajectory; RWMH: 1 energy)
+    const double traj = mode == 1 && A.kc.kind != ASMC_KERNEL_IDENTITY ? (double)A.kc.sweeps * A.kc.n_steps : 0.0;
+    const double per = A.kc.kind == ASMC_KERNEL_HMC ? (double)(A.kc.leapfrog + 1) : 1.0;
+    rec.normals = (double)A.L * A.L * (double)A.n_local * (1.0 + traj * per);
+    g_prof_recs.push_back(rec);
+  }
+  return 0;
+}
+
 // run_smc (engine.cpp:97-188) for the logistic target: step-outer because the
 // likelihood of all particles is one GEMM per proposal (SAIS = policy never).
 int enqueue_lg_round(DevCtx* C, const LgData& D, const asmc_target_desc* t, const asmc_kernel_desc* k,
@@ -608,6 +648,110 @@ int enqueue_lg_round(DevCtx* C, const LgData& D, const asmc_target_desc* t, cons
 }
 
 int copy_round(cudaStream_t s, RoundBufs& R, int T, bool smc, asmc_report* out, SmcState* st);
+
+// ------------------------------------------------------ config 5: Ising --
+int is_check(const asmc_target_desc* t, const asmc_kernel_desc* k, const asmc_exec& ex) {
+  if (ex.rng != ASMC_RNG_PHILOX || ex.precision != ASMC_PREC_FP32)
+    return fail(ASMC_ERR_CAPABILITY, "the ising target runs on the fp32 lattice path: rng = philox, precision = fp32");
+  if (!ising_side_supported((int)t->p[0]))
+    return fail(ASMC_ERR_CAPABILITY, "ising device kernels support L in {8, 16, 32, 64}");
+  if (k->kind != ASMC_KERNEL_RWMH && k->kind != ASMC_KERNEL_HMC && k->kind != ASMC_KERNEL_IDENTITY)
+    return fail(ASMC_ERR_CAPABILITY, "ising target supports the rwmh_cycle, hmc and identity kernels");
+  return 0;
+}
+
+IsArgs is_args(const asmc_target_desc* t, const asmc_kernel_desc* k) {
+  IsArgs A;
+  std::memset(&A, 0, sizeof A);
+  const int L = (int)t->p[0];
+  const double n = (double)L * L;
+  A.L = L;
+  A.row = L * L + 4;
+  A.K = (float)t->p[1];
+  A.c = (float)(t->p[2] + 4.0 * t->p[1]);
+  A.inv_s2 = (float)(1.0 / (t->p[3] * t->p[3]));
+  A.sigma = (float)t->p[3];
+  A.vconst = n * (std::log(t->p[3]) + 0.91893853320467274178);
+  A.kc = make_kcfg(k);
+  return A;
+}
+
+// run_smc (engine.cpp:97-188) for the lattice target, step-outer: per step the weight
+// kernel (lg = dbeta V(y), V cached in the state row), fold, decide, one move launch
+// (the whole RWMH / HMC cycle at beta_t per particle), resample + gather.
+int enqueue_is_round(DevCtx* C, const asmc_target_desc* t, const asmc_kernel_desc* k, const double* d_betas,
+                     int T, uint64_t n, int policy, double rho, uint64_t seed, uint64_t round, RoundDev* d_rd,
+                     SmcState* d_st, LgWork& W) {
+  IsArgs I = is_args(t, k);
+  const int row = I.row;
+  const uint64_t nblk = nblocks(n), nchunks = (nblk + kChunkBlocks - 1) / kChunkBlocks;
+  TRY(W.sa.alloc(n * row, C->stream));
+  TRY(W.sb.alloc(n * row, C->stream));
+  TRY(W.sbuf.alloc(2, C->stream));
+  TRY(W.xcur.alloc(1, C->stream));
+  TRY(W.lw.alloc(n, C->stream));
+  TRY(W.cum.alloc(n, C->stream));
+  TRY(W.btot.alloc(nblk, C->stream));
+  TRY(W.anc.alloc(n, C->stream));
+  TRY(W.part.alloc((size_t)kNAcc * nblk, C->stream));
+  TRY(W.chunk.alloc((size_t)kNAcc * nchunks, C->stream));
+  TRY(W.tot.alloc(kNAcc, C->stream));
+  float* ptrs[2] = {W.sa.p, W.sb.p};
+  CU(cudaMemcpyAsync(W.sbuf.p, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemsetAsync(W.xcur.p, 0, sizeof(int), C->stream));
+  CU(cudaMemsetAsync(W.lw.p, 0, n * sizeof(double), C->stream));
+  I.state = W.sbuf.p;
+  I.xcur = W.xcur.p;
+  I.n_local = n;
+  I.seed = seed;
+  I.round = round;
+  I.err = &d_st->err;
+  LgArgs A;  // the weight kernel and gather see the same state-row layout
+  std::memset(&A, 0, sizeof A);
+  A.state = W.sbuf.p;
+  A.xcur = W.xcur.p;
+  A.lw = W.lw.p;
+  A.n_local = n;
+  A.d = I.L * I.L;
+  A.row = row;
+  A.err = &d_st->err;
+  TRY(is_move(C, I, 0, d_betas, 0));  // engine_detail.hpp:91-100 (+ V(y_0))
+  for (int s = 1; s <= T; ++s) {
+    LCH(launch_lg_weight(A, d_betas, s, W.part.p, nblk, C->stream));
+    LCH(launch_fold(false, W.part.p, nblk, nblk, 0, 1, kNAcc, W.chunk.p, W.tot.p, C->stream));
+    LCH(launch_smc_decide(W.tot.p, s, T, n, policy, rho, seed, round, ASMC_RNG_PHILOX, d_rd, C->stream));
+    TRY(is_move(C, I, 1, d_betas, s));  // kernel.cpp:26-63 at beta_t
+    LCH(launch_resample(W.lw.p, n, d_st, W.cum.p, W.btot.p, W.anc.p, C->stream));
+    g_launches += 3;
+    LCH(launch_gather(W.anc.p, n, (uint64_t)row * sizeof(float), reinterpret_cast<void* const*>(W.sbuf.p),
+                      W.xcur.p, W.lw.p, d_st, C->sms, C->stream));
+    g_launches += 1;
+  }
+  return 0;
+}
+
+int run_is_single(const asmc_target_desc* target, const asmc_kernel_desc* kernel, const double* betas, int T,
+                  uint64_t n, int policy, double rho, uint64_t seed, uint64_t round, const asmc_exec& ex,
+                  asmc_report* out, bool smc) {
+  TRY(is_check(target, kernel, ex));
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C, ex.stream));
+  const double t0 = now_s();
+  DBuf<double> d_betas;
+  TRY(d_betas.alloc(T + 1, C->stream));
+  CU(cudaMemcpyAsync(d_betas.p, betas, sizeof(double) * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  RoundBufs R;
+  TRY(R.alloc(T, C->stream));
+  LgWork W;
+  TRY(enqueue_is_round(C, target, kernel, d_betas.p, T, n, policy, rho, seed, round, R.rd.p, R.st.p, W));
+  SmcState st;
+  TRY(copy_round(C->stream, R, T, smc, out, &st));
+  TRY(device_error(st.err, st.err_step, st.err_val));
+  out->kernel_applications = n * (uint64_t)T;
+  out->wall_seconds = now_s() - t0;
+  return 0;
+}
+
 
 // asmc_run_smc / asmc_run_sais_single body for the logistic target
 int run_lg_single(const asmc_target_desc* target, const asmc_kernel_desc* kernel, const double* betas, int T,
@@ -698,6 +842,8 @@ int asmc_run_sais_single(const asmc_target_desc* target, const asmc_kernel_desc*
   const asmc_exec ex = exec ? *exec : default_exec();
   if (target->kind == ASMC_TARGET_LOGISTIC)  // SAIS == run_smc(never) (drivers.hpp:80-86)
     return run_lg_single(target, kernel, betas, T, n, ASMC_POLICY_NEVER, 0.5, seed, round, ex, out, false);
+  if (target->kind == ASMC_TARGET_ISING)
+    return run_is_single(target, kernel, betas, T, n, ASMC_POLICY_NEVER, 0.5, seed, round, ex, out, false);
   Layout L;
   TRY(choose_layout(ex, target->dim, &L, T, 4));
   DevCtx* C;
@@ -733,6 +879,8 @@ int asmc_run_smc(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
   const asmc_exec ex = exec ? *exec : default_exec();
   if (target->kind == ASMC_TARGET_LOGISTIC)
     return run_lg_single(target, kernel, betas, T, n, policy, rho, seed, round, ex, out, true);
+  if (target->kind == ASMC_TARGET_ISING)
+    return run_is_single(target, kernel, betas, T, n, policy, rho, seed, round, ex, out, true);
   Layout L;
   TRY(choose_layout(ex, target->dim, &L));
   DevCtx* C;
@@ -789,8 +937,12 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
   const asmc_exec ex = exec ? *exec : default_exec();
   Layout L;
   const bool lg = target->kind == ASMC_TARGET_LOGISTIC;
+  const bool is = target->kind == ASMC_TARGET_ISING;
   if (lg) {
     TRY(lg_check(target, kernel, ex));
+    L = Layout{1, 0};
+  } else if (is) {
+    TRY(is_check(target, kernel, ex));
     L = Layout{1, 0};
   } else {
     TRY(choose_layout_impl(ex, target->dim, &L));
@@ -837,6 +989,11 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
       TRY(enqueue_lg_round(C, lgd, target, kernel, betas[k].p, ts[k], ns[k],
                            mode == ASMC_MODE_SAIS ? ASMC_POLICY_NEVER : policy, rho, seed,
                            (uint64_t)(k + 1), R[k].rd.p, R[k].st.p, w));
+    } else if (is) {  // config 5: step-outer lattice engine (SAIS = policy never)
+      LgWork w;
+      TRY(enqueue_is_round(C, target, kernel, betas[k].p, ts[k], ns[k],
+                           mode == ASMC_MODE_SAIS ? ASMC_POLICY_NEVER : policy, rho, seed, (uint64_t)(k + 1),
+                           R[k].rd.p, R[k].st.p, w));
     } else if (mode == ASMC_MODE_SAIS) {
       SaisWork w;  // stream-ordered: freed after this round's kernels retire
       TRY(enqueue_sais_round(C, ex, L, base, betas[k].p, ts[k], ns[k], seed, (uint64_t)(k + 1),
@@ -905,6 +1062,7 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
                        uint64_t seed, uint64_t round, const asmc_exec* exec, asmc_logacc* partials) {
   TRY(check_schedule(betas, T));
   TRY(check_pair(target, kernel));
+  TRY(check_pass_target(target, "asmc_sais_partials"));
   if (p_begin % ASMC_FOLD_CHUNK != 0)
     return fail(ASMC_ERR_INVALID_ARGUMENT, "p_begin must be a multiple of ASMC_FOLD_CHUNK");
   if (p_end > n || p_end < p_begin) return fail(ASMC_ERR_INVALID_ARGUMENT, "bad particle range");
@@ -993,6 +1151,7 @@ int asmc_trajectories(const asmc_target_desc* target, const asmc_kernel_desc* ke
                       double* x_out, double* log_w_out) {
   TRY(check_schedule(betas, T));
   TRY(check_pair(target, kernel));
+  TRY(check_pass_target(target, "asmc_trajectories"));
   const asmc_exec ex = exec ? *exec : default_exec();
   Layout L;
   TRY(choose_layout(ex, target->dim, &L, T, 4));
@@ -1289,8 +1448,7 @@ int asmc_smc_shard_create(const asmc_target_desc* target, const asmc_kernel_desc
   if (ex.precision == ASMC_PREC_FP64 || ex.rng != ASMC_RNG_PHILOX)
     return fail(ASMC_ERR_CAPABILITY,
                 "sharded SSMC uses the fp32 tree fold (rng = philox, precision = fp32); the fp64 reference order is single-GPU");
-  if (target->kind == ASMC_TARGET_LOGISTIC)
-    return fail(ASMC_ERR_CAPABILITY, "sharded SSMC does not support the logistic target yet");
+  TRY(check_pass_target(target, "sharded SSMC"));
   auto* h = new asmc_smc_shard;
   auto drop = [&](int rc) { delete h; return rc; };
   int rc = choose_layout(ex, target->dim, &h->L);
