@@ -287,6 +287,42 @@ bool LogisticTarget::device_descriptor(asmc_target_desc* o) const {
   return true;
 }
 
+IsingTarget::IsingTarget(int side, double coupling, double delta, double sigma)
+    : L_(side), K_(coupling), delta_(delta), sigma_(sigma) {
+  if (side < 3) throw std::invalid_argument("ising target needs an integer side L >= 3");
+  if (!(coupling >= 0.0)) throw std::invalid_argument("ising coupling must be non-negative");
+  if (!(delta > 0.0)) throw std::invalid_argument("ising relaxation delta must be positive");
+  if (!(sigma > 0.0)) throw std::invalid_argument("reference sigma must be positive");
+}
+double IsingTarget::log_reference(std::span<const double> x) const {
+  check_point(x);
+  double s = 0.0;
+  for (double v : x) s += log_normal_pdf(v, 0.0, sigma_);
+  return s;
+}
+double IsingTarget::potential(std::span<const double> y) const {
+  check_point(y);
+  const double c = delta_ + 4.0 * K_;
+  double acc = 0.0;
+  for (int a = 0; a < L_; ++a)
+    for (int b = 0; b < L_; ++b) {
+      const double nb = (y[((a + L_ - 1) % L_) * L_ + b] + y[((a + 1) % L_) * L_ + b]) +
+                        (y[a * L_ + (b + L_ - 1) % L_] + y[a * L_ + (b + 1) % L_]);
+      const double yi = y[a * L_ + b], u = c * yi + K_ * nb, au = std::fabs(u);
+      acc += -0.5 * yi * u + (au + std::log1p(std::exp(-2.0 * au))) - log_normal_pdf(yi, 0.0, sigma_);
+    }
+  return acc;
+}
+bool IsingTarget::device_descriptor(asmc_target_desc* o) const {
+  o->kind = ASMC_TARGET_ISING;
+  o->dim = dim();
+  o->p[0] = L_;
+  o->p[1] = K_;
+  o->p[2] = delta_;
+  o->p[3] = sigma_;
+  return true;
+}
+
 // ---- kernel / engine ------------------------------------------------------
 void validate_kernel(const Kernel& k) {  // kernel.cpp:12-22
   if (k.kind == KernelKind::hmc) {

@@ -138,6 +138,22 @@ class LogisticTarget final : public AnnealedTarget {
   double sp_;
 };
 
+// Config-5 plugin (new): relaxed Ising model on an L x L torus (include/asmc_b200.h,
+// ASMC_TARGET_ISING); coordinates y in R^{L*L}, coupling K, relaxation delta, eta = N(0, sigma^2 I).
+class IsingTarget final : public AnnealedTarget {
+ public:
+  IsingTarget(int side, double coupling, double delta = 1.0, double sigma = 1.0);
+  std::size_t dim() const override { return static_cast<std::size_t>(L_) * L_; }
+  double log_reference(std::span<const double> x) const override;
+  double potential(std::span<const double> x) const override;
+  bool device_descriptor(asmc_target_desc* out) const override;
+  int side() const { return L_; }
+
+ private:
+  int L_;
+  double K_, delta_, sigma_;
+};
+
 double log_normal_pdf(double x, double mu, double sigma);
 
 // ---- kernel.hpp -----------------------------------------------------------

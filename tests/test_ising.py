@@ -124,3 +124,19 @@ def test_ising_64_rounds_run_and_reject_bad_modes():
     with pytest.raises(capi.AsmcError) as e:
         capi.run_sais_single(abi.ising(12, KC), k, [0.0, 1.0], 16, exec_=abi.execopts(PH, F32))
     assert e.value.code == abi.ERR_CAPABILITY
+
+
+def test_host_api_ising_target_potential():
+    import paper_2408_12057_b200 as asmc
+    L, K, delta, sigma = 5, KC, 0.7, 1.3
+    t = asmc.IsingTarget(L, K, delta, sigma)
+    y = np.random.default_rng(0).normal(size=L * L)
+    Y = y.reshape(L, L)
+    u = (delta + 4 * K) * Y + K * (np.roll(Y, 1, 0) + np.roll(Y, -1, 0) + np.roll(Y, 1, 1) + np.roll(Y, -1, 1))
+    log_eta = np.sum(-0.5 * (y / sigma) ** 2 - math.log(sigma) - 0.5 * math.log(2 * math.pi))
+    V = np.sum(-0.5 * Y * u + np.logaddexp(u, -u)) - log_eta
+    assert t.dim() == L * L and t.side() == L
+    assert abs(t.potential(y.tolist()) - V) < 1e-10 * abs(V)
+    assert abs(t.log_reference(y.tolist()) - log_eta) < 1e-10 * abs(log_eta)
+    with pytest.raises(ValueError):
+        asmc.IsingTarget(2, K)
