@@ -20,6 +20,8 @@
  *   asmc_smc_shard_*      <- asmc::run_smc split per GPU: step_pass (src/engine_detail.hpp:113-156),
  *                            ess/decide (src/engine.cpp:46-59,82-95,140-160), systematic
  *                            resample + gather (src/engine.cpp:61-80,161-173)
+ *   asmc_run_zja          <- asmc::run_zja            include/asmc/drivers.hpp:88-111, src/drivers.cpp:234-341
+ *   asmc_zja_next_beta    <- asmc::zja_next_beta      include/asmc/schedule.hpp:51-64, src/schedule.cpp:199-264
  *   asmc_systematic_resample <- asmc::systematic_resample  src/engine.cpp:61-80
  *   asmc_ess              <- asmc::ess                src/engine.cpp:46-59
  *   asmc_barrier_estimate <- asmc::barrier_estimate   src/schedule.cpp:41-56
@@ -257,6 +259,41 @@ int asmc_smc_shard_accept(asmc_smc_shard* shard, const void* rows_dev);
 int asmc_smc_shard_report(asmc_smc_shard* shard, asmc_report* out);
 /* parity hook: copy this shard's particles (row-major, row_bytes each) and log-weights */
 int asmc_smc_shard_state(asmc_smc_shard* shard, void* rows_host, double* log_w_host);
+
+/* ---- online schedule adaptation (ZJA) ---- */
+/* ZjaOptions (drivers.hpp:88-97) */
+typedef struct asmc_zja_opts {
+  uint64_t n_particles;
+  int32_t target_steps; /* K: pilot resolution when delta_star == 0 */
+  int32_t max_steps;
+  double delta_star;    /* 0 -> pilot round sets (Lambda_hat / K)^2 */
+  uint64_t seed;
+} asmc_zja_opts;
+
+/* ZjaOutcome (drivers.hpp:99-104).  Main-round arrays have `capacity` entries
+ * (>= steps + 1); pilot arrays target_steps + 1.  Any array may be NULL. */
+typedef struct asmc_zja_out {
+  int32_t capacity;  /* in */
+  int32_t steps;     /* out: adaptive run's T */
+  int32_t pilot_ran; /* out: 1 when delta_star == 0 (pilot = round 1, main = round 2) */
+  int32_t warning;   /* out: the non-monotone bisection fallback was taken */
+  double delta_star; /* out: threshold used */
+  double* betas;     /* main schedule */
+  double* lambda;    /* main barrier estimate */
+  asmc_report main;
+  double* pilot_lambda;
+  asmc_report pilot;
+} asmc_zja_out;
+
+/* Device path: one probe = a log-sum-exp over the particles with log eta and V
+ * cached per particle.  precision fp64: the reference's sequential accumulation
+ * (one device thread); fp32: the whole bisection in one cooperative launch. */
+int asmc_run_zja(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                 const asmc_zja_opts* options, const asmc_exec* exec, asmc_zja_out* out);
+/* positions: n x dim row-major (host) */
+int asmc_zja_next_beta(const asmc_target_desc* target, double beta, const double* positions,
+                       uint64_t n_particles, const double* log_weights, double delta_star,
+                       double tol, const asmc_exec* exec, double* beta_next, int32_t* warning);
 
 /* ---- parity hooks ---- */
 /* key = {seed, round, particle, step, substep} (rng.hpp:11-17) */

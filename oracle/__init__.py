@@ -106,6 +106,21 @@ class Oracle:
                    C.c_double(rho), C.c_uint64(seed), C.c_uint64(round), C.byref(rep))
         return self._finish(rep, bufs)
 
+    def run_zja(self, target, kernel, n, target_steps=32, delta_star=0.0, seed=0, max_steps=100000, workers=1):
+        o = abi.zja_opts(n, target_steps, delta_star, seed, max_steps)
+        out, keep = abi.zja_buffers(o)
+        self._call("ora_run_zja", C.byref(target), C.byref(kernel), C.byref(o), C.c_int32(workers), C.byref(out))
+        return abi.zja_finish(out, keep)
+
+    def zja_next_beta(self, target, beta, positions, log_weights, delta_star, tol=1e-10):
+        x = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1)
+        lw = np.ascontiguousarray(log_weights, dtype=np.float64)
+        nb, w = C.c_double(0.0), C.c_int32(0)
+        self._call("ora_zja_next_beta", C.byref(target), C.c_double(beta), _arr(x, C.c_double),
+                   C.c_uint64(len(lw)), _arr(lw, C.c_double), C.c_double(delta_star), C.c_double(tol),
+                   C.byref(nb), C.byref(w))
+        return nb.value, bool(w.value)
+
     def run_sais_single(self, target, kernel, betas, n, seed=0, round=0, workers=1, chunk=0):
         betas = np.ascontiguousarray(betas, dtype=np.float64)
         T = len(betas) - 1

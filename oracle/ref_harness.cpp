@@ -463,6 +463,49 @@ int ora_analytic_log_z(const asmc_target_desc* target, double beta, double* out)
   return guard([&] { *out = make_target(target)->analytic_log_z(beta); });
 }
 
+// asmc::run_zja (drivers.cpp:234-341) and asmc::zja_next_beta (schedule.cpp:219-264)
+int ora_run_zja(const asmc_target_desc* target, const asmc_kernel_desc* kernel, const asmc_zja_opts* o,
+                int32_t workers, asmc_zja_out* out) {
+  return guard([&] {
+    const auto tg = make_target(target);
+    asmc::ZjaOptions zo;
+    zo.n_particles = o->n_particles;
+    zo.target_steps = o->target_steps;
+    zo.delta_star = o->delta_star;
+    zo.seed = o->seed;
+    zo.workers = workers;
+    zo.max_steps = o->max_steps;
+    const asmc::ZjaOutcome r = asmc::run_zja(*tg, make_kernel(kernel), zo);
+    out->delta_star = r.delta_star;
+    out->warning = r.warning ? 1 : 0;
+    out->pilot_ran = r.rounds.size() == 2 ? 1 : 0;
+    const asmc::RoundResult& m = r.rounds.back();
+    const int T = m.report.schedule.steps();
+    if (T + 1 > out->capacity) throw std::invalid_argument("output capacity too small");
+    out->steps = T;
+    if (out->betas) std::memcpy(out->betas, m.report.schedule.betas.data(), sizeof(double) * (T + 1));
+    if (out->lambda) std::memcpy(out->lambda, m.barrier.lambda.data(), sizeof(double) * (T + 1));
+    fill_report(m.report, &out->main);
+    if (out->pilot_ran) {
+      fill_report(r.rounds[0].report, &out->pilot);
+      if (out->pilot_lambda)
+        std::memcpy(out->pilot_lambda, r.rounds[0].barrier.lambda.data(),
+                    sizeof(double) * r.rounds[0].barrier.lambda.size());
+    }
+  });
+}
+
+int ora_zja_next_beta(const asmc_target_desc* target, double beta, const double* xs, uint64_t n,
+                      const double* lw, double delta, double tol, double* beta_next, int32_t* warning) {
+  return guard([&] {
+    const auto tg = make_target(target);
+    const auto r = asmc::zja_next_beta(*tg, beta, std::span<const double>(xs, n * tg->dim()), n,
+                                       std::span<const double>(lw, n), delta, tol);
+    *beta_next = r.beta_next;
+    if (warning) *warning = r.warning ? 1 : 0;
+  });
+}
+
 int ora_hardware_threads(void) { return static_cast<int>(std::thread::hardware_concurrency()); }
 
 }  // extern "C"

@@ -1153,3 +1153,208 @@ int ora_run_rounds(const asmc_target_desc* tg, const asmc_kernel_desc* k, int32_
 }
 
 int ora_hardware_threads(void) { return 1; }
+
+/* ---------------------------------------------------------------- ZJA -- */
+/* schedule.cpp:201-215 */
+static int zja_dhat(const asmc_target_desc* tg, double beta, double b2, const double* xs, uint64_t n,
+                    const double* lw, double log_m0, double* out) {
+  lacc_t m1 = LACC0, m2 = LACC0;
+  for (uint64_t p = 0; p < n; ++p) {
+    double lg;
+    TRY(log_incremental_weight(tg, beta, b2, xs + p * tg->dim, &lg));
+    lacc_add(&m1, lw[p] + lg);
+    lacc_add(&m2, lw[p] + 2.0 * lg);
+  }
+  const double raw = lacc_total(&m2) - 2.0 * lacc_total(&m1) + log_m0;
+  *out = raw > 0.0 ? raw : 0.0;
+  return 0;
+}
+
+static int zja_bisect(const asmc_target_desc* tg, double beta, const double* xs, uint64_t n, const double* lw,
+                      double log_m0, double delta, double tol, double lo, double hi, double* out) {
+  while (hi - lo > tol) {
+    const double mid = 0.5 * (lo + hi);
+    double dh;
+    TRY(zja_dhat(tg, beta, mid, xs, n, lw, log_m0, &dh));
+    if (dh <= delta) lo = mid;
+    else hi = mid;
+  }
+  *out = lo;
+  return 0;
+}
+
+/* schedule.cpp:219-264 */
+int ora_zja_next_beta(const asmc_target_desc* tg, double beta, const double* xs, uint64_t n, const double* lw,
+                      double delta, double tol, double* beta_next, int32_t* warning) {
+  if (!(beta >= 0.0 && beta < 1.0)) FAIL(ASMC_ERR_DOMAIN, "zja_next_beta requires beta in [0, 1)");
+  if (!(delta > 0.0)) FAIL(ASMC_ERR_INVALID_ARGUMENT, "delta_star must be positive");
+  if (!(tol > 0.0)) FAIL(ASMC_ERR_INVALID_ARGUMENT, "tol must be positive");
+  if (n == 0) FAIL(ASMC_ERR_INVALID_ARGUMENT, "particle arrays inconsistent with n_particles");
+  TRY(check_target(tg));
+  lacc_t m0 = LACC0;
+  for (uint64_t p = 0; p < n; ++p) lacc_add(&m0, lw[p]);
+  const double log_m0 = lacc_total(&m0);
+  if (log_m0 == -INFINITY) FAIL(ASMC_ERR_DEGENERATE, "all log-weights are -inf");
+  if (warning) *warning = 0;
+  double dh;
+  TRY(zja_dhat(tg, beta, 1.0, xs, n, lw, log_m0, &dh));
+  if (dh <= delta) {
+    *beta_next = 1.0;
+    return 0;
+  }
+  double root;
+  TRY(zja_bisect(tg, beta, xs, n, lw, log_m0, delta, tol, beta, 1.0, &root));
+  for (int i = 1; i < 16; ++i) {
+    const double probe = beta + (root - beta) * (double)i / 16;
+    TRY(zja_dhat(tg, beta, probe, xs, n, lw, log_m0, &dh));
+    if (dh > delta * (1.0 + 1e-12)) {
+      if (warning) *warning = 1;
+      return zja_bisect(tg, beta, xs, n, lw, log_m0, delta, tol, beta, probe, beta_next);
+    }
+  }
+  *beta_next = root;
+  return 0;
+}
+
+/* drivers.cpp:234-341 */
+int ora_run_zja(const asmc_target_desc* tg, const asmc_kernel_desc* k, const asmc_zja_opts* o, int32_t workers,
+                asmc_zja_out* out) {
+  (void)workers;
+  if (o->n_particles < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "n_particles must be at least 1");
+  if (o->target_steps < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "target_steps must be at least 1");
+  if (o->max_steps < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "max_steps must be at least 1");
+  if (!(o->delta_star >= 0.0) || !isfinite(o->delta_star))
+    FAIL(ASMC_ERR_INVALID_ARGUMENT, "delta_star must be finite and >= 0");
+  TRY(validate_kernel(k));
+  TRY(check_target(tg));
+  const uint64_t n = o->n_particles, d = tg->dim;
+  double delta = o->delta_star;
+  uint64_t main_round = 1;
+  out->pilot_ran = 0;
+  out->warning = 0;
+  if (delta <= 0.0) {
+    const int K = o->target_steps;
+    double* pb = malloc((size_t)(K + 1) * sizeof(double));
+    double* lam = malloc((size_t)(K + 1) * sizeof(double));
+    for (int t = 0; t <= K; ++t) pb[t] = (double)t / (double)K;
+    pb[0] = 0.0;
+    pb[K] = 1.0;
+    int rc = ora_run_sais_single(tg, k, pb, K, n, o->seed, 1, 1, 0, &out->pilot);
+    if (!rc) rc = ora_barrier_estimate(out->pilot.log_g0, out->pilot.log_g1, out->pilot.log_g2, pb, K, lam);
+    if (!rc) {
+      if (out->pilot_lambda) memcpy(out->pilot_lambda, lam, (size_t)(K + 1) * sizeof(double));
+      const double step_lam = lam[K] / (double)K;
+      delta = step_lam * step_lam > 1e-12 ? step_lam * step_lam : 1e-12;
+    }
+    free(pb);
+    free(lam);
+    TRY(rc);
+    out->pilot_ran = 1;
+    main_round = 2;
+  }
+  out->delta_star = delta;
+  const int cap = o->max_steps;
+  double* xs = calloc(n * d, sizeof(double));
+  double* lw = calloc(n, sizeof(double));
+  double* scratch = calloc(5 * d, sizeof(double));
+  double* betas = calloc((size_t)cap + 1, sizeof(double));
+  double* g0 = malloc(((size_t)cap + 1) * sizeof(double));
+  double* g1 = malloc(((size_t)cap + 1) * sizeof(double));
+  double* g2 = malloc(((size_t)cap + 1) * sizeof(double));
+  asmc_report* r = &out->main;
+  for (uint64_t p = 0; p < n; ++p) {
+    stream_t st;
+    stream_init(&st, o->seed, main_round, p, 0, 0);
+    sample_reference(tg, &st, xs + p * d);
+  }
+  g0[0] = g1[0] = g2[0] = -INFINITY;
+  const double log_n = log((double)n);
+  double log_z = 0.0, elbo = 0.0, den_log = log_n;
+  int rc = 0, t = 0;
+  const uint64_t nb = block_count(n);
+  r->n_resample_times = 0;
+  if (r->ess_trace) r->ess_trace[0] = (double)n;
+  if (r->cum_log_z) r->cum_log_z[0] = 0.0;
+  if (r->resampled) r->resampled[0] = 0;
+  while (betas[t] < 1.0 && !rc) {
+    ++t;
+    if (t > cap) {
+      snprintf(g_err, sizeof g_err, "online adaptation failed to reach beta = 1 within %d steps", cap);
+      rc = ASMC_ERR_EVALUATION;
+      break;
+    }
+    int32_t w = 0;
+    rc = ora_zja_next_beta(tg, betas[t - 1], xs, n, lw, delta, 1e-10, &betas[t], &w);
+    if (rc) break;
+    out->warning |= w;
+    /* step_pass (engine_detail.hpp:113-156) from betas[t-1] to betas[t] */
+    step_acc_t tot;
+    step_acc_init(&tot);
+    lacc_t sq_tot = LACC0;
+    double max1 = -INFINITY, max2 = -INFINITY;
+    for (uint64_t b = 0; b < nb && !rc; ++b) {
+      step_acc_t a;
+      step_acc_init(&a);
+      lacc_t s2 = LACC0;
+      double m1 = -INFINITY, m2 = -INFINITY;
+      const uint64_t lo = b * KBLOCK, hi = lo + KBLOCK < n ? lo + KBLOCK : n;
+      for (uint64_t p = lo; p < hi; ++p) {
+        stream_t st;
+        stream_init(&st, o->seed, main_round, p, (uint64_t)t, 1);
+        rc = weight_and_move(tg, k, betas[t - 1], betas[t], xs + p * d, lw + p, &a, scratch, &st);
+        if (rc) break;
+        lacc_add(&s2, 2.0 * lw[p]);
+        if (lw[p] > m1) { m2 = m1; m1 = lw[p]; }
+        else if (lw[p] > m2) m2 = lw[p];
+      }
+      step_acc_combine(&tot, &a);
+      lacc_combine(&sq_tot, &s2);
+      if (m1 > max1) { max2 = max1 > m2 ? max1 : m2; max1 = m1; }
+      else max2 = max2 > m1 ? max2 : m1;
+    }
+    if (rc) break;
+    g0[t] = lacc_total(&tot.g0);
+    g1[t] = lacc_total(&tot.g1);
+    g2[t] = lacc_total(&tot.g2);
+    if (g1[t] == -INFINITY) { snprintf(g_err, sizeof g_err, "all log-weights are -inf at step %d", t); rc = ASMC_ERR_DEGENERATE; break; }
+    double ess_t = exp(2.0 * g1[t] - lacc_total(&sq_tot));
+    ess_t = fmin((double)n, fmax(1.0, ess_t));
+    if (r->ess_trace) r->ess_trace[t] = ess_t;
+    rc = check_degenerate(n, ess_t, max1, max2, t);
+    if (rc) break;
+    elbo += sacc_value_scaled(&tot.el, den_log);
+    if (betas[t] == 1.0) {
+      log_z += g1[t] - log_n;
+      den_log = log_n;
+      if (r->resample_times) r->resample_times[r->n_resample_times] = t;
+      r->n_resample_times++;
+    } else {
+      den_log = g1[t];
+    }
+    if (r->cum_log_z) r->cum_log_z[t] = log_z;
+    if (r->resampled) r->resampled[t] = 0;
+  }
+  if (!rc && t + 1 > out->capacity) {
+    snprintf(g_err, sizeof g_err, "output capacity too small (%d needed)", t + 1);
+    rc = ASMC_ERR_INVALID_ARGUMENT;
+  }
+  if (!rc) {
+    out->steps = t;
+    for (int i = 0; i <= t; ++i) {
+      if (r->log_g0) r->log_g0[i] = g0[i];
+      if (r->log_g1) r->log_g1[i] = g1[i];
+      if (r->log_g2) r->log_g2[i] = g2[i];
+      if (out->betas) out->betas[i] = betas[i];
+    }
+    r->log_z_hat = log_z;
+    r->elbo_hat = elbo;
+    r->kernel_applications = n * (uint64_t)t;
+    r->wall_seconds = 0.0;
+    if (out->lambda) {
+      out->lambda[0] = 0.0;
+      for (int i = 1; i <= t; ++i) out->lambda[i] = out->lambda[i - 1] + sqrt(discrepancy_hat_raw(g0[i], g1[i], g2[i]));
+    }
+  }
+  free(xs); free(lw); free(scratch); free(betas); free(g0); free(g1); free(g2);
+  return rc;
+}

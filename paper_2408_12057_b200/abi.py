@@ -84,6 +84,73 @@ class RoundsOut(C.Structure):
                 ("kernel_applications", C.POINTER(C.c_uint64))]
 
 
+class ZjaOpts(C.Structure):
+    _fields_ = [("n_particles", C.c_uint64), ("target_steps", C.c_int32), ("max_steps", C.c_int32),
+                ("delta_star", C.c_double), ("seed", C.c_uint64)]
+
+
+class ZjaOut(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("steps", C.c_int32), ("pilot_ran", C.c_int32),
+                ("warning", C.c_int32), ("delta_star", C.c_double), ("betas", C.POINTER(C.c_double)),
+                ("lambda_", C.POINTER(C.c_double)), ("main", Report),
+                ("pilot_lambda", C.POINTER(C.c_double)), ("pilot", Report)]
+
+
+def zja_opts(n, target_steps=32, delta_star=0.0, seed=0, max_steps=100000):
+    o = ZjaOpts()
+    o.n_particles, o.target_steps, o.max_steps, o.delta_star, o.seed = n, target_steps, max_steps, delta_star, seed
+    return o
+
+
+def _report_bufs(T):
+    import numpy as np
+    bufs = dict(log_g0=np.full(T + 1, -np.inf), log_g1=np.full(T + 1, -np.inf),
+                log_g2=np.full(T + 1, -np.inf), ess_trace=np.zeros(T + 1), cum_log_z=np.zeros(T + 1),
+                resampled=np.zeros(T + 1, np.uint8), resample_times=np.zeros(T + 1, np.int32))
+    rep = Report()
+    for k in ("log_g0", "log_g1", "log_g2", "ess_trace", "cum_log_z"):
+        setattr(rep, k, bufs[k].ctypes.data_as(C.POINTER(C.c_double)))
+    rep.resampled = bufs["resampled"].ctypes.data_as(C.POINTER(C.c_uint8))
+    rep.resample_times = bufs["resample_times"].ctypes.data_as(C.POINTER(C.c_int32))
+    return rep, bufs
+
+
+def zja_buffers(opts):
+    """ZjaOut with numpy-backed arrays (main: max_steps + 1 entries, pilot: K + 1)."""
+    import numpy as np
+    out = ZjaOut()
+    cap = opts.max_steps + 1
+    out.capacity = cap
+    keep = {}
+    out.main, keep["main"] = _report_bufs(cap - 1)
+    out.pilot, keep["pilot"] = _report_bufs(opts.target_steps)
+    keep["betas"], keep["lambda_"], keep["pilot_lambda"] = np.zeros(cap), np.zeros(cap), np.zeros(opts.target_steps + 1)
+    for k in ("betas", "lambda_", "pilot_lambda"):
+        setattr(out, k, keep[k].ctypes.data_as(C.POINTER(C.c_double)))
+    return out, keep
+
+
+def zja_finish(out, keep):
+    """ZjaOutcome as a dict: 'rounds' = [pilot?, main], each a run report + betas/lambda."""
+    T = out.steps
+    def rep(r, b, n):
+        d = {k: v[: n + 1].copy() for k, v in b.items() if k != "resample_times"}
+        d["resample_times"] = [int(v) for v in b["resample_times"][: r.n_resample_times]]
+        d.update(log_z_hat=r.log_z_hat, elbo_hat=r.elbo_hat, kernel_applications=r.kernel_applications,
+                 wall_seconds=r.wall_seconds)
+        return d
+    main = rep(out.main, keep["main"], T)
+    main.update(round=2 if out.pilot_ran else 1, betas=keep["betas"][: T + 1].copy(),
+                lambda_=keep["lambda_"][: T + 1].copy())
+    rounds = [main]
+    if out.pilot_ran:
+        K = len(keep["pilot_lambda"]) - 1
+        pilot = rep(out.pilot, keep["pilot"], K)
+        pilot.update(round=1, lambda_=keep["pilot_lambda"].copy())
+        rounds.insert(0, pilot)
+    return {"rounds": rounds, "delta_star": out.delta_star, "warning": bool(out.warning), "steps": T}
+
+
 def target(kind, dim, *params):
     t = TargetDesc()
     t.kind = kind

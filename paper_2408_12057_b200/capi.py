@@ -281,6 +281,27 @@ def peak_normals(device, blocks, quads_per_thread):
     return s.value
 
 
+def run_zja(target, kernel, n, target_steps=32, delta_star=0.0, seed=0, max_steps=100000, exec_=None):
+    """asmc::run_zja (drivers.cpp:234-341) on the device; returns abi.zja_finish's dict."""
+    o = abi.zja_opts(n, target_steps, delta_star, seed, max_steps)
+    out, keep = abi.zja_buffers(o)
+    ex = exec_ or abi.execopts()
+    _check(lib().asmc_run_zja(C.byref(target), C.byref(kernel), C.byref(o), C.byref(ex), C.byref(out)))
+    return abi.zja_finish(out, keep)
+
+
+def zja_next_beta(target, beta, positions, log_weights, delta_star, tol=1e-10, exec_=None):
+    """asmc::zja_next_beta (schedule.cpp:219-264); positions n x dim.  Returns (beta_next, warning)."""
+    x = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1)
+    lw = np.ascontiguousarray(log_weights, dtype=np.float64)
+    nb, w = C.c_double(0.0), C.c_int32(0)
+    ex = exec_ or abi.execopts()
+    _check(lib().asmc_zja_next_beta(C.byref(target), C.c_double(beta), _arr(x, C.c_double), C.c_uint64(len(lw)),
+                                    _arr(lw, C.c_double), C.c_double(delta_star), C.c_double(tol), C.byref(ex),
+                                    C.byref(nb), C.byref(w)))
+    return nb.value, bool(w.value)
+
+
 class SmcShard:
     """One GPU's particle shard of a multi-GPU run_smc (asmc_smc_shard_* in
     include/asmc_b200.h).  Buffers passed to the methods are DEVICE addresses
@@ -366,5 +387,6 @@ EXPORTED = [
     "asmc_profile_collect", "asmc_peak_normals", "asmc_smc_shard_create", "asmc_smc_shard_destroy",
     "asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes",
     "asmc_smc_shard_step", "asmc_smc_shard_decide", "asmc_smc_shard_plan", "asmc_smc_shard_pack",
-    "asmc_smc_shard_accept", "asmc_smc_shard_report", "asmc_smc_shard_state",
+    "asmc_smc_shard_accept", "asmc_smc_shard_report", "asmc_smc_shard_state", "asmc_run_zja",
+    "asmc_zja_next_beta",
 ]

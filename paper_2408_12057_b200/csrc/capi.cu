@@ -4,6 +4,7 @@
 // CPU fallback: without a device every sampler entry returns ASMC_ERR_CUDA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -18,6 +19,7 @@
 #include "engine_kernels.h"
 #include "ising.h"
 #include "logistic.h"
+#include "zja.h"
 
 using namespace asmcdev;
 
@@ -1394,6 +1396,208 @@ int asmc_peak_normals(int32_t device, int32_t blocks, uint64_t quads_per_thread,
   *seconds = ms * 1e-3;
   cudaEventDestroy(a);
   cudaEventDestroy(b);
+  return 0;
+}
+
+}  // extern "C"
+
+// ===================================================================== ZJA
+extern "C" {
+
+int asmc_zja_next_beta(const asmc_target_desc* target, double beta, const double* positions, uint64_t n,
+                       const double* log_weights, double delta_star, double tol, const asmc_exec* exec,
+                       double* beta_next, int32_t* warning) {
+  // schedule.cpp:219-231
+  if (!(beta >= 0.0 && beta < 1.0)) return fail(ASMC_ERR_DOMAIN, "zja_next_beta requires beta in [0, 1)");
+  if (!(delta_star > 0.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "delta_star must be positive");
+  if (!(tol > 0.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "tol must be positive");
+  if (n == 0 || !positions || !log_weights)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "particle arrays inconsistent with n_particles");
+  TRY(check_target(target));
+  TRY(check_pass_target(target, "asmc_zja_next_beta"));
+  if (!beta_next) return fail(ASMC_ERR_INVALID_ARGUMENT, "null output");
+  const asmc_exec ex = exec ? *exec : default_exec();
+  const bool exact = ex.precision == ASMC_PREC_FP64;
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C, ex.stream));
+  const uint64_t d = target->dim;
+  DBuf<char> x;
+  DBuf<void*> xbuf;
+  DBuf<int> xcur, warn, err;
+  DBuf<double> lw, lr, V, betas;
+  DBuf<LogAcc> part;
+  const int grid = zja_grid_blocks(ex.device);
+  TRY(x.alloc(n * d * sizeof(double), C->stream));
+  TRY(xbuf.alloc(2, C->stream));
+  TRY(xcur.alloc(1, C->stream));
+  TRY(warn.alloc(1, C->stream));
+  TRY(err.alloc(1, C->stream));
+  TRY(lw.alloc(n, C->stream));
+  TRY(lr.alloc(n, C->stream));
+  TRY(V.alloc(n, C->stream));
+  TRY(betas.alloc(2, C->stream));
+  TRY(part.alloc((size_t)4 * grid, C->stream));
+  std::vector<float> xf;
+  if (exact) {
+    CU(cudaMemcpyAsync(x.p, positions, n * d * sizeof(double), cudaMemcpyHostToDevice, C->stream));
+  } else {
+    xf.assign(positions, positions + n * d);
+    CU(cudaMemcpyAsync(x.p, xf.data(), n * d * sizeof(float), cudaMemcpyHostToDevice, C->stream));
+  }
+  void* ptrs[2] = {x.p, x.p};
+  CU(cudaMemcpyAsync(xbuf.p, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemsetAsync(xcur.p, 0, sizeof(int), C->stream));
+  CU(cudaMemsetAsync(warn.p, 0, sizeof(int), C->stream));
+  CU(cudaMemsetAsync(err.p, 0, sizeof(int), C->stream));
+  CU(cudaMemcpyAsync(lw.p, log_weights, n * sizeof(double), cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemcpyAsync(betas.p, &beta, sizeof(double), cudaMemcpyHostToDevice, C->stream));
+  LCH(launch_zja_eval(make_params(target), exact, xbuf.p, xcur.p, n, lr.p, V.p, err.p, C->stream));
+  ZjaArgs A{lw.p, lr.p, V.p, n, betas.p, 1, exact ? 1 : 0, delta_star, tol, warn.p, err.p, part.p};
+  LCH(launch_zja_next_beta(A, grid, C->stream));
+  double nb[2];
+  int h[2];
+  CU(cudaMemcpyAsync(nb, betas.p, sizeof nb, cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaMemcpyAsync(&h[0], warn.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaMemcpyAsync(&h[1], err.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  if (h[1]) return fail(ASMC_ERR_DEGENERATE, "all log-weights are -inf");
+  *beta_next = nb[1];
+  if (warning) *warning = h[0];
+  return 0;
+}
+
+int asmc_run_zja(const asmc_target_desc* target, const asmc_kernel_desc* kernel, const asmc_zja_opts* o,
+                 const asmc_exec* exec, asmc_zja_out* out) {
+  if (!o || !out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null options or output");
+  // ZjaOptions::validate (drivers.cpp:23-31)
+  if (o->n_particles < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "n_particles must be at least 1");
+  if (o->target_steps < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "target_steps must be at least 1");
+  if (o->max_steps < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "max_steps must be at least 1");
+  if (!(o->delta_star >= 0.0) || !std::isfinite(o->delta_star))
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "delta_star must be finite and >= 0");
+  TRY(check_pair(target, kernel));
+  TRY(check_pass_target(target, "asmc_run_zja"));
+  const asmc_exec ex = exec ? *exec : default_exec();
+  const bool exact = ex.precision == ASMC_PREC_FP64;
+  const uint64_t n = o->n_particles, d = target->dim;
+  if (out->capacity < 2) return fail(ASMC_ERR_INVALID_ARGUMENT, "output capacity must be at least 2");
+  Layout L;
+  TRY(choose_layout(ex, d, &L));
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C, ex.stream));
+  const PassArgs base = base_args(target, kernel);
+  double delta = o->delta_star;
+  uint64_t main_round = 1;
+  out->pilot_ran = 0;
+  out->warning = 0;
+  if (delta <= 0.0) {  // drivers.cpp:244-265: uniform-K pilot, policy never, round 1
+    const int K = o->target_steps;
+    std::vector<double> pb(K + 1);
+    for (int t = 0; t <= K; ++t) pb[t] = (double)t / (double)K;
+    pb[0] = 0.0;
+    pb[K] = 1.0;
+    Layout Lp;
+    TRY(choose_layout(ex, d, &Lp, K, 4));
+    DBuf<double> d_pb;
+    TRY(d_pb.alloc(K + 1, C->stream));
+    CU(cudaMemcpyAsync(d_pb.p, pb.data(), sizeof(double) * (K + 1), cudaMemcpyHostToDevice, C->stream));
+    RoundBufs R;
+    TRY(R.alloc(K, C->stream));
+    SaisWork W;  // run_smc(never) == run_sais_single (drivers.hpp:80-86)
+    TRY(enqueue_sais_round(C, ex, Lp, base, d_pb.p, K, n, o->seed, 1, R.rd.p, &R.st.p->err, W));
+    SmcState st;
+    TRY(copy_round(C->stream, R, K, false, &out->pilot, &st));
+    TRY(device_error(st.err, st.err_step, st.err_val));
+    out->pilot.kernel_applications = n * (uint64_t)K;
+    std::vector<double> lam(K + 1);
+    CU(cudaMemcpy(lam.data(), R.lam.p, sizeof(double) * (K + 1), cudaMemcpyDeviceToHost));
+    if (out->pilot_lambda) std::memcpy(out->pilot_lambda, lam.data(), sizeof(double) * (K + 1));
+    const double step_lam = lam[K] / (double)K;
+    delta = std::max(1e-12, step_lam * step_lam);
+    out->pilot_ran = 1;
+    main_round = 2;
+  }
+  out->delta_star = delta;
+  const double t0 = now_s();
+  const int cap = o->max_steps;
+  const size_t real = exact ? sizeof(double) : sizeof(float);
+  const uint64_t nblk = nblocks(n), nchunks = (nblk + kChunkBlocks - 1) / kChunkBlocks;
+  const int grid = zja_grid_blocks(ex.device);
+  DBuf<char> x;
+  DBuf<void*> xbuf;
+  DBuf<int> xcur, warn;
+  DBuf<double> lw, lr, V, betas;
+  DBuf<LogAcc> part, chunk, tot, zpart;
+  RoundBufs R;
+  TRY(x.alloc(n * d * real, C->stream));
+  TRY(xbuf.alloc(2, C->stream));
+  TRY(xcur.alloc(1, C->stream));
+  TRY(warn.alloc(1, C->stream));
+  TRY(lw.alloc(n, C->stream));
+  TRY(lr.alloc(n, C->stream));
+  TRY(V.alloc(n, C->stream));
+  TRY(betas.alloc(cap + 1, C->stream));
+  TRY(part.alloc((size_t)kNAcc * nblk, C->stream));
+  TRY(chunk.alloc((size_t)kNAcc * nchunks, C->stream));
+  TRY(tot.alloc(kNAcc, C->stream));
+  TRY(zpart.alloc((size_t)4 * grid, C->stream));
+  TRY(R.alloc(cap, C->stream));
+  void* ptrs[2] = {x.p, x.p};  // no resampling in ZJA: one live buffer
+  CU(cudaMemcpyAsync(xbuf.p, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemsetAsync(xcur.p, 0, sizeof(int), C->stream));
+  CU(cudaMemsetAsync(warn.p, 0, sizeof(int), C->stream));
+  CU(cudaMemsetAsync(betas.p, 0, sizeof(double), C->stream));
+  PassArgs A = base;
+  A.betas = betas.p;
+  A.T = cap;
+  A.n = n;
+  A.p_begin = 0;
+  A.n_local = n;
+  A.seed = o->seed;
+  A.round = main_round;
+  A.xbuf = xbuf.p;
+  A.xcur = xcur.p;
+  A.lw = lw.p;
+  A.part = part.p;
+  A.part_stride = nblk;
+  A.err = &R.st.p->err;
+  A.mode = kModeSmcInit;  // detail::init_particles at the main round
+  LCH(launch_pass(ex, L, A, nblk, C->stream));
+  const TgtParams tp = make_params(target);
+  int t = 0;
+  double bt = 0.0;
+  while (bt < 1.0) {
+    ++t;
+    if (t > cap)
+      return fail(ASMC_ERR_EVALUATION, "online adaptation failed to reach beta = 1 within %d steps", cap);
+    LCH(launch_zja_eval(tp, exact, xbuf.p, xcur.p, n, lr.p, V.p, &R.st.p->err, C->stream));
+    ZjaArgs Z{lw.p, lr.p, V.p, n, betas.p, t, exact ? 1 : 0, delta, 1e-10, warn.p, &R.st.p->err, zpart.p};
+    LCH(launch_zja_next_beta(Z, grid, C->stream));
+    A.mode = kModeSmcStep;
+    A.t_begin = A.t_end = t;
+    A.row_base = t;
+    LCH(launch_pass(ex, L, A, nblk, C->stream));
+    LCH(launch_fold(exact, part.p, nblk, nblk, 0, 1, kNAcc, chunk.p, tot.p, C->stream));
+    LCH(launch_smc_decide(tot.p, t, -1, n, ASMC_POLICY_NEVER, 0.5, o->seed, main_round, ex.rng, R.rd.p, C->stream,
+                          betas.p));
+    SmcState st;
+    CU(cudaMemcpyAsync(&bt, betas.p + t, sizeof(double), cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaMemcpyAsync(&st, R.st.p, sizeof st, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaStreamSynchronize(C->stream));
+    TRY(device_error(st.err, st.err_step, st.err_val));
+  }
+  if (t + 1 > out->capacity) return fail(ASMC_ERR_INVALID_ARGUMENT, "output capacity too small (%d needed)", t + 1);
+  SmcState st;
+  TRY(copy_round(C->stream, R, t, true, &out->main, &st));
+  TRY(device_error(st.err, st.err_step, st.err_val));
+  out->main.kernel_applications = n * (uint64_t)t;
+  out->main.wall_seconds = now_s() - t0;
+  out->steps = t;
+  if (out->betas) CU(cudaMemcpy(out->betas, betas.p, sizeof(double) * (t + 1), cudaMemcpyDeviceToHost));
+  if (out->lambda) CU(cudaMemcpy(out->lambda, R.lam.p, sizeof(double) * (t + 1), cudaMemcpyDeviceToHost));
+  int hw = 0;
+  CU(cudaMemcpy(&hw, warn.p, sizeof(int), cudaMemcpyDeviceToHost));
+  out->warning = hw;
   return 0;
 }
 

@@ -126,15 +126,19 @@ __device__ uint64_t smc_mix64(uint64_t z) {
 // engine.cpp:132-182 for step t: statistics, ESS, degeneracy, ELBO, the
 // resampling decision and the estimator update.  Draws the resampling
 // uniform from key (seed, round, 0, t, resample) when ancestors are selected.
-__global__ void smc_decide_kernel(const LogAcc* tot, int t, int T, uint64_t n, int policy,
+// T < 0: open-ended schedule (run_zja, drivers.cpp:300-336): step t is the last
+// iff zja_betas[t] == 1.
+__global__ void smc_decide_kernel(const LogAcc* tot, int t, int T_in, uint64_t n, int policy,
                                   double rho, uint64_t seed, uint64_t round, int rng,
-                                  RoundDev* rd) {
+                                  RoundDev* rd, const double* zja_betas) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   SmcState* st = rd->state;
   if (st->err) return;
+  const int T = T_in >= 0 ? T_in : (zja_betas[t] == 1.0 ? t : 0x7fffffff);
   const double log_n = log((double)n);
+  if (T_in < 0) rd->resampled[t] = 0;
   if (t == 1) {
-    for (int i = 0; i <= T; ++i) {
+    for (int i = 0; i <= (T_in >= 0 ? T : 0); ++i) {
       rd->log_g0[i] = rd->log_g1[i] = rd->log_g2[i] = kNegInf;
       rd->ess[i] = (double)n;
       rd->cum_log_z[i] = 0.0;
@@ -601,8 +605,8 @@ cudaError_t launch_sais_report(const LogAcc* tot, int T, uint64_t n, RoundDev* r
 
 cudaError_t launch_smc_decide(const LogAcc* tot_row, int t, int T, uint64_t n, int policy,
                               double rho, uint64_t seed, uint64_t round, int rng, RoundDev* rd,
-                              cudaStream_t s) {
-  smc_decide_kernel<<<1, 1, 0, s>>>(tot_row, t, T, n, policy, rho, seed, round, rng, rd);
+                              cudaStream_t s, const double* zja_betas) {
+  smc_decide_kernel<<<1, 1, 0, s>>>(tot_row, t, T, n, policy, rho, seed, round, rng, rd, zja_betas);
   return LAUNCH_OK();
 }
 

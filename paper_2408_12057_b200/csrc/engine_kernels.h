@@ -47,7 +47,7 @@ cudaError_t launch_fold_chunks_final(const LogAcc* chunk, uint64_t nchunks, int 
 cudaError_t launch_sais_report(const LogAcc* tot, int T, uint64_t n, RoundDev* rd, cudaStream_t s);
 cudaError_t launch_smc_decide(const LogAcc* tot_row, int t, int T, uint64_t n, int policy,
                               double rho, uint64_t seed, uint64_t round, int rng, RoundDev* rd,
-                              cudaStream_t s);
+                              cudaStream_t s, const double* zja_betas = nullptr);
 cudaError_t launch_resample(const double* lw_in, uint64_t n, SmcState* st, double* cum,
                             double* btot, uint32_t* anc, cudaStream_t s);
 cudaError_t launch_gather(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,

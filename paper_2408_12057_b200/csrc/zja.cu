@@ -1,0 +1,238 @@
+// ZJA online schedule selection on the device (src/schedule.cpp:201-264).
+//
+// zja_next_beta picks the largest beta' in (beta, 1] whose one-step discrepancy
+//   D(beta') = lse(lw + 2 lg) - 2 lse(lw + lg) + lse(lw),   lg = log gamma_beta'(x) - log gamma_beta(x),
+// stays <= delta*, by bisection to 1e-10 plus a 16-point monotonicity scan: ~50
+// probes per annealing step, each a log-sum-exp over all particles.  With log eta(x)
+// and V(x) cached per particle (zja_eval_kernel, once per step) a probe reads 24 B
+// per particle and never touches the particle state.
+//
+//  * exact (reference mode): one thread, sequential LogAccumulators in particle
+//    order -- the reference's own accumulation order, so the probe values agree with
+//    it to libm ulps and the bisection takes the same branches.
+//  * cooperative (throughput mode): the whole search in ONE persistent cooperative
+//    launch; per probe every CTA folds its strided particles (thread: sequential;
+//    warp: xor butterfly; warps in order), writes its partial, one grid.sync(), then
+//    every CTA folds the CTA partials in order and takes the same branch.  No host
+//    round trip per probe; the per-particle arrays stay L2-resident across probes.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "zja.h"
+
+namespace asmcdev {
+namespace cg = cooperative_groups;
+
+template <class Tgt, typename Real>
+__global__ void zja_eval_kernel(TgtParams T, const void* const* xbuf, const int* xcur, uint64_t n,
+                                double* lr, double* V, const int* err) {
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n || (err && *err)) return;
+  const int d = (int)T.dim;
+  const Real* x = reinterpret_cast<const Real*>(xbuf[*xcur]) + p * (uint64_t)d;
+  double L = 0.0, v = 0.0;  // target.cpp:34-39: two ordered sums
+  for (int k = 0; k < d; ++k) L += Tgt::lr64(T, (double)x[k]);
+  for (int k = 0; k < d; ++k) v += Tgt::v64(T, (double)x[k]);
+  lr[p] = L;
+  V[p] = v;
+}
+
+// log_incremental_weight (kernel.cpp:65-73) from cached log eta and V
+__device__ __forceinline__ double zja_lg(double lr, double V, double b2, double beta) {
+  const double g2 = b2 == 0.0 ? lr : lr + b2 * V;
+  const double g1 = beta == 0.0 ? lr : lr + beta * V;
+  return g2 - g1;
+}
+
+__device__ __forceinline__ double lacc_log_total(const LogAcc& a) {
+  return a.max == -__builtin_huge_val() ? -__builtin_huge_val() : a.max + log(a.sum);
+}
+
+// The search itself, shared by both modes: `dhat(b2)` and `lse_lw()` are the probes.
+template <class Probe>
+__device__ void zja_search(const ZjaArgs& A, Probe& P, double* out_beta, int* out_warn) {
+  const double beta = A.betas[A.t - 1];
+  const double delta = A.delta, tol = A.tol;
+  *out_warn = 0;
+  if (P.dhat(1.0) <= delta) {
+    *out_beta = 1.0;
+    return;
+  }
+  auto bisect = [&](double lo, double hi) {
+    while (hi - lo > tol) {
+      const double mid = 0.5 * (lo + hi);
+      if (P.dhat(mid) <= delta) lo = mid;
+      else hi = mid;
+    }
+    return lo;
+  };
+  const double root = bisect(beta, 1.0);
+  constexpr int kGridPoints = 16;  // schedule.cpp:254-261
+  for (int i = 1; i < kGridPoints; ++i) {
+    const double probe = beta + (root - beta) * (double)i / kGridPoints;
+    if (P.dhat(probe) > delta * (1.0 + 1e-12)) {
+      *out_beta = bisect(beta, probe);
+      *out_warn = 1;
+      return;
+    }
+  }
+  *out_beta = root;
+}
+
+struct SeqProbe {
+  const ZjaArgs& A;
+  double beta, log_m0;
+  __device__ double dhat(double b2) const {  // schedule.cpp:201-215
+    LogAcc m1 = lacc_empty(), m2 = lacc_empty();
+    for (uint64_t p = 0; p < A.n; ++p) {
+      const double lg = zja_lg(A.lr[p], A.V[p], b2, beta);
+      lacc_add(m1, A.lw[p] + lg);
+      lacc_add(m2, A.lw[p] + 2.0 * lg);
+    }
+    const double raw = lacc_log_total(m2) - 2.0 * lacc_log_total(m1) + log_m0;
+    return raw > 0.0 ? raw : 0.0;
+  }
+};
+
+__global__ void zja_exact_kernel(ZjaArgs A) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || *A.err) return;
+  LogAcc m0 = lacc_empty();  // logsumexp (logsum.hpp:97-101)
+  for (uint64_t p = 0; p < A.n; ++p) lacc_add(m0, A.lw[p]);
+  const double log_m0 = lacc_log_total(m0);
+  if (log_m0 == -__builtin_huge_val()) {
+    *A.err = ASMC_ERR_DEGENERATE;
+    return;
+  }
+  SeqProbe P{A, A.betas[A.t - 1], log_m0};
+  int warn = 0;
+  double nb;
+  zja_search(A, P, &nb, &warn);
+  A.betas[A.t] = nb;
+  if (warn) *A.warn = 1;
+}
+
+constexpr int kZjaThreads = 256;
+
+struct GridProbe {
+  const ZjaArgs& A;
+  double beta, log_m0;
+  int parity;
+  LogAcc* s_w;    // [2 * 8] warp partials
+  double* s_out;  // broadcast slot
+
+  // fold (a, b) over the grid in a fixed order; every thread receives the totals
+  __device__ void fold2(LogAcc a, LogAcc b, LogAcc& ta, LogAcc& tb) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      lacc_combine(a, shfl_xor_acc(a, m));
+      lacc_combine(b, shfl_xor_acc(b, m));
+    }
+    if (lane == 0) {
+      s_w[w] = a;
+      s_w[8 + w] = b;
+    }
+    __syncthreads();
+    LogAcc* buf = A.part + (size_t)parity * 2 * gridDim.x;
+    parity ^= 1;
+    if (threadIdx.x == 0) {
+      LogAcc x = lacc_empty(), y = lacc_empty();
+      for (int i = 0; i < kZjaThreads / 32; ++i) {
+        lacc_combine(x, s_w[i]);
+        lacc_combine(y, s_w[8 + i]);
+      }
+      buf[blockIdx.x] = x;
+      buf[gridDim.x + blockIdx.x] = y;
+    }
+    cg::this_grid().sync();
+    if (threadIdx.x == 0) {
+      LogAcc x = lacc_empty(), y = lacc_empty();
+      for (unsigned i = 0; i < gridDim.x; ++i) {
+        lacc_combine(x, buf[i]);
+        lacc_combine(y, buf[gridDim.x + i]);
+      }
+      s_w[0] = x;
+      s_w[8] = y;
+    }
+    __syncthreads();
+    ta = s_w[0];
+    tb = s_w[8];
+    __syncthreads();
+  }
+
+  __device__ double dhat(double b2) {
+    LogAcc m1 = lacc_empty(), m2 = lacc_empty();
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < A.n; p += stride) {
+      const double lg = (b2 - beta) * A.V[p];  // difference form of zja_lg
+      lacc_add(m1, A.lw[p] + lg);
+      lacc_add(m2, A.lw[p] + 2.0 * lg);
+    }
+    LogAcc t1, t2;
+    fold2(m1, m2, t1, t2);
+    const double raw = lacc_log_total(t2) - 2.0 * lacc_log_total(t1) + log_m0;
+    return raw > 0.0 ? raw : 0.0;
+  }
+};
+
+__global__ void __launch_bounds__(kZjaThreads) zja_coop_kernel(ZjaArgs A) {
+  __shared__ LogAcc s_w[16];
+  __shared__ double s_out[2];
+  const int err0 = *(volatile int*)A.err;  // uniform across the grid (read before any write)
+  if (err0) return;
+  GridProbe P{A, A.betas[A.t - 1], 0.0, 0, s_w, s_out};
+  LogAcc m0 = lacc_empty();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < A.n; p += stride) lacc_add(m0, A.lw[p]);
+  LogAcc t0, unused;
+  P.fold2(m0, lacc_empty(), t0, unused);
+  P.log_m0 = lacc_log_total(t0);
+  if (P.log_m0 == -__builtin_huge_val()) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *A.err = ASMC_ERR_DEGENERATE;
+    return;
+  }
+  double nb;
+  int warn;
+  zja_search(A, P, &nb, &warn);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.betas[A.t] = nb;
+    if (warn) *A.warn = 1;
+  }
+}
+
+cudaError_t launch_zja_eval(const TgtParams& T, bool fp64_state, const void* const* xbuf, const int* xcur,
+                            uint64_t n, double* lr, double* V, const int* err, cudaStream_t s) {
+  const unsigned g = (unsigned)((n + 127) / 128);
+#define ZJA_EVAL(TG)                                                                            \
+  (fp64_state ? (zja_eval_kernel<TG, double><<<g, 128, 0, s>>>(T, xbuf, xcur, n, lr, V, err), 0) \
+              : (zja_eval_kernel<TG, float><<<g, 128, 0, s>>>(T, xbuf, xcur, n, lr, V, err), 0))
+  switch (T.kind) {
+    case ASMC_TARGET_GAUSSIAN_SHIFT: ZJA_EVAL(TgtGaussShift); break;
+    case ASMC_TARGET_MIXTURE: ZJA_EVAL(TgtMixture); break;
+    case ASMC_TARGET_SCALE_GAUSSIAN: ZJA_EVAL(TgtScale); break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef ZJA_EVAL
+  return cudaGetLastError();
+}
+
+int zja_grid_blocks(int device) {
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, zja_coop_kernel, kZjaThreads, 0);
+  if (per > 2) per = 2;  // 2 CTAs / SM saturate the L2 reads; fewer partials to fold
+  return sms * (per > 0 ? per : 1);
+}
+
+cudaError_t launch_zja_next_beta(const ZjaArgs& A, int grid_blocks, cudaStream_t s) {
+  if (A.exact) {
+    zja_exact_kernel<<<1, 32, 0, s>>>(A);
+    return cudaGetLastError();
+  }
+  ZjaArgs a = A;
+  void* args[] = {&a};
+  return cudaLaunchCooperativeKernel((const void*)zja_coop_kernel, dim3(grid_blocks), dim3(kZjaThreads), args, 0,
+                                     s);
+}
+
+}  // namespace asmcdev
