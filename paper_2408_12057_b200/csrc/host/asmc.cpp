@@ -570,6 +570,79 @@ std::vector<RoundResult> run_sais(const AnnealedTarget& t, const Kernel& k, cons
   return round_loop(t, k, o, DriverMode::sais);
 }
 
+void ZjaOptions::validate() const {  // drivers.cpp:23-31
+  if (n_particles < 1) throw std::invalid_argument("n_particles must be at least 1");
+  if (target_steps < 1) throw std::invalid_argument("target_steps must be at least 1");
+  if (workers < 1) throw std::invalid_argument("workers must be at least 1");
+  if (max_steps < 1) throw std::invalid_argument("max_steps must be at least 1");
+  if (!(delta_star >= 0.0) || !std::isfinite(delta_star))
+    throw std::invalid_argument("delta_star must be finite and >= 0");
+}
+
+ZjaResult zja_next_beta(const AnnealedTarget& target, double beta, std::span<const double> positions,
+                        std::size_t n, std::span<const double> log_weights, double delta_star, double tol) {
+  if (n == 0 || log_weights.size() != n || positions.size() != n * target.dim())
+    throw std::invalid_argument("particle arrays inconsistent with n_particles");
+  const asmc_target_desc td = descriptor(target);
+  const asmc_exec ex = exec_of(Rng::xoshiro, Precision::fp64, 0, 0);
+  ZjaResult r;
+  int32_t w = 0;
+  check(asmc_zja_next_beta(&td, beta, positions.data(), n, log_weights.data(), delta_star, tol, &ex,
+                           &r.beta_next, &w));
+  r.warning = w != 0;
+  return r;
+}
+
+ZjaOutcome run_zja(const AnnealedTarget& target, const Kernel& kernel, const ZjaOptions& o) {
+  o.validate();
+  validate_kernel(kernel);
+  const asmc_target_desc td = descriptor(target);
+  const asmc_kernel_desc kd = kernel_desc(kernel);
+  const asmc_exec ex = exec_of(o.rng, o.precision, o.device, o.lanes);
+  asmc_zja_opts zo{o.n_particles, o.target_steps, o.max_steps, o.delta_star, o.seed};
+  ReportBufs main(o.max_steps), pilot(o.target_steps);
+  std::vector<double> betas(o.max_steps + 1), lam(o.max_steps + 1), plam(o.target_steps + 1);
+  asmc_zja_out out;
+  std::memset(&out, 0, sizeof out);
+  out.capacity = o.max_steps + 1;
+  out.betas = betas.data();
+  out.lambda = lam.data();
+  out.main = main.rep;
+  out.pilot_lambda = plam.data();
+  out.pilot = pilot.rep;
+  check(asmc_run_zja(&td, &kd, &zo, &ex, &out));
+  ZjaOutcome res;
+  res.delta_star = out.delta_star;
+  res.warning = out.warning != 0;
+  if (out.pilot_ran) {
+    pilot.rep = out.pilot;
+    RoundResult rr;
+    rr.round = 1;
+    rr.report = pilot.to_report(Schedule::uniform(o.target_steps), o.n_particles, false);
+    rr.barrier.lambda = plam;
+    rr.barrier.beta = rr.report.schedule.betas;
+    res.rounds.push_back(std::move(rr));
+  }
+  const int T = out.steps;
+  main.rep = out.main;
+  Schedule s;
+  s.betas.assign(betas.begin(), betas.begin() + T + 1);
+  RoundResult rr;
+  rr.round = out.pilot_ran ? 2 : 1;
+  rr.report = main.to_report(s, o.n_particles, true);
+  auto cut = [T](auto& v) { v.resize(T + 1); };
+  cut(rr.report.stats.log_g0);
+  cut(rr.report.stats.log_g1);
+  cut(rr.report.stats.log_g2);
+  cut(rr.report.ess_trace);
+  cut(rr.report.cum_log_z);
+  cut(rr.report.resampled);
+  rr.barrier.lambda.assign(lam.begin(), lam.begin() + T + 1);
+  rr.barrier.beta = s.betas;
+  res.rounds.push_back(std::move(rr));
+  return res;
+}
+
 SaisMemoryProfile sais_memory_profile(int total_steps, int workers, std::size_t chunk) {
   // drivers.cpp:59-70 semantics: adaptation storage 3(T+1) + (T+1), never N
   if (total_steps < 1) throw std::invalid_argument("profile needs at least one step");

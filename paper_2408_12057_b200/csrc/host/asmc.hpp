@@ -242,6 +242,15 @@ BarrierEstimate barrier_estimate(const IncrementStats& stats, const Schedule& sc
 Schedule generate_schedule(const BarrierEstimate& estimate, int t_new);
 std::vector<double> local_barrier(const BarrierEstimate& estimate);
 
+// schedule.hpp:51-64
+struct ZjaResult {
+  double beta_next = 1.0;
+  bool warning = false;
+};
+ZjaResult zja_next_beta(const AnnealedTarget& target, double beta, std::span<const double> positions,
+                        std::size_t n_particles, std::span<const double> log_weights, double delta_star,
+                        double tol = 1e-10);
+
 // ---- drivers.hpp ----------------------------------------------------------
 enum class DriverMode { ssmc, sais };
 
@@ -284,6 +293,31 @@ std::vector<RoundResult> run_sais(const AnnealedTarget& target, const Kernel& ke
 RunReport run_sais_single(const AnnealedTarget& target, const Kernel& kernel,
                           const Schedule& schedule, const RunOptions& options,
                           std::size_t chunk = 0);
+
+// drivers.hpp:88-111
+struct ZjaOptions {
+  std::size_t n_particles = 1024;
+  int target_steps = 32;
+  double delta_star = 0.0;
+  std::uint64_t seed = 0;
+  int workers = 1;
+  int max_steps = 100000;
+  // device execution (new)
+  Rng rng = Rng::xoshiro;
+  Precision precision = Precision::fp64;
+  int device = 0;
+  int lanes = 0;
+
+  void validate() const;
+};
+
+struct ZjaOutcome {
+  std::vector<RoundResult> rounds;  // pilot round first (when one ran), then the adaptive run
+  double delta_star = 0.0;
+  bool warning = false;
+};
+
+ZjaOutcome run_zja(const AnnealedTarget& target, const Kernel& kernel, const ZjaOptions& options);
 
 struct SaisMemoryProfile {
   std::size_t moment_accumulators = 0;

@@ -120,8 +120,9 @@ struct GridProbe {
   LogAcc* s_w;    // [2 * 8] warp partials
   double* s_out;  // broadcast slot
 
-  // fold (a, b) over the grid in a fixed order; every thread receives the totals
-  __device__ void fold2(LogAcc a, LogAcc b, LogAcc& ta, LogAcc& tb) {
+  // CTA-wide fixed tree (xor butterfly in each warp, warps in order); the totals
+  // are broadcast to every thread of the CTA
+  __device__ void cta_fold2(LogAcc& a, LogAcc& b) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) {
@@ -133,31 +134,40 @@ struct GridProbe {
       s_w[8 + w] = b;
     }
     __syncthreads();
-    LogAcc* buf = A.part + (size_t)parity * 2 * gridDim.x;
-    parity ^= 1;
     if (threadIdx.x == 0) {
       LogAcc x = lacc_empty(), y = lacc_empty();
       for (int i = 0; i < kZjaThreads / 32; ++i) {
         lacc_combine(x, s_w[i]);
         lacc_combine(y, s_w[8 + i]);
       }
-      buf[blockIdx.x] = x;
-      buf[gridDim.x + blockIdx.x] = y;
+      s_w[16] = x;
+      s_w[17] = y;
+    }
+    __syncthreads();
+    a = s_w[16];
+    b = s_w[17];
+    __syncthreads();
+  }
+
+  // fold (a, b) over the grid in a fixed order; every thread receives the totals
+  __device__ void fold2(LogAcc a, LogAcc b, LogAcc& ta, LogAcc& tb) {
+    cta_fold2(a, b);
+    LogAcc* buf = A.part + (size_t)parity * 2 * gridDim.x;
+    parity ^= 1;
+    if (threadIdx.x == 0) {
+      buf[blockIdx.x] = a;
+      buf[gridDim.x + blockIdx.x] = b;
     }
     cg::this_grid().sync();
-    if (threadIdx.x == 0) {
-      LogAcc x = lacc_empty(), y = lacc_empty();
-      for (unsigned i = 0; i < gridDim.x; ++i) {
-        lacc_combine(x, buf[i]);
-        lacc_combine(y, buf[gridDim.x + i]);
-      }
-      s_w[0] = x;
-      s_w[8] = y;
+    // CTA partials: thread i folds partials i, i + 256, ... in order, then the CTA tree
+    LogAcc x = lacc_empty(), y = lacc_empty();
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+      lacc_combine(x, buf[i]);
+      lacc_combine(y, buf[gridDim.x + i]);
     }
-    __syncthreads();
-    ta = s_w[0];
-    tb = s_w[8];
-    __syncthreads();
+    cta_fold2(x, y);
+    ta = x;
+    tb = y;
   }
 
   __device__ double dhat(double b2) {
@@ -176,7 +186,7 @@ struct GridProbe {
 };
 
 __global__ void __launch_bounds__(kZjaThreads) zja_coop_kernel(ZjaArgs A) {
-  __shared__ LogAcc s_w[16];
+  __shared__ LogAcc s_w[18];
   __shared__ double s_out[2];
   const int err0 = *(volatile int*)A.err;  // uniform across the grid (read before any write)
   if (err0) return;

@@ -123,3 +123,23 @@ def test_device_run_zja_known_answers_and_errors():
     with pytest.raises(capi.AsmcError) as e:
         capi.run_zja(tg, k, 64, delta_star=-1.0, exec_=ex)
     assert e.value.code == abi.ERR_INVALID_ARGUMENT
+
+
+@pytest.mark.gpu
+def test_drop_in_run_zja_matches_reference():
+    """The reference-shaped API (asmc.run_zja / ZjaOptions / ZjaOutcome) on the device."""
+    import paper_2408_12057_b200 as asmc
+    t = asmc.GaussianShiftTarget(0.0, 1.0, 1.0, 1)
+    o = asmc.ZjaOptions()
+    o.n_particles, o.target_steps, o.seed = 1024, 8, 22
+    out = asmc.run_zja(t, asmc.Kernel(), o)
+    ref = _ref(XO).run_zja(abi.gaussian_shift(0.0, 1.0, 1.0, 1), abi.kernel(abi.KERNEL_IDEALIZED), 1024,
+                           target_steps=8, seed=22)
+    assert len(out.rounds) == 2 and [r.round for r in out.rounds] == [1, 2]
+    assert abs(out.delta_star - ref["delta_star"]) < 1e-12 * ref["delta_star"]
+    m = out.rounds[1].report
+    assert np.max(np.abs(np.array(m.schedule.betas) - ref["rounds"][1]["betas"])) < 1e-12
+    assert abs(m.log_z_hat - ref["rounds"][1]["log_z_hat"]) < 1e-10
+    assert m.kernel_applications == 1024 * (len(m.schedule.betas) - 1)
+    r = asmc.zja_next_beta(t, 0.0, [0.1 * i for i in range(64)], 64, [0.0] * 64, 0.01)
+    assert 0.0 < r.beta_next <= 1.0
