@@ -23,7 +23,9 @@
 #include <thread>
 #include <vector>
 
+#include "asmc/config.hpp"
 #include "asmc/drivers.hpp"
+#include "asmc/experiment.hpp"
 #include "asmc/engine.hpp"
 #include "asmc/errors.hpp"
 #include "asmc/kernel.hpp"
@@ -503,6 +505,16 @@ int ora_zja_next_beta(const asmc_target_desc* target, double beta, const double*
                                        std::span<const double>(lw, n), delta, tol);
     *beta_next = r.beta_next;
     if (warning) *warning = r.warning ? 1 : 0;
+  });
+}
+
+// asmc::run_experiment (experiment.cpp:200-233) on a key=value config text: the
+// reference's own CSV writer, used to pin the report/CSV format of the B200 path.
+int ora_run_experiment(const char* config_text, const char* out_dir) {
+  return guard([&] {
+    asmc::RunConfig c = asmc::parse_config_text(config_text);
+    c.out_dir = out_dir;
+    if (asmc::run_experiment(c) != 0) throw std::runtime_error("run_experiment failed");
   });
 }
 

@@ -1239,7 +1239,7 @@ int ora_run_zja(const asmc_target_desc* tg, const asmc_kernel_desc* k, const asm
     for (int t = 0; t <= K; ++t) pb[t] = (double)t / (double)K;
     pb[0] = 0.0;
     pb[K] = 1.0;
-    int rc = ora_run_sais_single(tg, k, pb, K, n, o->seed, 1, 1, 0, &out->pilot);
+    int rc = run_smc_impl(tg, k, pb, K, n, ASMC_POLICY_NEVER, 0.5, o->seed, 1, 0, &out->pilot);
     if (!rc) rc = ora_barrier_estimate(out->pilot.log_g0, out->pilot.log_g1, out->pilot.log_g2, pb, K, lam);
     if (!rc) {
       if (out->pilot_lambda) memcpy(out->pilot_lambda, lam, (size_t)(K + 1) * sizeof(double));

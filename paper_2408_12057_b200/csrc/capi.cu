@@ -1496,17 +1496,15 @@ int asmc_run_zja(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
     for (int t = 0; t <= K; ++t) pb[t] = (double)t / (double)K;
     pb[0] = 0.0;
     pb[K] = 1.0;
-    Layout Lp;
-    TRY(choose_layout(ex, d, &Lp, K, 4));
     DBuf<double> d_pb;
     TRY(d_pb.alloc(K + 1, C->stream));
     CU(cudaMemcpyAsync(d_pb.p, pb.data(), sizeof(double) * (K + 1), cudaMemcpyHostToDevice, C->stream));
     RoundBufs R;
     TRY(R.alloc(K, C->stream));
-    SaisWork W;  // run_smc(never) == run_sais_single (drivers.hpp:80-86)
-    TRY(enqueue_sais_round(C, ex, Lp, base, d_pb.p, K, n, o->seed, 1, R.rd.p, &R.st.p->err, W));
+    SmcWork W;  // run_smc(policy never): the report carries the ESS trace, as the reference's pilot
+    TRY(enqueue_smc_round(C, ex, L, base, d_pb.p, K, n, ASMC_POLICY_NEVER, 0.5, o->seed, 1, R.rd.p, R.st.p, W));
     SmcState st;
-    TRY(copy_round(C->stream, R, K, false, &out->pilot, &st));
+    TRY(copy_round(C->stream, R, K, true, &out->pilot, &st));
     TRY(device_error(st.err, st.err_step, st.err_val));
     out->pilot.kernel_applications = n * (uint64_t)K;
     std::vector<double> lam(K + 1);

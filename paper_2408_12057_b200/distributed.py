@@ -82,7 +82,8 @@ def run_sais(target, kernel, n1, rounds, seed, exec_, rank, world, partials_fn=N
     betas = np.array([0.0, 1.0])
     n, T = n1, 1
     res = {k: [] for k in ("n_particles", "steps", "betas", "log_g0", "log_g1", "log_g2",
-                           "lambda_", "log_z_hat", "elbo_hat", "kernel_applications")}
+                           "lambda_", "log_z_hat", "elbo_hat", "kernel_applications", "cum_log_z",
+                           "resampled", "wall_seconds")}
     for k in range(1, rounds + 1):
         ranges = chunk_partition(n, world)
         counts = [chunks_of(r) for r in ranges]
@@ -95,7 +96,10 @@ def run_sais(target, kernel, n1, rounds, seed, exec_, rank, world, partials_fn=N
                          ("log_g0", rep["log_g0"]), ("log_g1", rep["log_g1"]),
                          ("log_g2", rep["log_g2"]), ("lambda_", lam),
                          ("log_z_hat", rep["log_z_hat"]), ("elbo_hat", rep["elbo_hat"]),
-                         ("kernel_applications", n * T)):
+                         ("kernel_applications", n * T),
+                         ("cum_log_z", rep.get("cum_log_z", np.zeros(T + 1))),
+                         ("resampled", rep.get("resampled", np.zeros(T + 1, np.uint8))),
+                         ("wall_seconds", 0.0)):
             res[key].append(val)
         if k < rounds:
             n, T_new = budget_fn(n, T)
