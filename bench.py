@@ -172,6 +172,60 @@ def load_profile_traffic():
     return None
 
 
+def other_configs(stream, ex):
+    """BASELINE.json configs 3-5 on this GPU (single-GPU shapes), device time by CUDA
+    events on the library's stream; inputs resident, one warm-up each."""
+    import torch
+    from paper_2408_12057_b200 import capi, exact
+    out = {}
+
+    def timed(fn):
+        fn()  # warm-up (JIT-free, but first-touch of pools / data upload)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return r, e0.elapsed_time(e1) * 1e-3
+
+    # config 3: SSMC, adaptive ESS, d=100 bimodal mixture, N=2^22, 6 rounds
+    tg = abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100)
+    k = abi.kernel(abi.KERNEL_RWMH, STEPS, 1)
+    r, dt = timed(lambda: capi.run_rounds(tg, k, abi.MODE_SSMC, 1 << 22, 6, policy=abi.POLICY_ADAPTIVE_ESS,
+                                          seed=SEED, exec_=ex))
+    ps = float(np.sum(r["kernel_applications"]))
+    out["config3"] = {"workload": "SSMC adaptive-ESS (rho 0.5) d=100 mixture, N1=2^22, 6 rounds, RWMH [0.1,1,10]",
+                      "psteps": ps, "device_s": dt, "value": ps / dt, "unit": "particle-steps/s",
+                      "resampling_events": int(np.sum(r["resampled"])),
+                      "last_log_z_hat": float(r["log_z_hat"][-1]), "exact_log_z": 0.0}
+    # config 4: SAIS Bayesian logistic regression, X 1e5 x 256, N=2^20 (tensor cores)
+    X, y = abi.logistic_data(100000, 256, 0)
+    tg = abi.logistic(X, y, 1.0)
+    k = abi.kernel(abi.KERNEL_RWMH, (0.002, 0.005, 0.01), 1)
+    betas = np.linspace(0.0, 1.0, 5)
+    capi.profile_enable(True)
+    r, dt = timed(lambda: capi.run_sais_single(tg, k, betas, 1 << 20, seed=SEED, round=1, exec_=ex))
+    ms, flops = capi.profile_collect()
+    capi.profile_enable(False)
+    n_ev = len(ms) // 2
+    ev_ms, ev_flops = float(np.sum(ms[n_ev:])), float(np.sum(flops[n_ev:]))
+    out["config4"] = {"workload": "SAIS logistic regression n=1e5 d=256, N=2^20, T=4, RWMH x3 (split-bf16 tcgen05)",
+                      "psteps": float((1 << 20) * 4), "device_s": dt, "value": (1 << 20) * 4 / dt,
+                      "unit": "particle-steps/s", "likelihood_tflops_algorithmic": ev_flops / (ev_ms * 1e-3) / 1e12,
+                      "tensor_tflops_issued": 3 * ev_flops / (ev_ms * 1e-3) / 1e12}
+    # config 5: SAIS relaxed Ising 64x64 at K_c, HMC, N=2^18
+    tg = abi.ising(64, exact.K_CRITICAL, 1.0, 1.0)
+    k = abi.kernel(abi.KERNEL_HMC, (0.25,), 1, leapfrog=10)
+    betas = np.linspace(0.0, 1.0, 9)
+    r, dt = timed(lambda: capi.run_sais_single(tg, k, betas, 1 << 18, seed=SEED, round=1, exec_=ex))
+    out["config5"] = {"workload": "SAIS relaxed Ising 64x64 K=K_c, HMC eps 0.25 x 10 leapfrog, N=2^18, T=8",
+                      "psteps": float((1 << 18) * 8), "device_s": dt, "value": (1 << 18) * 8 / dt,
+                      "unit": "particle-steps/s", "site_gradients_per_s": (1 << 18) * 8 * 11 * 4096 / dt,
+                      "log_z_hat": r["log_z_hat"], "exact_log_z": exact.ising_relaxed_log_z(64, exact.K_CRITICAL, 1.0)}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,6 +238,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-target measurement")
     ap.add_argument("--ttt-seeds", type=int, default=1000)
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs 3-5 measurements")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU chunk-partial round loop even at one rank")
     args = ap.parse_args()
@@ -316,6 +371,11 @@ def main():
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if world == 1 and not args.no_configs:
+            try:
+                line["other_configs"] = other_configs(stream, ex)
+            except Exception as exc:  # reported, never required
+                line["other_configs"] = {"unavailable": str(exc)}
         if world == 1 and not args.no_ttt:
             try:
                 sys.path.insert(0, os.path.join(ROOT, "tools"))
