@@ -83,6 +83,13 @@ extern "C" {
  * epsilon (one trajectory of `leapfrog` steps per step size per sweep; unit
  * mass; momentum = the trajectory's d normals, accept uniform after them) */
 #define ASMC_KERNEL_HMC 3
+/* new: elliptical slice sampling w.r.t. the Gaussian reference eta (Murray, Adams &
+ * MacKay 2010), `sweeps` updates per step.  Draw order per update: d normals for
+ * nu ~ eta, uniform u (log y = beta V(x) + log u), uniform for theta in [0, 2 pi),
+ * one uniform per bracket shrink (at most ASMC_SLICE_MAX_SHRINK, then x is kept).
+ * Accept x' = mu + (x - mu) cos theta + (nu - mu) sin theta iff beta V(x') > log y. */
+#define ASMC_KERNEL_SLICE 4
+#define ASMC_SLICE_MAX_SHRINK 100
 #define ASMC_MAX_STEP_SIZES 16
 
 /* ---- resampling policies (include/asmc/engine.hpp:22) ---- */

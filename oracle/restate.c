@@ -387,6 +387,8 @@ static int validate_kernel(const asmc_kernel_desc* k) {
       if (!(k->step_sizes[i] > 0.0)) FAIL(ASMC_ERR_INVALID_ARGUMENT, "hmc step sizes must be positive");
     if (k->sweeps < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "hmc sweeps must be at least 1");
     if (k->leapfrog < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "hmc leapfrog steps must be at least 1");
+  } else if (k->kind == ASMC_KERNEL_SLICE) {
+    if (k->sweeps < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "slice sweeps must be at least 1");
   } else if (k->kind != ASMC_KERNEL_IDEALIZED && k->kind != ASMC_KERNEL_IDENTITY) {
     FAIL(ASMC_ERR_INVALID_ARGUMENT, "unknown kernel kind");
   }
@@ -483,13 +485,47 @@ static void hmc_cycle_move(const asmc_target_desc* t, const asmc_kernel_desc* k,
   }
 }
 
-/* kernel.cpp:46-63 (+ the new HMC branch) */
+/* NEW kernel (no reference code): elliptical slice sampling w.r.t. the Gaussian
+ * reference eta = N(mu, sigma^2 I) (Murray, Adams & MacKay 2010), include/asmc_b200.h
+ * ASMC_KERNEL_SLICE.  Per update: nu ~ eta (d normals), log y = beta V(x) + log u,
+ * theta ~ U[0, 2 pi), bracket [theta - 2 pi, theta]; x' = mu + (x - mu) cos + (nu - mu) sin,
+ * accept iff beta V(x') > log y, else shrink toward 0 with a fresh uniform. */
+static void slice_move(const asmc_target_desc* t, const asmc_kernel_desc* k, double beta, double* x,
+                       double* scratch, stream_t* st) {
+  const uint64_t d = t->dim;
+  double* nu = scratch;
+  double* xp = scratch + d;
+  const double two_pi = 6.283185307179586476925286766559;
+  const double mu = t->kind == ASMC_TARGET_GAUSSIAN_SHIFT ? t->p[0] : 0.0;
+  for (int sweep = 0; sweep < k->sweeps; ++sweep) {
+    sample_reference(t, st, nu);
+    const double ll = beta == 0.0 ? 0.0 : beta * potential(t, x);
+    const double log_y = ll + log(uniform(st));
+    double theta = uniform(st) * two_pi;
+    double lo = theta - two_pi, hi = theta;
+    for (int it = 0; it < ASMC_SLICE_MAX_SHRINK; ++it) {
+      const double c = cos(theta), sn = sin(theta);
+      for (uint64_t i = 0; i < d; ++i) xp[i] = mu + (x[i] - mu) * c + (nu[i] - mu) * sn;
+      const double llp = beta == 0.0 ? 0.0 : beta * potential(t, xp);
+      if (llp > log_y) {
+        for (uint64_t i = 0; i < d; ++i) x[i] = xp[i];
+        break;
+      }
+      if (theta < 0.0) lo = theta;
+      else hi = theta;
+      theta = lo + (hi - lo) * uniform(st);
+    }
+  }
+}
+
+/* kernel.cpp:46-63 (+ the new HMC and slice branches) */
 static int propagate(const asmc_target_desc* t, const asmc_kernel_desc* k, double beta, double* x,
                      double* scratch, stream_t* st) {
   switch (k->kind) {
     case ASMC_KERNEL_IDEALIZED: return exact_sample(t, beta, st, x);
     case ASMC_KERNEL_RWMH: rwmh_cycle_move(t, k, beta, x, scratch, st); return 0;
     case ASMC_KERNEL_HMC: hmc_cycle_move(t, k, beta, x, scratch, st); return 0;
+    case ASMC_KERNEL_SLICE: slice_move(t, k, beta, x, scratch, st); return 0;
     default: return 0;
   }
 }

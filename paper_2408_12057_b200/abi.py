@@ -24,6 +24,8 @@ KERNEL_IDEALIZED = 0
 KERNEL_RWMH = 1
 KERNEL_IDENTITY = 2
 KERNEL_HMC = 3
+KERNEL_SLICE = 4  # elliptical slice w.r.t. the Gaussian reference
+SLICE_MAX_SHRINK = 100
 MAX_STEP_SIZES = 16
 
 POLICY_NEVER = 0

@@ -150,6 +150,8 @@ int check_kernel(const asmc_kernel_desc* k) {
         return fail(ASMC_ERR_INVALID_ARGUMENT, "hmc step sizes must be positive");
     if (k->sweeps < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "hmc sweeps must be at least 1");
     if (k->leapfrog < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "hmc leapfrog steps must be at least 1");
+  } else if (k->kind == ASMC_KERNEL_SLICE) {  // new kernel; same checks as oracle/restate.c
+    if (k->sweeps < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "slice sweeps must be at least 1");
   } else if (k->kind != ASMC_KERNEL_IDEALIZED && k->kind != ASMC_KERNEL_IDENTITY) {
     return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown kernel kind");
   }
@@ -259,7 +261,8 @@ KernelCfg make_kcfg(const asmc_kernel_desc* k) {
   c.sweeps = k->sweeps;
   c.leapfrog = k->leapfrog;
   for (int i = 0; i < k->n_step_sizes && i < ASMC_MAX_STEP_SIZES; ++i) c.steps[i] = k->step_sizes[i];
-  if (c.kind != ASMC_KERNEL_RWMH && c.kind != ASMC_KERNEL_HMC) {
+  if (c.kind == ASMC_KERNEL_SLICE) c.n_steps = 1;
+  if (c.kind != ASMC_KERNEL_RWMH && c.kind != ASMC_KERNEL_HMC && c.kind != ASMC_KERNEL_SLICE) {
     c.n_steps = 1;
     c.sweeps = 1;
   }
@@ -278,15 +281,15 @@ asmc_exec default_exec() {
 
 int check_smem(Layout L, uint64_t d, int rows, int nacc);
 
-int choose_layout_impl(const asmc_exec& ex, uint64_t d, Layout* L);
+int choose_layout_impl(const asmc_exec& ex, int kind, uint64_t d, Layout* L);
 
 // rows / nacc: per-launch step rows and accumulators, for the shared-memory budget
-int choose_layout(const asmc_exec& ex, uint64_t d, Layout* L, int rows = 1, int nacc = kNAcc) {
-  TRY(choose_layout_impl(ex, d, L));
+int choose_layout(const asmc_exec& ex, int kind, uint64_t d, Layout* L, int rows = 1, int nacc = kNAcc) {
+  TRY(choose_layout_impl(ex, kind, d, L));
   return check_smem(*L, d, rows, nacc);
 }
 
-int choose_layout_impl(const asmc_exec& ex, uint64_t d, Layout* L) {
+int choose_layout_impl(const asmc_exec& ex, int kind, uint64_t d, Layout* L) {
   if (ex.rng != ASMC_RNG_XOSHIRO && ex.rng != ASMC_RNG_PHILOX)
     return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown rng %d", ex.rng);
   if (ex.precision != ASMC_PREC_FP64 && ex.precision != ASMC_PREC_FP32)
@@ -303,6 +306,11 @@ int choose_layout_impl(const asmc_exec& ex, uint64_t d, Layout* L) {
     return 0;
   }
   int lanes = ex.lanes;
+  if (kind == ASMC_KERNEL_SLICE) {  // elliptical slice: one lane per particle (pass_kernel)
+    if (lanes > 1) return fail(ASMC_ERR_CAPABILITY, "the slice kernel runs one lane per particle (lanes = 1)");
+    if (d > 1024) return fail(ASMC_ERR_CAPABILITY, "the slice kernel supports dim <= 1024");
+    lanes = 1;
+  }
   if (lanes == 0) lanes = d <= 16 ? 1 : (d <= 128 ? 4 : 32);
   if (lanes == 1 && d <= 1024) *L = Layout{1, d <= 16 ? 16 : 1024};
   else if (lanes == 4 || lanes == 32) *L = Layout{lanes, 0};  // shared-memory particle store
@@ -847,7 +855,7 @@ int asmc_run_sais_single(const asmc_target_desc* target, const asmc_kernel_desc*
   if (target->kind == ASMC_TARGET_ISING)
     return run_is_single(target, kernel, betas, T, n, ASMC_POLICY_NEVER, 0.5, seed, round, ex, out, false);
   Layout L;
-  TRY(choose_layout(ex, target->dim, &L, T, 4));
+  TRY(choose_layout(ex, kernel->kind, target->dim, &L, T, 4));
   DevCtx* C;
   TRY(get_ctx(ex.device, &C, ex.stream));
   const double t0 = now_s();
@@ -884,7 +892,7 @@ int asmc_run_smc(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
   if (target->kind == ASMC_TARGET_ISING)
     return run_is_single(target, kernel, betas, T, n, policy, rho, seed, round, ex, out, true);
   Layout L;
-  TRY(choose_layout(ex, target->dim, &L));
+  TRY(choose_layout(ex, kernel->kind, target->dim, &L));
   DevCtx* C;
   TRY(get_ctx(ex.device, &C, ex.stream));
   const double t0 = now_s();
@@ -947,7 +955,7 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
     TRY(is_check(target, kernel, ex));
     L = Layout{1, 0};
   } else {
-    TRY(choose_layout_impl(ex, target->dim, &L));
+    TRY(choose_layout_impl(ex, kernel->kind, target->dim, &L));
   }
   // The (N_k, T_k) plan depends on the budget rule only, so the whole round
   // loop is enqueued up front; only the betas are data-dependent (device).
@@ -1072,7 +1080,7 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
   if (ex.precision == ASMC_PREC_FP64)
     return fail(ASMC_ERR_CAPABILITY, "sharded partials use the fp32 tree fold; fp64 reference order is single-GPU");
   Layout L;
-  TRY(choose_layout(ex, target->dim, &L, T, 4));
+  TRY(choose_layout(ex, kernel->kind, target->dim, &L, T, 4));
   DevCtx* C;
   TRY(get_ctx(ex.device, &C, ex.stream));
   const uint64_t nloc = p_end - p_begin, nblk = nblocks(nloc);
@@ -1156,7 +1164,7 @@ int asmc_trajectories(const asmc_target_desc* target, const asmc_kernel_desc* ke
   TRY(check_pass_target(target, "asmc_trajectories"));
   const asmc_exec ex = exec ? *exec : default_exec();
   Layout L;
-  TRY(choose_layout(ex, target->dim, &L, T, 4));
+  TRY(choose_layout(ex, kernel->kind, target->dim, &L, T, 4));
   DevCtx* C;
   TRY(get_ctx(ex.device, &C, ex.stream));
   const uint64_t d = target->dim;
@@ -1482,7 +1490,7 @@ int asmc_run_zja(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
   const uint64_t n = o->n_particles, d = target->dim;
   if (out->capacity < 2) return fail(ASMC_ERR_INVALID_ARGUMENT, "output capacity must be at least 2");
   Layout L;
-  TRY(choose_layout(ex, d, &L));
+  TRY(choose_layout(ex, kernel->kind, d, &L));
   DevCtx* C;
   TRY(get_ctx(ex.device, &C, ex.stream));
   const PassArgs base = base_args(target, kernel);
@@ -1653,7 +1661,7 @@ int asmc_smc_shard_create(const asmc_target_desc* target, const asmc_kernel_desc
   TRY(check_pass_target(target, "sharded SSMC"));
   auto* h = new asmc_smc_shard;
   auto drop = [&](int rc) { delete h; return rc; };
-  int rc = choose_layout(ex, target->dim, &h->L);
+  int rc = choose_layout(ex, kernel->kind, target->dim, &h->L);
   if (rc) return drop(rc);
   DevCtx* C;
   if ((rc = get_ctx(ex.device, &C, ex.stream))) return drop(rc);

@@ -325,6 +325,7 @@ bool IsingTarget::device_descriptor(asmc_target_desc* o) const {
 
 // ---- kernel / engine ------------------------------------------------------
 void validate_kernel(const Kernel& k) {  // kernel.cpp:12-22
+  if (k.kind == KernelKind::slice && k.sweeps < 1) throw std::invalid_argument("slice sweeps must be at least 1");
   if (k.kind == KernelKind::hmc) {
     if (k.step_sizes.empty()) throw std::invalid_argument("hmc requires at least one step size");
     for (double s : k.step_sizes)

@@ -158,7 +158,8 @@ double log_normal_pdf(double x, double mu, double sigma);
 
 // ---- kernel.hpp -----------------------------------------------------------
 // hmc (new): Hamiltonian Monte Carlo cycling through step_sizes as epsilon
-enum class KernelKind { idealized_exact, rwmh_cycle, identity, hmc };
+// slice (new): elliptical slice sampling w.r.t. the Gaussian reference, `sweeps` updates
+enum class KernelKind { idealized_exact, rwmh_cycle, identity, hmc, slice };
 
 struct Kernel {
   KernelKind kind = KernelKind::idealized_exact;

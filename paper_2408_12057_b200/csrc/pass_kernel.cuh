@@ -29,6 +29,8 @@
 
 namespace asmcdev {
 
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
 enum PassMode : int { kModeSais = 0, kModeSmcInit = 1, kModeSmcStep = 2, kModeTraj = 3 };
 
 struct KernelCfg {
@@ -100,6 +102,14 @@ struct Exact {
     return L + beta * V;
   }
 
+  __device__ static double potential(const TgtParams& T, int d, const double* x) {
+    double V = 0.0;
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+    for (int k = 0; k < KMAX; ++k)
+      if (k < d) V += Tgt::v64(T, x[k]);
+    return V;
+  }
+
   __device__ static void init(const TgtParams& T, int d, double* x, Seq& st) {
 #pragma unroll(KMAX <= 64 ? KMAX : 1)
     for (int k = 0; k < KMAX; ++k)
@@ -158,6 +168,37 @@ struct Exact {
               if (k < d) x[k] = prop[k];
             lgx = lgp;
           }
+        }
+      }
+      return;
+    }
+    if (kc.kind == ASMC_KERNEL_SLICE) {
+      // oracle/restate.c:slice_move: elliptical slice w.r.t. eta = N(mu, sigma^2 I)
+      const double mu = Tgt::ref_draw(T, 0.0);
+      double nu[KMAX];
+      for (int sw = 0; sw < kc.sweeps; ++sw) {
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+        for (int k = 0; k < KMAX; ++k)
+          if (k < d) nu[k] = Tgt::ref_draw(T, (double)st.normal());
+        const double ll = beta == 0.0 ? 0.0 : beta * potential(T, d, x);
+        const double log_y = ll + log(st.uniform());
+        double theta = st.uniform() * kTwoPi;
+        double lo = theta - kTwoPi, hi = theta;
+        for (int it = 0; it < ASMC_SLICE_MAX_SHRINK; ++it) {
+          const double c = cos(theta), sn = sin(theta);
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+          for (int k = 0; k < KMAX; ++k)
+            if (k < d) prop[k] = mu + (x[k] - mu) * c + (nu[k] - mu) * sn;
+          const double llp = beta == 0.0 ? 0.0 : beta * potential(T, d, prop);
+          if (llp > log_y) {
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+            for (int k = 0; k < KMAX; ++k)
+              if (k < d) x[k] = prop[k];
+            break;
+          }
+          if (theta < 0.0) lo = theta;
+          else hi = theta;
+          theta = lo + (hi - lo) * st.uniform();
         }
       }
       return;
@@ -290,6 +331,44 @@ struct Fast {
               for (int k = 0; k < KMAX; ++k)
                 if (k < d) x[k] = prop[k];
             }
+          }
+        }
+      }
+      return;
+    }
+    if (kc.kind == ASMC_KERNEL_SLICE) {  // elliptical slice, one lane per particle
+      if constexpr (kSeq) {
+        const typename Tgt::F32 kb = Tgt::f32(T, beta), k0 = Tgt::f32(T, 0.0);
+        const float mu = (float)Tgt::ref_draw(T, 0.0);
+        for (int sw = 0; sw < kc.sweeps; ++sw) {
+          float nu[KMAX], prop[KMAX];
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+          for (int k = 0; k < KMAX; ++k)
+            if (k < d) nu[k] = (float)Tgt::ref_draw(T, (double)src.seq.normal());
+          const double log_u = log(src.seq.uniform());
+          double theta = src.seq.uniform() * kTwoPi;
+          double lo = theta - kTwoPi, hi = theta;
+          for (int it = 0; it < ASMC_SLICE_MAX_SHRINK; ++it) {
+            const float c = (float)cos(theta), sn = (float)sin(theta);
+            float dl = 0.0f;  // beta (V(x') - V(x)) as a difference of log-density differences
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+            for (int k = 0; k < KMAX; ++k) {
+              if (k < d) {
+                const float xp = mu + (x[k] - mu) * c + (nu[k] - mu) * sn;
+                const float h = xp - x[k];
+                dl += Tgt::dlg(kb, x[k], h) - Tgt::dlg(k0, x[k], h);
+                prop[k] = xp;
+              }
+            }
+            if ((double)dl > log_u) {
+#pragma unroll(KMAX <= 64 ? KMAX : 1)
+              for (int k = 0; k < KMAX; ++k)
+                if (k < d) x[k] = prop[k];
+              break;
+            }
+            if (theta < 0.0) lo = theta;
+            else hi = theta;
+            theta = lo + (hi - lo) * src.seq.uniform();
           }
         }
       }
