@@ -22,6 +22,7 @@
  *                            resample + gather (src/engine.cpp:61-80,161-173)
  *   asmc_run_zja          <- asmc::run_zja            include/asmc/drivers.hpp:88-111, src/drivers.cpp:234-341
  *   asmc_zja_next_beta    <- asmc::zja_next_beta      include/asmc/schedule.hpp:51-64, src/schedule.cpp:199-264
+ *   asmc_run_pt           <- asmc::run_pt (NRPT)      include/asmc/pt.hpp:14-77, src/pt.cpp:21-152
  *   asmc_systematic_resample <- asmc::systematic_resample  src/engine.cpp:61-80
  *   asmc_ess              <- asmc::ess                src/engine.cpp:46-59
  *   asmc_barrier_estimate <- asmc::barrier_estimate   src/schedule.cpp:41-56
@@ -301,6 +302,38 @@ int asmc_run_zja(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
 int asmc_zja_next_beta(const asmc_target_desc* target, double beta, const double* positions,
                        uint64_t n_particles, const double* log_weights, double delta_star,
                        double tol, const asmc_exec* exec, double* beta_next, int32_t* warning);
+
+/* ---- non-reversible parallel tempering (NRPT) ---- */
+/* PtOptions (pt.hpp:18-24) + `replicas`: independent runs with seeds seed .. seed +
+ * replicas - 1, all in one launch (one CTA per run, one thread per level). */
+typedef struct asmc_pt_opts {
+  int32_t iterations;
+  int32_t burn_in; /* -1 -> iterations / 10 */
+  uint64_t seed;
+  uint64_t round;
+  int32_t replicas;
+  int32_t reserved;
+} asmc_pt_opts;
+
+/* PtReport (pt.hpp:45-58) per replica r; caller-owned arrays, any may be NULL:
+ *   log_z_hat[r], trace[(r * iterations + it) * (levels + 1) + n],
+ *   swap_accepted[(r * iterations + it) * (levels + 1) + lo],
+ *   swap_attempts / swap_accepts[r * (levels + 1) + lo] */
+typedef struct asmc_pt_out {
+  double* log_z_hat;
+  double* trace;
+  uint8_t* swap_accepted;
+  uint64_t* swap_attempts;
+  uint64_t* swap_accepts;
+  uint64_t kernel_applications; /* per replica: levels * iterations */
+  double wall_seconds;
+  int32_t burn_in;              /* resolved */
+  int32_t reserved;
+} asmc_pt_out;
+
+/* levels <= 255; targets with a device pass (shift, mixture, scale), d <= 1024 */
+int asmc_run_pt(const asmc_target_desc* target, const asmc_kernel_desc* kernel, const double* betas,
+                int32_t levels, const asmc_pt_opts* options, const asmc_exec* exec, asmc_pt_out* out);
 
 /* ---- parity hooks ---- */
 /* key = {seed, round, particle, step, substep} (rng.hpp:11-17) */

@@ -106,6 +106,14 @@ class Oracle:
                    C.c_double(rho), C.c_uint64(seed), C.c_uint64(round), C.byref(rep))
         return self._finish(rep, bufs)
 
+    def run_pt(self, target, kernel, betas, iterations=1024, burn_in=-1, seed=0, round=1, replicas=1):
+        betas = np.ascontiguousarray(betas, dtype=np.float64)
+        L = len(betas) - 1
+        o, out, b = abi.pt_buffers(L, iterations, burn_in, seed, round, replicas)
+        self._call("ora_run_pt", C.byref(target), C.byref(kernel), _arr(betas, C.c_double), C.c_int32(L),
+                   C.byref(o), C.byref(out))
+        return abi.pt_finish(out, b)
+
     def run_zja(self, target, kernel, n, target_steps=32, delta_star=0.0, seed=0, max_steps=100000, workers=1):
         o = abi.zja_opts(n, target_steps, delta_star, seed, max_steps)
         out, keep = abi.zja_buffers(o)

@@ -29,6 +29,7 @@
 #include "asmc/engine.hpp"
 #include "asmc/errors.hpp"
 #include "asmc/kernel.hpp"
+#include "asmc/pt.hpp"
 #include "asmc/logsum.hpp"
 #include "asmc/rng.hpp"
 #include "asmc/schedule.hpp"
@@ -515,6 +516,34 @@ int ora_run_experiment(const char* config_text, const char* out_dir) {
     asmc::RunConfig c = asmc::parse_config_text(config_text);
     c.out_dir = out_dir;
     if (asmc::run_experiment(c) != 0) throw std::runtime_error("run_experiment failed");
+  });
+}
+
+// asmc::run_pt (pt.cpp:84-128) for replicas r = 0..R-1 with seeds seed + r
+int ora_run_pt(const asmc_target_desc* target, const asmc_kernel_desc* kernel, const double* betas,
+               int32_t levels, const asmc_pt_opts* o, asmc_pt_out* out) {
+  return guard([&] {
+    const auto tg = make_target(target);
+    const asmc::Kernel k = make_kernel(kernel);
+    const asmc::Schedule sched = make_schedule(betas, levels);
+    const std::size_t L1 = static_cast<std::size_t>(levels) + 1, I = o->iterations;
+    for (int r = 0; r < o->replicas; ++r) {
+      asmc::PtOptions po;
+      po.iterations = o->iterations;
+      po.burn_in = o->burn_in;
+      po.seed = o->seed + static_cast<std::uint64_t>(r);
+      po.round = o->round;
+      const asmc::PtReport rep = asmc::run_pt(*tg, k, sched, po);
+      if (out->log_z_hat) out->log_z_hat[r] = rep.log_z_hat;
+      if (out->trace) std::memcpy(out->trace + r * I * L1, rep.trace.values.data(), sizeof(double) * I * L1);
+      if (out->swap_accepted) std::memcpy(out->swap_accepted + r * I * L1, rep.swap_accepted.data(), I * L1);
+      if (out->swap_attempts)
+        std::memcpy(out->swap_attempts + r * L1, rep.swap_attempts.data(), sizeof(std::uint64_t) * L1);
+      if (out->swap_accepts)
+        std::memcpy(out->swap_accepts + r * L1, rep.swap_accepts.data(), sizeof(std::uint64_t) * L1);
+      out->kernel_applications = rep.kernel_applications;
+      out->burn_in = rep.burn_in;
+    }
   });
 }
 

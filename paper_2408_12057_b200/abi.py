@@ -98,6 +98,42 @@ class ZjaOut(C.Structure):
                 ("pilot_lambda", C.POINTER(C.c_double)), ("pilot", Report)]
 
 
+class PtOpts(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("burn_in", C.c_int32), ("seed", C.c_uint64), ("round", C.c_uint64),
+                ("replicas", C.c_int32), ("reserved", C.c_int32)]
+
+
+class PtOut(C.Structure):
+    _fields_ = [("log_z_hat", C.POINTER(C.c_double)), ("trace", C.POINTER(C.c_double)),
+                ("swap_accepted", C.POINTER(C.c_uint8)), ("swap_attempts", C.POINTER(C.c_uint64)),
+                ("swap_accepts", C.POINTER(C.c_uint64)), ("kernel_applications", C.c_uint64),
+                ("wall_seconds", C.c_double), ("burn_in", C.c_int32), ("reserved", C.c_int32)]
+
+
+def pt_buffers(levels, iterations, burn_in=-1, seed=0, round=1, replicas=1):
+    """(PtOpts, PtOut, numpy buffers) for asmc_run_pt / ora_run_pt."""
+    import numpy as np
+    o = PtOpts()
+    o.iterations, o.burn_in, o.seed, o.round, o.replicas = iterations, burn_in, seed, round, replicas
+    L1 = levels + 1
+    b = dict(log_z_hat=np.zeros(replicas), trace=np.zeros((replicas, iterations, L1)),
+             swap_accepted=np.zeros((replicas, iterations, L1), np.uint8),
+             swap_attempts=np.zeros((replicas, L1), np.uint64), swap_accepts=np.zeros((replicas, L1), np.uint64))
+    out = PtOut()
+    out.log_z_hat = b["log_z_hat"].ctypes.data_as(C.POINTER(C.c_double))
+    out.trace = b["trace"].ctypes.data_as(C.POINTER(C.c_double))
+    out.swap_accepted = b["swap_accepted"].ctypes.data_as(C.POINTER(C.c_uint8))
+    out.swap_attempts = b["swap_attempts"].ctypes.data_as(C.POINTER(C.c_uint64))
+    out.swap_accepts = b["swap_accepts"].ctypes.data_as(C.POINTER(C.c_uint64))
+    return o, out, b
+
+
+def pt_finish(out, b):
+    d = dict(b)
+    d.update(kernel_applications=out.kernel_applications, wall_seconds=out.wall_seconds, burn_in=out.burn_in)
+    return d
+
+
 def zja_opts(n, target_steps=32, delta_star=0.0, seed=0, max_steps=100000):
     o = ZjaOpts()
     o.n_particles, o.target_steps, o.max_steps, o.delta_star, o.seed = n, target_steps, max_steps, delta_star, seed

@@ -281,6 +281,17 @@ def peak_normals(device, blocks, quads_per_thread):
     return s.value
 
 
+def run_pt(target, kernel, betas, iterations=1024, burn_in=-1, seed=0, round=1, replicas=1, exec_=None):
+    """asmc::run_pt (pt.cpp:84-128) for `replicas` seeds at once; returns per-replica arrays."""
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    L = len(betas) - 1
+    o, out, b = abi.pt_buffers(L, iterations, burn_in, seed, round, replicas)
+    ex = exec_ or abi.execopts()
+    _check(lib().asmc_run_pt(C.byref(target), C.byref(kernel), _arr(betas, C.c_double), C.c_int32(L), C.byref(o),
+                             C.byref(ex), C.byref(out)))
+    return abi.pt_finish(out, b)
+
+
 def run_zja(target, kernel, n, target_steps=32, delta_star=0.0, seed=0, max_steps=100000, exec_=None):
     """asmc::run_zja (drivers.cpp:234-341) on the device; returns abi.zja_finish's dict."""
     o = abi.zja_opts(n, target_steps, delta_star, seed, max_steps)
@@ -388,5 +399,5 @@ EXPORTED = [
     "asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes",
     "asmc_smc_shard_step", "asmc_smc_shard_decide", "asmc_smc_shard_plan", "asmc_smc_shard_pack",
     "asmc_smc_shard_accept", "asmc_smc_shard_report", "asmc_smc_shard_state", "asmc_run_zja",
-    "asmc_zja_next_beta",
+    "asmc_zja_next_beta", "asmc_run_pt",
 ]

@@ -19,6 +19,7 @@
 #include "engine_kernels.h"
 #include "ising.h"
 #include "logistic.h"
+#include "pt.h"
 #include "zja.h"
 
 using namespace asmcdev;
@@ -1608,6 +1609,104 @@ int asmc_run_zja(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
 }
 
 }  // extern "C"
+
+// ==================================================================== NRPT
+namespace {
+// LogAccumulator (logsum.hpp:18-49), host copy for the stepping-stone estimator
+struct HostLogAcc {
+  double max = -HUGE_VAL, sum = 0.0;
+  void add(double l) {
+    if (l == -HUGE_VAL) return;
+    if (l <= max) {
+      sum += std::exp(l - max);
+    } else {
+      sum = sum * std::exp(max - l) + 1.0;
+      max = l;
+    }
+  }
+  double log_total() const { return max == -HUGE_VAL ? -HUGE_VAL : max + std::log(sum); }
+};
+}  // namespace
+
+extern "C" int asmc_run_pt(const asmc_target_desc* target, const asmc_kernel_desc* kernel, const double* betas,
+                           int32_t levels, const asmc_pt_opts* o, const asmc_exec* exec, asmc_pt_out* out) {
+  if (!o || !out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null options or output");
+  TRY(check_schedule(betas, levels));
+  // PtOptions::validate (pt.cpp:14-19)
+  if (o->iterations < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "iterations must be at least 1");
+  if (o->burn_in >= o->iterations)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "burn_in must leave at least one recorded iteration");
+  if (o->replicas < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "replicas must be at least 1");
+  TRY(check_pair(target, kernel));
+  TRY(check_pass_target(target, "asmc_run_pt"));
+  if (levels > kPtMaxLevels) return fail(ASMC_ERR_CAPABILITY, "at most %d levels per run on the device", kPtMaxLevels);
+  if (target->dim > 1024) return fail(ASMC_ERR_CAPABILITY, "asmc_run_pt supports dim <= 1024");
+  const asmc_exec ex = exec ? *exec : default_exec();
+  if (ex.rng != ASMC_RNG_XOSHIRO && ex.rng != ASMC_RNG_PHILOX) return fail(ASMC_ERR_INVALID_ARGUMENT, "unknown rng");
+  const bool fp64 = ex.precision == ASMC_PREC_FP64;
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C, ex.stream));
+  const double t0 = now_s();
+  const int L = levels, I = o->iterations, R = o->replicas;
+  const int burn = o->burn_in < 0 ? I / 10 : o->burn_in;
+  const size_t rows = (size_t)R * I * (L + 1);
+  DBuf<double> d_betas, trace;
+  DBuf<uint8_t> acc;
+  DBuf<char> scratch;
+  TRY(d_betas.alloc(L + 1, C->stream));
+  TRY(trace.alloc(rows, C->stream));
+  TRY(acc.alloc(rows, C->stream));
+  TRY(scratch.alloc((size_t)R * (L + 1) * target->dim * (fp64 ? 8 : 4), C->stream));
+  CU(cudaMemcpyAsync(d_betas.p, betas, sizeof(double) * (L + 1), cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemsetAsync(acc.p, 0, rows, C->stream));
+  PtArgs A;
+  std::memset(&A, 0, sizeof A);
+  A.tg = make_params(target);
+  A.kc = make_kcfg(kernel);
+  A.betas = d_betas.p;
+  A.levels = L;
+  A.iterations = I;
+  A.seed0 = o->seed;
+  A.round = o->round;
+  A.replicas = R;
+  A.scratch = scratch.p;
+  A.trace = trace.p;
+  A.accepted = acc.p;
+  LCH(launch_pt(A, fp64, ex.rng, C->stream));
+  std::vector<double> tr(rows);
+  std::vector<uint8_t> ac(rows);
+  CU(cudaMemcpyAsync(tr.data(), trace.p, rows * sizeof(double), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaMemcpyAsync(ac.data(), acc.p, rows, cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  if (out->trace) std::memcpy(out->trace, tr.data(), rows * sizeof(double));
+  if (out->swap_accepted) std::memcpy(out->swap_accepted, ac.data(), rows);
+  const double log_used = std::log((double)(I - burn));
+  for (int r = 0; r < R; ++r) {
+    const double* t = tr.data() + (size_t)r * I * (L + 1);
+    double log_z = 0.0;  // stepping_stone (pt.cpp:130-152)
+    for (int n = 1; n <= L; ++n) {
+      const double delta_beta = betas[n] - betas[n - 1];
+      HostLogAcc a;
+      for (int it = burn; it < I; ++it) a.add(delta_beta * t[(size_t)it * (L + 1) + n - 1]);
+      log_z += a.log_total() - log_used;
+    }
+    if (out->log_z_hat) out->log_z_hat[r] = log_z;
+    for (int lo = 0; lo <= L; ++lo) {  // run_pt's attempt / accept counters (pt.cpp:110-121)
+      uint64_t att = 0, accn = 0;
+      for (int it = 0; it < I; ++it)
+        if (lo + 1 <= L && (lo & 1) == (it & 1)) {
+          ++att;
+          accn += ac[((size_t)r * I + it) * (L + 1) + lo];
+        }
+      if (out->swap_attempts) out->swap_attempts[(size_t)r * (L + 1) + lo] = att;
+      if (out->swap_accepts) out->swap_accepts[(size_t)r * (L + 1) + lo] = accn;
+    }
+  }
+  out->kernel_applications = (uint64_t)L * (uint64_t)I;
+  out->wall_seconds = now_s() - t0;
+  out->burn_in = burn;
+  return 0;
+}
 
 // ============================================================ sharded SSMC
 // One particle shard of a multi-GPU run_smc (include/asmc_b200.h).  The state,

@@ -644,6 +644,78 @@ ZjaOutcome run_zja(const AnnealedTarget& target, const Kernel& kernel, const Zja
   return res;
 }
 
+void PtOptions::validate() const {  // pt.cpp:14-19
+  if (iterations < 1) throw std::invalid_argument("iterations must be at least 1");
+  if (burn_in >= iterations) throw std::invalid_argument("burn_in must leave at least one recorded iteration");
+}
+
+std::vector<PtReport> run_pt_replicas(const AnnealedTarget& target, const Kernel& kernel, const Schedule& schedule,
+                                      const PtOptions& o, int replicas) {
+  schedule.validate();
+  o.validate();
+  validate_kernel(kernel);
+  if (replicas < 1) throw std::invalid_argument("replicas must be at least 1");
+  const asmc_target_desc td = descriptor(target);
+  const asmc_kernel_desc kd = kernel_desc(kernel);
+  const asmc_exec ex = exec_of(o.rng, o.precision, o.device, 0);
+  const int L = schedule.steps(), I = o.iterations;
+  const std::size_t rows = static_cast<std::size_t>(replicas) * I * (L + 1);
+  std::vector<double> lz(replicas), tr(rows);
+  std::vector<std::uint8_t> ac(rows);
+  std::vector<std::uint64_t> att(static_cast<std::size_t>(replicas) * (L + 1)), acc(att.size());
+  asmc_pt_opts po{I, o.burn_in, o.seed, o.round, replicas, 0};
+  asmc_pt_out out{lz.data(), tr.data(), ac.data(), att.data(), acc.data(), 0, 0.0, 0, 0};
+  check(asmc_run_pt(&td, &kd, schedule.betas.data(), L, &po, &ex, &out));
+  std::vector<PtReport> res(replicas);
+  const std::size_t per = static_cast<std::size_t>(I) * (L + 1);
+  for (int r = 0; r < replicas; ++r) {
+    PtReport& p = res[r];
+    p.schedule = schedule;
+    p.iterations = I;
+    p.burn_in = out.burn_in;
+    p.log_z_hat = lz[r];
+    p.trace.iterations = I;
+    p.trace.levels = L;
+    p.trace.values.assign(tr.begin() + r * per, tr.begin() + (r + 1) * per);
+    p.swap_accepted.assign(ac.begin() + r * per, ac.begin() + (r + 1) * per);
+    p.swap_attempts.assign(att.begin() + r * (L + 1), att.begin() + (r + 1) * (L + 1));
+    p.swap_accepts.assign(acc.begin() + r * (L + 1), acc.begin() + (r + 1) * (L + 1));
+    p.kernel_applications = out.kernel_applications;
+    p.wall_seconds = out.wall_seconds;
+  }
+  return res;
+}
+
+PtReport run_pt(const AnnealedTarget& target, const Kernel& kernel, const Schedule& schedule, const PtOptions& o) {
+  return run_pt_replicas(target, kernel, schedule, o, 1)[0];
+}
+
+double stepping_stone(const PotentialTrace& trace, const Schedule& schedule, int burn_in) {  // pt.cpp:130-152
+  schedule.validate();
+  const int levels = schedule.steps();
+  if (trace.levels != levels) throw std::invalid_argument("trace level count does not match schedule");
+  if (burn_in < 0 || burn_in >= trace.iterations)
+    throw std::invalid_argument("burn_in must leave at least one recorded iteration");
+  const double log_used = std::log(static_cast<double>(trace.iterations - burn_in));
+  double log_z = 0.0;
+  for (int n = 1; n <= levels; ++n) {
+    const double delta_beta = schedule.betas[n] - schedule.betas[n - 1];
+    double mx = kNegInf, sum = 0.0;  // LogAccumulator (logsum.hpp:18-49)
+    for (int it = burn_in; it < trace.iterations; ++it) {
+      const double l = delta_beta * trace.at(it, n - 1);
+      if (l == kNegInf) continue;
+      if (l <= mx) {
+        sum += std::exp(l - mx);
+      } else {
+        sum = sum * std::exp(mx - l) + 1.0;
+        mx = l;
+      }
+    }
+    log_z += (mx == kNegInf ? kNegInf : mx + std::log(sum)) - log_used;
+  }
+  return log_z;
+}
+
 SaisMemoryProfile sais_memory_profile(int total_steps, int workers, std::size_t chunk) {
   // drivers.cpp:59-70 semantics: adaptation storage 3(T+1) + (T+1), never N
   if (total_steps < 1) throw std::invalid_argument("profile needs at least one step");

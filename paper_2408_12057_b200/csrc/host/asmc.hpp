@@ -320,6 +320,48 @@ struct ZjaOutcome {
 
 ZjaOutcome run_zja(const AnnealedTarget& target, const Kernel& kernel, const ZjaOptions& options);
 
+// ---- pt.hpp (non-reversible parallel tempering) -------------------------------
+struct PtOptions {
+  int iterations = 1024;
+  int burn_in = -1;  // -1 -> iterations / 10
+  std::uint64_t seed = 0;
+  std::uint64_t round = 1;
+  // device execution (new)
+  Rng rng = Rng::xoshiro;
+  Precision precision = Precision::fp64;
+  int device = 0;
+  void validate() const;
+};
+
+struct PotentialTrace {
+  int iterations = 0;
+  int levels = 0;
+  std::vector<double> values;
+  double at(int iteration, int level) const {
+    return values[static_cast<std::size_t>(iteration) * (levels + 1) + level];
+  }
+};
+
+struct PtReport {
+  Schedule schedule;
+  int iterations = 0;
+  int burn_in = 0;
+  double log_z_hat = 0.0;
+  PotentialTrace trace;
+  std::vector<std::uint8_t> swap_accepted;
+  std::vector<std::uint64_t> swap_attempts;
+  std::vector<std::uint64_t> swap_accepts;
+  std::uint64_t kernel_applications = 0;
+  double wall_seconds = 0.0;
+};
+
+PtReport run_pt(const AnnealedTarget& target, const Kernel& kernel, const Schedule& schedule,
+                const PtOptions& options);
+// new: `replicas` independent runs (seeds seed + r) in one device launch
+std::vector<PtReport> run_pt_replicas(const AnnealedTarget& target, const Kernel& kernel,
+                                      const Schedule& schedule, const PtOptions& options, int replicas);
+double stepping_stone(const PotentialTrace& trace, const Schedule& schedule, int burn_in);
+
 struct SaisMemoryProfile {
   std::size_t moment_accumulators = 0;
   std::size_t signed_accumulators = 0;

@@ -17,6 +17,7 @@ SUMMARY = "round,N,T,log_Z_hat,elbo_hat,Lambda_hat,kernel_applications,wall_cloc
 TRACE = "round,t,beta,log_g0,log_g1,log_g2,ess,resampled,cum_log_Z"
 SCHEDULE = "round,t,beta"
 BARRIER = "round,t,beta,D_hat,Lambda_hat,lambda_hat"
+PT_TRACE = "iteration,level,beta,V,swap_accepted"
 
 
 def fmt(v):
@@ -98,3 +99,30 @@ def write_experiment(out_dir, replicates, local_barrier, timing=False):
     finally:
         for f in files.values():
             f.close()
+
+
+def write_pt_experiment(out_dir, betas, reports, timing=False):
+    """run_pt_driver's outputs (experiment.cpp:143-186) from capi.run_pt / oracle
+    run_pt (all replicas of one call): summary.csv rows per replica, schedule.csv and
+    pt_trace.csv from replicate 0, trace.csv and barrier.csv header-only."""
+    os.makedirs(out_dir, exist_ok=True)
+    nan = float("nan")
+    L = len(betas) - 1
+    with open(os.path.join(out_dir, "summary.csv"), "w", newline="\n") as f:
+        f.write(SUMMARY + "\n")
+        for r in range(len(reports["log_z_hat"])):
+            f.write(f"1,{L},{reports['trace'].shape[1]},{fmt(reports['log_z_hat'][r])},{fmt(nan)},{fmt(nan)},"
+                    f"{reports['kernel_applications']},{fmt(reports['wall_seconds'] if timing else 0.0)}\n")
+    for name, hdr in (("trace.csv", TRACE), ("barrier.csv", BARRIER)):
+        with open(os.path.join(out_dir, name), "w", newline="\n") as f:
+            f.write(hdr + "\n")
+    with open(os.path.join(out_dir, "schedule.csv"), "w", newline="\n") as f:
+        f.write(SCHEDULE + "\n")
+        for t in range(L + 1):
+            f.write(f"1,{t},{fmt(betas[t])}\n")
+    with open(os.path.join(out_dir, "pt_trace.csv"), "w", newline="\n") as f:
+        f.write(PT_TRACE + "\n")
+        tr, acc = reports["trace"][0], reports["swap_accepted"][0]
+        for it in range(tr.shape[0]):
+            for n in range(L + 1):
+                f.write(f"{it},{n},{fmt(betas[n])},{fmt(tr[it, n])},{int(acc[it, n])}\n")

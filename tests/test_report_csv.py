@@ -146,3 +146,20 @@ def test_sharded_csvs_byte_identical(tmp_path):
         dirs.append(_read(d))
     assert dirs[0] == dirs[1]
     assert dirs[0]["summary.csv"].count("\n") == 4
+
+
+PT_TEXT = ("driver = pt\ntarget = gaussian_shift\ndim = 2\nkernel = rwmh\nlevels = 6\niterations = 200\n"
+           "seed = 3\nreplicates = 3\nworkers = 1\n")
+
+
+def test_pt_writer_reproduces_reference_bytes(tmp_path):
+    ref_files = _reference_csvs(PT_TEXT, tmp_path)
+    o = oracle.load("ref", XO)
+    betas = np.array([t / 6 for t in range(6)] + [1.0])
+    r = o.run_pt(abi.gaussian_shift(0.0, 1.0, 1.0, 2), abi.kernel(abi.KERNEL_RWMH, (0.1, 1.0, 10.0), 1), betas,
+                 iterations=200, seed=3, replicas=3)
+    report_csv.write_pt_experiment(str(tmp_path / "ours"), betas, r)
+    ours = _read(str(tmp_path / "ours"))
+    ours["pt_trace.csv"] = open(str(tmp_path / "ours" / "pt_trace.csv")).read()
+    ref_files["pt_trace.csv"] = open(str(tmp_path / "ref" / "pt_trace.csv")).read()
+    assert ours == ref_files
