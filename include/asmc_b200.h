@@ -373,6 +373,10 @@ int asmc_budget(uint64_t n_particles, int32_t steps, uint64_t dim, uint64_t memo
  * and the algorithmic normal draws each launch had to make. */
 int asmc_profile_enable(int on);
 int asmc_profile_collect(double* ms, double* normals, int max_launches, int* n_launches);
+/* same, plus the normals each launch actually generated (the shared-memory RWMH pass
+ * draws fewer than the algorithmic count when proposals are rejected early); equals
+ * the algorithmic count for launches without a counter */
+int asmc_profile_collect_drawn(double* ms, double* units, double* drawn, int max_launches, int* n_launches);
 /* Generator peak: `blocks` CTAs x 256 threads each drawing quads_per_thread
  * Philox quads (4 fp32 normals) in registers; returns kernel seconds. */
 int asmc_peak_normals(int32_t device, int32_t blocks, uint64_t quads_per_thread, double* seconds);

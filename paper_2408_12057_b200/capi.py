@@ -264,14 +264,17 @@ def profile_enable(on=True):
     _check(lib().asmc_profile_enable(C.c_int(1 if on else 0)))
 
 
-def profile_collect(max_launches=65536):
+def profile_collect(max_launches=65536, drawn=False):
+    """(ms, algorithmic units) per profiled launch; with drawn=True also the normals
+    each launch actually generated (early-rejected RWMH proposals draw fewer)."""
     ms = np.zeros(max_launches)
     nrm = np.zeros(max_launches)
+    drw = np.zeros(max_launches)
     cnt = C.c_int()
-    _check(lib().asmc_profile_collect(_arr(ms, C.c_double), _arr(nrm, C.c_double),
-                                      C.c_int(max_launches), C.byref(cnt)))
+    _check(lib().asmc_profile_collect_drawn(_arr(ms, C.c_double), _arr(nrm, C.c_double), _arr(drw, C.c_double),
+                                            C.c_int(max_launches), C.byref(cnt)))
     k = min(cnt.value, max_launches)
-    return ms[:k], nrm[:k]
+    return (ms[:k], nrm[:k], drw[:k]) if drawn else (ms[:k], nrm[:k])
 
 
 def peak_normals(device, blocks, quads_per_thread):
@@ -399,5 +402,5 @@ EXPORTED = [
     "asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes",
     "asmc_smc_shard_step", "asmc_smc_shard_decide", "asmc_smc_shard_plan", "asmc_smc_shard_pack",
     "asmc_smc_shard_accept", "asmc_smc_shard_report", "asmc_smc_shard_state", "asmc_run_zja",
-    "asmc_zja_next_beta", "asmc_run_pt",
+    "asmc_zja_next_beta", "asmc_run_pt", "asmc_profile_collect_drawn",
 ]

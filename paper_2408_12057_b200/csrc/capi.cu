@@ -334,7 +334,8 @@ int check_smem(Layout L, uint64_t d, int rows, int nacc) {
 // the launching stream around each pass, plus its algorithmic normal draws.
 struct ProfRec {
   cudaEvent_t a, b;
-  double normals;
+  double normals;                        // algorithmic units of the launch
+  unsigned long long* drawn = nullptr;   // device counter: normals actually generated (smem pass)
 };
 thread_local bool g_prof = false;
 thread_local std::vector<ProfRec> g_prof_recs;
@@ -354,14 +355,19 @@ cudaError_t launch_pass(const asmc_exec& ex, Layout L, const PassArgs& A, uint64
                         cudaStream_t s) {
   if (blocks == 0) return cudaSuccess;
   ProfRec rec{};
+  PassArgs Ap = A;
   if (g_prof) {
     cudaEventCreate(&rec.a);
     cudaEventCreate(&rec.b);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&rec.drawn), sizeof(unsigned long long), s) == cudaSuccess) {
+      cudaMemsetAsync(rec.drawn, 0, sizeof(unsigned long long), s);
+      Ap.drawn = rec.drawn;
+    }
     cudaEventRecord(rec.a, s);
   }
   const cudaError_t e = ex.precision == ASMC_PREC_FP64
-                            ? launch_pass_fp64(A.tg.kind, ex.rng, L, A, blocks, s)
-                            : launch_pass_fp32(A.tg.kind, ex.rng, L, A, blocks, s);
+                            ? launch_pass_fp64(A.tg.kind, ex.rng, L, Ap, blocks, s)
+                            : launch_pass_fp32(A.tg.kind, ex.rng, L, Ap, blocks, s);
   if (g_prof) {
     cudaEventRecord(rec.b, s);
     rec.normals = pass_normals(A, A.n_local);
@@ -1368,7 +1374,7 @@ int asmc_profile_enable(int on) {
   return 0;
 }
 
-int asmc_profile_collect(double* ms, double* normals, int max_launches, int* n_launches) {
+int asmc_profile_collect_drawn(double* ms, double* normals, double* drawn, int max_launches, int* n_launches) {
   int i = 0;
   for (auto& r : g_prof_recs) {
     CU(cudaEventSynchronize(r.b));
@@ -1377,7 +1383,13 @@ int asmc_profile_collect(double* ms, double* normals, int max_launches, int* n_l
       CU(cudaEventElapsedTime(&t, r.a, r.b));
       if (ms) ms[i] = t;
       if (normals) normals[i] = r.normals;
+      if (drawn) {
+        unsigned long long c = 0;
+        if (r.drawn) CU(cudaMemcpy(&c, r.drawn, sizeof c, cudaMemcpyDeviceToHost));
+        drawn[i] = r.drawn ? (double)c : r.normals;
+      }
     }
+    if (r.drawn) cudaFree(r.drawn);
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
     ++i;
@@ -1385,6 +1397,10 @@ int asmc_profile_collect(double* ms, double* normals, int max_launches, int* n_l
   if (n_launches) *n_launches = i;
   g_prof_recs.clear();
   return 0;
+}
+
+int asmc_profile_collect(double* ms, double* normals, int max_launches, int* n_launches) {
+  return asmc_profile_collect_drawn(ms, normals, nullptr, max_launches, n_launches);
 }
 
 int asmc_peak_normals(int32_t device, int32_t blocks, uint64_t quads_per_thread, double* seconds) {

@@ -33,7 +33,7 @@ template <int G, bool kHmc>
 static cudaError_t go_smem_k(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
   const int nacc = A.mode == kModeSmcStep ? kNAcc : 4;
   const int rows = A.t_end - A.t_begin + 1 > 0 ? A.t_end - A.t_begin + 1 : 1;
-  const size_t bytes = smem_pass_bytes(G, A.tg.dim, rows - 1, nacc, CacheWords<Tgt>::value);
+  const size_t bytes = smem_pass_bytes(G, A.tg.dim, rows - 1, nacc, RowWords<Tgt, kHmc>::value);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(pass_smem_kernel<Tgt, G, kHmc>,

@@ -63,6 +63,7 @@ struct PassArgs {
   double* rec_x;         // kModeTraj: [(i * (T+1) + t) * dim + k]
   double* rec_lw;        // kModeTraj: [i * (T+1) + t]
   int* err;
+  unsigned long long* drawn;  // profiling: normals actually generated (null = off)
 };
 
 // coordinate owned by (lane, slot k): quads of 4 consecutive coordinates dealt

@@ -34,9 +34,19 @@ struct CacheWords {
   static constexpr int value = Tgt::kCacheV ? 2 : 1;
 };
 
+// RWMH on uncached targets keeps two rows per particle: the MH pass writes the
+// proposal x + s z into the spare row and an accepted proposal just flips rows
+// (no regeneration of its normals).  Same footprint as a cached target's x + vterm.
+template <class Tgt, bool kHmc>
+struct RowWords {
+  static constexpr bool kDual = !kHmc && !Tgt::kCacheV;
+  static constexpr int value = CacheWords<Tgt>::value * (kDual ? 2 : 1);
+};
+
 template <class Tgt, int G, bool kHmc = false>
 struct SmemOps {
   static constexpr bool kCache = Tgt::kCacheV;
+  static constexpr bool kDual = RowWords<Tgt, kHmc>::kDual;
 
   // normals 4q .. 4q+3 of the draw set based at `base`
   __device__ static void quad(const PhiloxKey& k, uint64_t base, int q, float z[4]) {
@@ -59,14 +69,16 @@ struct SmemOps {
     }
   }
 
-  __device__ static void init(const TgtParams& T, int lane, int d, float4* xq, const PhiloxKey& k) {
+  __device__ static void init(const TgtParams& T, int lane, int d, float4* xq, const PhiloxKey& k,
+                              uint32_t& drawn) {
     const int nq = (d + 3) >> 2;
     for (int q = lane; q < nq; q += G) {
+      ++drawn;
       float z[4];
       quad(k, 0, q, z);
       float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = (4 * q + e < d) ? (float)Tgt::ref_draw(T, (double)z[e]) : 0.f;
+      for (int e = 0; e < 4; ++e) v[e] = (4 * q + e < d) ? Tgt::ref_draw32(T, z[e]) : 0.f;
       xq[q] = make_float4(v[0], v[1], v[2], v[3]);
     }
     refresh_v(T, lane, d, xq);
@@ -95,7 +107,7 @@ struct SmemOps {
   }
 
   __device__ static void move(const TgtParams& T, const KernelCfg& kc, int lane, int d,
-                              double beta, float4* xq, const PhiloxKey& k) {
+                              double beta, float4*& xq, float4*& xalt, const PhiloxKey& k, uint32_t& drawn) {
     const int nq = (d + 3) >> 2;
     if (kc.kind == ASMC_KERNEL_IDEALIZED) {
       const double mu = Tgt::exact_mu(T, beta);
@@ -141,6 +153,8 @@ struct SmemOps {
     // hot loops use the one-block path with no tail checks (one copy of the
     // generator per loop: the loop body stays inside the L0 I-cache).
     const bool aligned = (d & 3) == 0;
+    // early rejection: this lane's sum of max_h dlg(x_i, h) over its coordinates
+    float bnd = Tgt::kEarly ? bound_total(kf, lane, d, nq, xq) : 0.f;
     for (int p = 0; p < nprop; ++p) {
       const float s = (float)kc.steps[p % kc.n_steps];
       const uint64_t base = (uint64_t)p * (uint64_t)d;
@@ -148,15 +162,47 @@ struct SmemOps {
         const int pp = p + lane;
         lu_pre = pp < nprop ? log(k.uniform((uint32_t)pp)) : 0.0;
       }
-      const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq)
-                               : delta_pass<false>(kf, k, lane, d, nq, base, s, xq);
-      const double delta = group_sum<G>((double)dl);
       const double log_u = __shfl_sync(0xffffffffu, lu_pre, gbase + (p % G));
-      if (log_u < delta) {  // kernel.cpp:35: accept -> regenerate the proposal's normals
-        if (aligned) accept_pass<true>(kf, k, lane, nq, base, s, xq);
-        else accept_pass<false>(kf, k, lane, nq, base, s, xq);
+      bool rejected = false;
+      const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, rejected, drawn)
+                               : delta_pass<false>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, rejected, drawn);
+      if (rejected) continue;  // certainly rejected: the remaining normals are never drawn
+      const double delta = group_sum<G>((double)dl);
+      if (log_u < delta) {  // kernel.cpp:35: accept
+        if constexpr (kDual) {  // the proposal is already in the spare row
+          // only this particle's lanes take the branch (G < 32: other groups may reject)
+          __syncwarp(G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase));
+          float4* t = xq;
+          xq = xalt;
+          xalt = t;
+          if (Tgt::kEarly) bnd = bound_total(kf, lane, d, nq, xq);
+        } else {  // regenerate the proposal's normals
+          const float nb = aligned ? accept_pass<true>(kf, k, lane, nq, base, s, xq)
+                                   : accept_pass<false>(kf, k, lane, nq, base, s, xq);
+          drawn += (uint32_t)((nq - lane + G - 1) / G);
+          if (Tgt::kEarly) bnd = nb;
+        }
       }
     }
+  }
+
+  // sum of the early-rejection bound over this lane's coordinates (same order as delta_pass)
+  __device__ static float bound_total(const typename Tgt::F32& kf, int lane, int d, int nq, const float4* xq) {
+    float b = 0.f;
+#pragma unroll 1
+    for (int q = lane; q < nq; q += G) {
+      const float4 x = xq[q];
+      const float xv[4] = {x.x, x.y, x.z, x.w};
+      float vv[4] = {0.f, 0.f, 0.f, 0.f};
+      if constexpr (kCache) {
+        const float4 v = xq[nq + q];
+        vv[0] = v.x; vv[1] = v.y; vv[2] = v.z; vv[3] = v.w;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e < d) b += Tgt::dmax(kf, xv[e], vv[e]);
+    }
+    return b;
   }
 
   // one coordinate's leapfrog trajectory from (x, p); returns x', sets p'
@@ -215,36 +261,68 @@ struct SmemOps {
     return dl;
   }
 
-  // sum over this lane's quads of f_beta(x + s z) - f_beta(x)
+  // sum over this lane's quads of f_beta(x + s z) - f_beta(x).  Early rejection
+  // (exact): after 1, 2, 4 and 6 quad-iterations the group checks
+  //   partial + sum over unprocessed coordinates of max_h dlg  <  log u
+  // (with a rounding margin); then the proposal is rejected whatever the remaining
+  // normals are, so they are not drawn.  Accepted proposals see the identical sum.
   template <bool kAligned>
-  __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane,
-                                     int d, int nq, uint64_t base, float s, const float4* xq) {
-    float dl = 0.f;
+  __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane, int d, int nq,
+                                     uint64_t base, float s, const float4* xq, float4* xalt, double log_u,
+                                     float bnd, bool& rejected, uint32_t& drawn) {
+    float dl = 0.f, bp = 0.f;
+    const int mmax = (nq + G - 1) / G;
+    int q = lane;
 #pragma unroll 1
-    for (int q = lane; q < nq; q += G) {
-      float z[4];
-      if (kAligned) k.template normals4<float>((uint32_t)(base >> 2) + (uint32_t)q, z);
-      else k.template normals4_at<float>(base + 4 * (uint64_t)q, z);
-      const float4 x = xq[q];
-      const float xv[4] = {x.x, x.y, x.z, x.w};
-      if constexpr (kCache) {
-        const float4 v = xq[nq + q];
-        const float vv[4] = {v.x, v.y, v.z, v.w};
+    for (int seg = 0; seg < 5; ++seg) {
+      const int mend = seg == 4 ? mmax : min(mmax, seg == 0 ? 1 : (seg == 1 ? 2 : (seg == 2 ? 4 : 6)));
+      const int qend = min(nq, lane + G * mend);
+#pragma unroll 1
+      for (; q < qend; q += G) {
+        ++drawn;
+        float z[4];
+        if (kAligned) k.template normals4<float>((uint32_t)(base >> 2) + (uint32_t)q, z);
+        else k.template normals4_at<float>(base + 4 * (uint64_t)q, z);
+        const float4 x = xq[q];
+        const float xv[4] = {x.x, x.y, x.z, x.w};
+        if constexpr (kCache) {
+          const float4 v = xq[nq + q];
+          const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (kAligned || 4 * q + e < d) dl += Tgt::dlg_cached(kf, xv[e], vv[e], fmaf(s, z[e], xv[e]));
-      } else {
+          for (int e = 0; e < 4; ++e)
+            if (kAligned || 4 * q + e < d) {
+              dl += Tgt::dlg_cached(kf, xv[e], vv[e], fmaf(s, z[e], xv[e]));
+              if (Tgt::kEarly) bp += Tgt::dmax(kf, xv[e], vv[e]);
+            }
+        } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (kAligned || 4 * q + e < d) dl += Tgt::dlg(kf, xv[e], s * z[e]);
+          for (int e = 0; e < 4; ++e)
+            if (kAligned || 4 * q + e < d) {
+              dl += Tgt::dlg(kf, xv[e], s * z[e]);
+              if (Tgt::kEarly) bp += Tgt::dmax(kf, xv[e], 0.f);
+            }
+          if constexpr (kDual)
+            xalt[q] = make_float4(fmaf(s, z[0], xv[0]), fmaf(s, z[1], xv[1]), fmaf(s, z[2], xv[2]),
+                                  fmaf(s, z[3], xv[3]));
+        }
+      }
+      const int m = mend;
+      if (!Tgt::kEarly || m >= mmax) break;
+      const float tdl = group_sumf<G>(dl), trem = group_sumf<G>(bnd - bp);
+      const bool hopeless =
+          (double)tdl + (double)trem < log_u - (1e-4 * (fabs((double)tdl) + fabs((double)trem)) + 1e-2);
+      if (__all_sync(0xffffffffu, hopeless)) {  // warp-uniform exit keeps the key schedule uniform
+        rejected = true;
+        return dl;
       }
     }
     return dl;
   }
 
   template <bool kAligned>
-  __device__ static void accept_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane,
-                                     int nq, uint64_t base, float s, float4* xq) {
+  __device__ static float accept_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane,
+                                      int nq, uint64_t base, float s, float4* xq) {
+    float b = 0.f;  // the new x's early-rejection bound (same order as bound_total)
 #pragma unroll 1
     for (int q = lane; q < nq; q += G) {
       float z[4];
@@ -256,9 +334,21 @@ struct SmemOps {
       x.z = fmaf(s, z[2], x.z);
       x.w = fmaf(s, z[3], x.w);
       xq[q] = x;
-      if constexpr (kCache) xq[nq + q] = vquad(kf, x);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (kCache) {
+        v = vquad(kf, x);
+        xq[nq + q] = v;
+      }
+      if (Tgt::kEarly) {
+        b += Tgt::dmax(kf, x.x, v.x);
+        b += Tgt::dmax(kf, x.y, v.y);
+        b += Tgt::dmax(kf, x.z, v.z);
+        b += Tgt::dmax(kf, x.w, v.w);
+      }
     }
+    return b;
   }
+
 };
 
 // per-warp fold of this warp's groups for one (particle iteration, step), added
@@ -311,7 +401,8 @@ __device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_po
 }
 
 template <class Tgt, int G, bool kHmc = false>
-__global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant__ PassArgs A) {
+// RWMH passes: <= 85 registers (3 CTAs/SM; the dual-row footprint allows no more at d = 1000)
+__global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const __grid_constant__ PassArgs A) {
   constexpr int NG = kBlock / G;
   const int tid = threadIdx.x, g = tid / G, lane = tid % G, warp = tid >> 5;
   const int d = (int)A.tg.dim;
@@ -321,8 +412,9 @@ __global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant
   if (A.err && *(volatile int*)A.err) return;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int kWords = CacheWords<Tgt>::value;
+  constexpr int kWords = RowWords<Tgt, kHmc>::value;
   float4* xq = reinterpret_cast<float4*>(smem) + (size_t)g * nq * kWords;
+  float4* xalt = xq + (size_t)nq * CacheWords<Tgt>::value;  // spare row (kDual only)
   LogAcc* wacc = reinterpret_cast<LogAcc*>(smem + (size_t)NG * nq * 16 * kWords);
   const int rows = A.t_end - A.t_begin + 1;
   LogAcc* myacc = wacc + (size_t)warp * rows * nacc;  // [row][a] of this warp
@@ -331,6 +423,7 @@ __global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant
       myacc[i] = (i % nacc == kAccTop2) ? LogAcc{-__builtin_huge_val(), -__builtin_huge_val()}
                                          : lacc_empty();
   using Ops = SmemOps<Tgt, G, kHmc>;
+  uint32_t drawn = 0;  // quads of normals this lane generated (profiling)
 
   for (int r = 0; r < G; ++r) {
     const uint64_t local = blk * kBlock + (uint64_t)r * NG + g;
@@ -360,7 +453,7 @@ __global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant
     } else {
       PhiloxKey k;
       k.init(A.seed, A.round, pid, 0, 0);
-      Ops::init(A.tg, lane, d, xq, k);
+      Ops::init(A.tg, lane, d, xq, k, drawn);
     }
     __syncwarp();
     if (A.mode == kModeSmcInit) {
@@ -389,7 +482,7 @@ __global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant
       PhiloxKey k;
       k.init(A.seed, A.round, pid, (uint64_t)t, 1);
       __syncwarp();
-      Ops::move(A.tg, A.kc, lane, d, b1, xq, k);
+      Ops::move(A.tg, A.kc, lane, d, b1, xq, xalt, k, drawn);
       __syncwarp();
       const double pre = lw;
       lw += lg;
@@ -415,6 +508,12 @@ __global__ void __launch_bounds__(kBlock) pass_smem_kernel(const __grid_constant
       if (lane == 0) A.lw[local] = lw;
     }
     __syncwarp();
+  }
+  if (A.drawn) {  // profiling: normals generated by this warp (one atomic per warp)
+    unsigned long long c = drawn;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) c += __shfl_xor_sync(0xffffffffu, c, m);
+    if ((tid & 31) == 0) atomicAdd(A.drawn, 4ull * c);
   }
   if (A.mode == kModeTraj || A.mode == kModeSmcInit) return;
   __syncthreads();

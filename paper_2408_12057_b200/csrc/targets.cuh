@@ -42,6 +42,8 @@ struct TgtGaussShift {
   }
   __device__ static double v64(const TgtParams& T, double x) { return T.c[1] * (x - T.c[2]); }
   __device__ static double ref_draw(const TgtParams& T, double n) { return T.p[0] + T.p[2] * n; }
+  // fp32 paths: the same draw without the float -> double -> float round trip
+  __device__ static float ref_draw32(const TgtParams& T, float n) { return fmaf((float)T.p[2], n, (float)T.p[0]); }
   // target.cpp:107-113: mu computed once, then mu + sigma * normal
   __device__ static double exact_mu(const TgtParams& T, double beta) {
     return (1.0 - beta) * T.p[0] + beta * T.p[1];
@@ -66,6 +68,12 @@ struct TgtGaussShift {
   }
   __device__ static float grad32(const F32& k, float x) { return fmaf(-(x - k.mu0), k.inv_s2, k.ba); }
   __device__ static float vpart(const F32&, float x) { return x; }
+  // early rejection: max over h of dlg(x, h) (a concave quadratic in h)
+  static constexpr bool kEarly = true;
+  __device__ static float dmax(const F32& k, float x, float) {
+    const float g = k.ba - (x - k.mu0) * k.inv_s2;
+    return __fdividef(0.5f * g * g, k.inv_s2);
+  }
   // V = a * (sum x - d * mid)
   __device__ static double v_from(const TgtParams& T, double s) {
     return T.c[1] * (s - (double)T.dim * T.c[2]);
@@ -90,17 +98,27 @@ struct TgtMixture {
     return log_mix - lnpdf64(x, 0.0, T.p[0], T.c[0]);
   }
   __device__ static double ref_draw(const TgtParams& T, double n) { return T.p[0] * n; }
+  __device__ static float ref_draw32(const TgtParams& T, float n) { return (float)T.p[0] * n; }
   __device__ static double exact_mu(const TgtParams&, double) { return 0.0; }
   __device__ static double exact_draw(const TgtParams&, double, double n) { return n; }
   // fp32 ----------------------------------------------------------------
   struct F32 {
     float beta, inv_r, lw1, mu1, inv_s1, lw2, mu2, inv_s2;
+    float lmix;  // log(e^lw1 + e^lw2) >= hi + log1p(e^(lo-hi)) for every x (early rejection)
   };
   __device__ static F32 f32(const TgtParams& T, double beta) {
     // log-normal constants folded: log N(x; mu, s) = -0.5((x-mu)/s)^2 - log s - c
-    return F32{(float)beta, (float)(1.0 / T.p[0]),
-               (float)(T.c[1] - T.c[3] + T.c[0]), (float)T.p[2], (float)(1.0 / T.p[3]),
-               (float)(T.c[2] - T.c[4] + T.c[0]), (float)T.p[4], (float)(1.0 / T.p[5])};
+    const double l1 = T.c[1] - T.c[3] + T.c[0], l2 = T.c[2] - T.c[4] + T.c[0];
+    const double lm = (l1 > l2 ? l1 : l2) + log1p(exp(-fabs(l1 - l2)));
+    return F32{(float)beta, (float)(1.0 / T.p[0]), (float)l1, (float)T.p[2], (float)(1.0 / T.p[3]),
+               (float)l2, (float)T.p[4], (float)(1.0 / T.p[5]), (float)lm};
+  }
+  // early rejection: f_beta(y) = beta (hi + log1p) - (1 - beta) sr^2 / 2 <= beta lmix, so
+  // max_h dlg(x, h) <= beta (lmix - vterm(x)) + sr(x)^2 / 2  (v = the cached vterm(x))
+  static constexpr bool kEarly = false;  // bound too loose at d = 100 to pay for its bookkeeping
+  __device__ static float dmax(const F32& k, float x, float v) {
+    const float sr = x * k.inv_r;
+    return fmaf(k.beta, k.lmix - v, 0.5f * sr * sr);
   }
   // log_mix(x) - log eta(x) with the common -log(sqrt(2 pi)) - log(ref_sigma) folded out.
   // log1p(e^{lo-hi}) with lo <= hi: the MUFU ex2/lg2 pair is accurate to ~2e-7
@@ -173,6 +191,7 @@ struct TgtScale {
     return lnpdf64(x, 0.0, T.p[1], T.c[1]) - lnpdf64(x, 0.0, T.p[0], T.c[0]);
   }
   __device__ static double ref_draw(const TgtParams& T, double n) { return T.p[0] * n; }
+  __device__ static float ref_draw32(const TgtParams& T, float n) { return (float)T.p[0] * n; }
   // ref_harness.cpp ScaleGaussianTarget::exact_sample: sd = 1/sqrt(tau), x = sd * normal
   __device__ static double exact_mu(const TgtParams& T, double beta) {
     const double tau = (1.0 - beta) / (T.p[0] * T.p[0]) + beta / (T.p[1] * T.p[1]);
@@ -196,6 +215,9 @@ struct TgtScale {
   }
   __device__ static float grad32(const F32& k, float x) { return -k.tau * x; }
   __device__ static float vpart(const F32&, float x) { return x * x; }
+  // early rejection: max over h of -tau h (x + h/2) = tau x^2 / 2
+  static constexpr bool kEarly = true;
+  __device__ static float dmax(const F32& k, float x, float) { return 0.5f * k.tau * x * x; }
   __device__ static double v_from(const TgtParams& T, double s) {
     return T.c[4] * s - (double)T.dim * T.c[5];
   }
