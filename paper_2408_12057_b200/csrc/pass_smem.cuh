@@ -271,6 +271,7 @@ struct SmemOps {
                                      uint64_t base, float s, const float4* xq, float4* xalt, double log_u,
                                      float bnd, bool& rejected, uint32_t& drawn) {
     float dl = 0.f, bp = 0.f;
+    const float lu = (float)log_u;
     const int mmax = (nq + G - 1) / G;
     int q = lane;
 #pragma unroll 1
@@ -308,10 +309,11 @@ struct SmemOps {
       }
       const int m = mend;
       if (!Tgt::kEarly || m >= mmax) break;
-      const float tdl = group_sumf<G>(dl), trem = group_sumf<G>(bnd - bp);
-      const bool hopeless =
-          (double)tdl + (double)trem < log_u - (1e-4 * (fabs((double)tdl) + fabs((double)trem)) + 1e-2);
-      if (__all_sync(0xffffffffu, hopeless)) {  // warp-uniform exit keeps the key schedule uniform
+      // partial + remaining bound + a margin dominating the fp32 rounding of both sums
+      // (per-lane 1e-4 (|dl| + rem), summed, >= 1e-4 (|sum dl| + sum rem)): one reduction
+      const float rem = bnd - bp;
+      const float v = group_sumf<G>(dl + rem + 1e-4f * (fabsf(dl) + rem));
+      if (__all_sync(0xffffffffu, v < lu - 1e-2f)) {  // warp-uniform exit
         rejected = true;
         return dl;
       }
