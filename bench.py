@@ -172,6 +172,45 @@ def load_profile_traffic():
     return None
 
 
+def other_cpu_baselines():
+    """The reference's CPU path beside configs 3-5, on bounded samples of each workload
+    (same targets, kernels and rounds, smaller N): config 3 and 4 through the unmodified
+    reference engine (oracle/_ref, all host cores), config 5's HMC through the oracle port
+    (the reference has no HMC; one core)."""
+    import oracle
+    from paper_2408_12057_b200 import exact
+    workers = os.cpu_count() or 1
+    out = {}
+    ref = oracle.load("ref", abi.RNG_XOSHIRO) if oracle.available("ref", abi.RNG_XOSHIRO) else None
+    if ref is not None:
+        tg = abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100)
+        t0 = time.perf_counter()
+        r = ref.run_rounds(tg, abi.kernel(abi.KERNEL_RWMH, STEPS, 1), abi.MODE_SSMC, 4096, 6,
+                           policy=abi.POLICY_ADAPTIVE_ESS, seed=SEED, workers=workers)
+        dt = time.perf_counter() - t0
+        ka = float(np.sum(r["kernel_applications"]))
+        out["config3"] = {"value": ka / dt, "unit": "particle-steps/s", "cores": workers, "kind": "reference",
+                          "sample": f"run_ssmc N1=4096, 6 rounds, {dt:.1f}s"}
+        X, y = abi.logistic_data(100000, 256, 0)
+        tg = abi.logistic(X, y, 1.0)
+        refp = oracle.load("ref", abi.RNG_PHILOX)
+        t0 = time.perf_counter()
+        refp.run_sais_single(tg, abi.kernel(abi.KERNEL_RWMH, (0.002, 0.005, 0.01), 1), [0.0, 1.0], 32, seed=SEED,
+                             round=1, workers=workers)
+        dt = time.perf_counter() - t0
+        out["config4"] = {"value": 32 / dt, "unit": "particle-steps/s", "cores": workers, "kind": "reference",
+                          "sample": f"run_sais_single with the logistic plugin, N=32, T=1, {dt:.1f}s"}
+    rs = oracle.load("restate", abi.RNG_PHILOX)
+    tg = abi.ising(64, exact.K_CRITICAL, 1.0, 1.0)
+    t0 = time.perf_counter()
+    rs.run_sais_single(tg, abi.kernel(abi.KERNEL_HMC, (0.25,), 1, leapfrog=10), [0.0, 0.5, 1.0], 16, seed=SEED,
+                       round=1)
+    dt = time.perf_counter() - t0
+    out["config5"] = {"value": 32 / dt, "unit": "particle-steps/s", "cores": 1, "kind": "port",
+                      "sample": f"oracle restatement (HMC: no reference kernel), N=16, T=2, {dt:.1f}s"}
+    return out
+
+
 def other_configs(stream, ex):
     """BASELINE.json configs 3-5 on this GPU (single-GPU shapes), device time by CUDA
     events on the library's stream; inputs resident, one warm-up each."""
@@ -383,8 +422,11 @@ def main():
         if world == 1 and not args.no_configs:
             try:
                 line["other_configs"] = other_configs(stream, ex)
+                if not args.no_cpu_baseline:
+                    for key, v in other_cpu_baselines().items():
+                        line["other_configs"][key]["cpu_baseline"] = v
             except Exception as exc:  # reported, never required
-                line["other_configs"] = {"unavailable": str(exc)}
+                line["other_configs"] = dict(line.get("other_configs", {}), unavailable=str(exc))
         if world == 1 and not args.no_ttt:
             try:
                 sys.path.insert(0, os.path.join(ROOT, "tools"))
