@@ -253,15 +253,21 @@ def other_configs(stream, ex):
                       "psteps": float((1 << 20) * 4), "device_s": dt, "value": (1 << 20) * 4 / dt,
                       "unit": "particle-steps/s", "likelihood_tflops_algorithmic": ev_flops / (ev_ms * 1e-3) / 1e12,
                       "tensor_tflops_issued": 3 * ev_flops / (ev_ms * 1e-3) / 1e12}
-    # config 5: SAIS relaxed Ising 64x64 at K_c, HMC, N=2^18
+    # config 5: SAIS relaxed Ising 64x64 at K_c, HMC, schedule adaptation over 12 doubling
+    # rounds ending at N = 2^18 (N1 = 5793: the budget rule's sqrt(2) growth)
     tg = abi.ising(64, exact.K_CRITICAL, 1.0, 1.0)
     k = abi.kernel(abi.KERNEL_HMC, (0.25,), 1, leapfrog=10)
-    betas = np.linspace(0.0, 1.0, 9)
-    r, dt = timed(lambda: capi.run_sais_single(tg, k, betas, 1 << 18, seed=SEED, round=1, exec_=ex))
-    out["config5"] = {"workload": "SAIS relaxed Ising 64x64 K=K_c, HMC eps 0.25 x 10 leapfrog, N=2^18, T=8",
-                      "psteps": float((1 << 18) * 8), "device_s": dt, "value": (1 << 18) * 8 / dt,
-                      "unit": "particle-steps/s", "site_gradients_per_s": (1 << 18) * 8 * 11 * 4096 / dt,
-                      "log_z_hat": r["log_z_hat"], "exact_log_z": exact.ising_relaxed_log_z(64, exact.K_CRITICAL, 1.0)}
+    r, dt = timed(lambda: capi.run_rounds(tg, k, abi.MODE_SAIS, 5793, 12, seed=SEED, exec_=ex))
+    ps = float(np.sum(r["kernel_applications"]))
+    steps = [int(v) for v in r["steps"]]
+    out["config5"] = {"workload": "SAIS relaxed Ising 64x64 K=K_c, HMC eps 0.25 x 10 leapfrog, 12 adaptive rounds, "
+                                  "N 5793 -> 2^18, T 1 -> 104",
+                      "psteps": ps, "device_s": dt, "value": ps / dt, "unit": "particle-steps/s",
+                      "site_gradients_per_s": ps * 11 * 4096 / dt,
+                      "n_final": int(r["n_particles"][-1]), "T": steps,
+                      "lambda_hat": [float(r["lambda_"][i][steps[i]]) for i in range(len(steps))],
+                      "log_z_hat": [float(v) for v in r["log_z_hat"]],
+                      "exact_log_z": exact.ising_relaxed_log_z(64, exact.K_CRITICAL, 1.0)}
     return out
 
 
