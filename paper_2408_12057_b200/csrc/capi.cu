@@ -611,9 +611,13 @@ int is_move(DevCtx* C, const IsArgs& A, int mode, const double* betas, int t) {
 
 // run_smc (engine.cpp:97-188) for the logistic target: step-outer because the
 // likelihood of all particles is one GEMM per proposal (SAIS = policy never).
+// chunk_out != nullptr: SAIS partial mode for particles [p_begin, p_begin + n) of a
+// sharded round (asmc_sais_partials): per step the chunk partials of g0 g1 g2 elbo are
+// written to chunk_out[(t * kNAcc + a) * nch + c]; no decision / resampling.
 int enqueue_lg_round(DevCtx* C, const LgData& D, const asmc_target_desc* t, const asmc_kernel_desc* k,
                      const double* d_betas, int T, uint64_t n, int policy, double rho, uint64_t seed,
-                     uint64_t round, RoundDev* d_rd, SmcState* d_st, LgWork& W) {
+                     uint64_t round, RoundDev* d_rd, SmcState* d_st, LgWork& W, uint64_t p_begin = 0,
+                     LogAcc* chunk_out = nullptr, int* d_err = nullptr) {
   const int d = D.d, row = d + 4;
   const uint64_t nblk = nblocks(n), nchunks = (nblk + kChunkBlocks - 1) / kChunkBlocks;
   TRY(W.sa.alloc(n * row, C->stream));
@@ -644,13 +648,21 @@ int enqueue_lg_round(DevCtx* C, const LgData& D, const asmc_target_desc* t, cons
   A.seed = seed;
   A.round = round;
   A.sigma_p = t->p[0];
-  A.err = &d_st->err;
+  A.err = chunk_out ? d_err : &d_st->err;
+  A.p_begin = p_begin;
   LCH(launch_lg_init(A, C->stream));        // engine_detail.hpp:91-100
   TRY(lg_eval(C, D, A, 0, d_betas, 0.f, 0));  // V(theta_0)
   const int nprop = k->kind == ASMC_KERNEL_RWMH ? k->sweeps * k->n_step_sizes : 0;
   for (int s = 1; s <= T; ++s) {
     A.t = s;
     LCH(launch_lg_weight(A, d_betas, s, W.part.p, nblk, C->stream));
+    if (chunk_out) {
+      LCH(launch_fold_chunks(W.part.p, nblk, nblk, 0, 1, 4, nchunks, chunk_out + (size_t)s * kNAcc * nchunks,
+                             C->stream));
+      for (int q = 0; q < nprop; ++q)
+        TRY(lg_eval(C, D, A, 1, d_betas, (float)k->step_sizes[q % k->n_step_sizes], q));
+      continue;
+    }
     LCH(launch_fold(false, W.part.p, nblk, nblk, 0, 1, kNAcc, W.chunk.p, W.tot.p, C->stream));
     LCH(launch_smc_decide(W.tot.p, s, T, n, policy, rho, seed, round, ASMC_RNG_PHILOX, d_rd, C->stream));
     for (int q = 0; q < nprop; ++q)  // kernel.cpp:31-40 at beta_t
@@ -698,7 +710,8 @@ IsArgs is_args(const asmc_target_desc* t, const asmc_kernel_desc* k) {
 // (the whole RWMH / HMC cycle at beta_t per particle), resample + gather.
 int enqueue_is_round(DevCtx* C, const asmc_target_desc* t, const asmc_kernel_desc* k, const double* d_betas,
                      int T, uint64_t n, int policy, double rho, uint64_t seed, uint64_t round, RoundDev* d_rd,
-                     SmcState* d_st, LgWork& W) {
+                     SmcState* d_st, LgWork& W, uint64_t p_begin = 0, LogAcc* chunk_out = nullptr,
+                     int* d_err = nullptr) {
   IsArgs I = is_args(t, k);
   const int row = I.row;
   const uint64_t nblk = nblocks(n), nchunks = (nblk + kChunkBlocks - 1) / kChunkBlocks;
@@ -720,9 +733,10 @@ int enqueue_is_round(DevCtx* C, const asmc_target_desc* t, const asmc_kernel_des
   I.state = W.sbuf.p;
   I.xcur = W.xcur.p;
   I.n_local = n;
+  I.p_begin = p_begin;
   I.seed = seed;
   I.round = round;
-  I.err = &d_st->err;
+  I.err = chunk_out ? d_err : &d_st->err;
   LgArgs A;  // the weight kernel and gather see the same state-row layout
   std::memset(&A, 0, sizeof A);
   A.state = W.sbuf.p;
@@ -731,10 +745,16 @@ int enqueue_is_round(DevCtx* C, const asmc_target_desc* t, const asmc_kernel_des
   A.n_local = n;
   A.d = I.L * I.L;
   A.row = row;
-  A.err = &d_st->err;
+  A.err = I.err;
   TRY(is_move(C, I, 0, d_betas, 0));  // engine_detail.hpp:91-100 (+ V(y_0))
   for (int s = 1; s <= T; ++s) {
     LCH(launch_lg_weight(A, d_betas, s, W.part.p, nblk, C->stream));
+    if (chunk_out) {  // SAIS partial mode (see enqueue_lg_round)
+      LCH(launch_fold_chunks(W.part.p, nblk, nblk, 0, 1, 4, nchunks, chunk_out + (size_t)s * kNAcc * nchunks,
+                             C->stream));
+      TRY(is_move(C, I, 1, d_betas, s));
+      continue;
+    }
     LCH(launch_fold(false, W.part.p, nblk, nblk, 0, 1, kNAcc, W.chunk.p, W.tot.p, C->stream));
     LCH(launch_smc_decide(W.tot.p, s, T, n, policy, rho, seed, round, ASMC_RNG_PHILOX, d_rd, C->stream));
     TRY(is_move(C, I, 1, d_betas, s));  // kernel.cpp:26-63 at beta_t
@@ -792,6 +812,53 @@ int run_lg_single(const asmc_target_desc* target, const asmc_kernel_desc* kernel
   TRY(device_error(st.err, st.err_step, st.err_val));
   out->kernel_applications = n * (uint64_t)T;
   out->wall_seconds = now_s() - t0;
+  return 0;
+}
+
+// asmc_sais_partials for the step-outer engines (logistic: tcgen05 likelihood; Ising:
+// lattice moves): the engine runs its particle range in SAIS partial mode and the
+// per-step chunk partials are returned in the fused pass's layout.
+int stepouter_partials(const asmc_target_desc* target, const asmc_kernel_desc* kernel, const double* betas, int T,
+                       uint64_t p_begin, uint64_t p_end, uint64_t seed, uint64_t round, const asmc_exec& ex,
+                       asmc_logacc* partials) {
+  const bool lg = target->kind == ASMC_TARGET_LOGISTIC;
+  TRY(lg ? lg_check(target, kernel, ex) : is_check(target, kernel, ex));
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C, ex.stream));
+  const uint64_t nloc = p_end - p_begin;
+  const uint64_t nch = asmc_fold_chunks(p_begin, p_end);
+  if (nch == 0) return 0;
+  DBuf<double> d_betas;
+  TRY(d_betas.alloc(T + 1, C->stream));
+  CU(cudaMemcpyAsync(d_betas.p, betas, sizeof(double) * (T + 1), cudaMemcpyHostToDevice, C->stream));
+  DBuf<LogAcc> chunk;
+  DBuf<int> err;
+  TRY(chunk.alloc((size_t)(T + 1) * kNAcc * nch, C->stream));
+  TRY(err.alloc(1, C->stream));
+  CU(cudaMemsetAsync(err.p, 0, sizeof(int), C->stream));
+  LgWork W;
+  if (lg) {
+    LgData D;
+    TRY(lg_upload(C, target, D));
+    TRY(enqueue_lg_round(C, D, target, kernel, d_betas.p, T, nloc, ASMC_POLICY_NEVER, 0.5, seed, round, nullptr,
+                         nullptr, W, p_begin, chunk.p, err.p));
+    CU(cudaStreamSynchronize(C->stream));  // D (the uploaded data) is released at scope exit
+  } else {
+    TRY(enqueue_is_round(C, target, kernel, d_betas.p, T, nloc, ASMC_POLICY_NEVER, 0.5, seed, round, nullptr,
+                         nullptr, W, p_begin, chunk.p, err.p));
+  }
+  std::vector<LogAcc> h((size_t)(T + 1) * kNAcc * nch);
+  CU(cudaMemcpyAsync(h.data(), chunk.p, h.size() * sizeof(LogAcc), cudaMemcpyDeviceToHost, C->stream));
+  int herr = 0;
+  CU(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
+  TRY(device_error(herr, 0, 0.0));
+  for (uint64_t c = 0; c < nch; ++c)
+    for (int t = 0; t <= T; ++t)
+      for (int a = 0; a < 4; ++a) {
+        const LogAcc v = t == 0 ? LogAcc{-HUGE_VAL, 0.0} : h[((size_t)t * kNAcc + a) * nch + c];
+        partials[(c * (T + 1) + t) * 4 + a] = asmc_logacc{v.max, v.sum};
+      }
   return 0;
 }
 
@@ -1079,13 +1146,14 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
                        uint64_t seed, uint64_t round, const asmc_exec* exec, asmc_logacc* partials) {
   TRY(check_schedule(betas, T));
   TRY(check_pair(target, kernel));
-  TRY(check_pass_target(target, "asmc_sais_partials"));
   if (p_begin % ASMC_FOLD_CHUNK != 0)
     return fail(ASMC_ERR_INVALID_ARGUMENT, "p_begin must be a multiple of ASMC_FOLD_CHUNK");
   if (p_end > n || p_end < p_begin) return fail(ASMC_ERR_INVALID_ARGUMENT, "bad particle range");
   const asmc_exec ex = exec ? *exec : default_exec();
   if (ex.precision == ASMC_PREC_FP64)
     return fail(ASMC_ERR_CAPABILITY, "sharded partials use the fp32 tree fold; fp64 reference order is single-GPU");
+  if (target->kind == ASMC_TARGET_LOGISTIC || target->kind == ASMC_TARGET_ISING)
+    return stepouter_partials(target, kernel, betas, T, p_begin, p_end, seed, round, ex, partials);
   Layout L;
   TRY(choose_layout(ex, kernel->kind, target->dim, &L, T, 4));
   DevCtx* C;
