@@ -284,6 +284,8 @@ def main():
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-target measurement")
     ap.add_argument("--ttt-seeds", type=int, default=1000)
     ap.add_argument("--no-configs", action="store_true", help="skip the configs 3-5 measurements")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional multi-rank check on one GPU (CPU collectives; not for timing)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU chunk-partial round loop even at one rank")
     args = ap.parse_args()
@@ -296,10 +298,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo" and "ASMC_BENCH_DEVICE" in os.environ:  # functional check on one GPU
+        local = int(os.environ["ASMC_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     stream = torch.cuda.current_stream()
     ex = abi.execopts(abi.RNG_PHILOX, abi.PREC_FP32, device=local, stream=stream.cuda_stream)
     tg = abi.scale_gaussian(SIGMA0, SIGMA1, args.dim)
@@ -310,7 +317,8 @@ def main():
     def one_step():
         if world == 1 and not args.sharded:
             return capi.run_rounds(tg, kern, abi.MODE_SAIS, n1, ROUNDS, seed=SEED, exec_=ex)
-        return distributed.run_sais(tg, kern, n1, ROUNDS, SEED, ex, rank, world)
+        return distributed.run_sais(tg, kern, n1, ROUNDS, SEED, ex, rank, world,
+                                    device="cpu" if args.dist_backend == "gloo" else None)
 
     # generator peak (same Philox + fp32 Box-Muller code path, registers only)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
@@ -350,7 +358,8 @@ def main():
             prof_drawn += list(drw)
     launches = capi.launch_count(reset=True)
     if world > 1:
-        t = torch.tensor([dev_ms, wall_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([dev_ms, wall_s], device="cuda" if args.dist_backend == "nccl" else "cpu",
+                         dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         dev_ms, wall_s = float(t[0]), float(t[1])
     clocks = clk.summary()
