@@ -265,6 +265,18 @@ int asmc_smc_shard_plan(asmc_smc_shard* shard, double* all_block_totals_dev, uin
 int asmc_smc_shard_pack(asmc_smc_shard* shard, void* rows_dev);
 int asmc_smc_shard_accept(asmc_smc_shard* shard, const void* rows_dev);
 int asmc_smc_shard_report(asmc_smc_shard* shard, asmc_report* out);
+/* Multi-GPU ZJA (drivers.cpp:234-341 across GPUs): a shard in ZJA mode has an open-ended
+ * schedule (run_smc(never) whose step t is the last iff beta_t = 1).  Per step: eval
+ * (cache log eta, V), probes -- each returns this shard's per-chunk (m1, m2) partials of
+ * the one-step discrepancy at b2 (b2 < 0: the log-weights' lse) for the caller to
+ * all-gather and fold in chunk order (schedule.cpp:201-264's bisection runs on every rank,
+ * identically) --, set_beta(t, chosen), then asmc_smc_shard_step / decide as in SSMC. */
+int asmc_zja_shard_create(const asmc_target_desc* target, const asmc_kernel_desc* kernel, uint64_t n_particles,
+                          uint64_t p_begin, uint64_t p_end, uint64_t seed, uint64_t round, int32_t max_steps,
+                          const asmc_exec* exec, asmc_smc_shard** out);
+int asmc_zja_shard_eval(asmc_smc_shard* shard);
+int asmc_zja_shard_probe(asmc_smc_shard* shard, double beta, double b2, asmc_logacc* chunk_partials);
+int asmc_zja_shard_set_beta(asmc_smc_shard* shard, int32_t t, double beta);
 /* parity hook: copy this shard's particles (row-major, row_bytes each) and log-weights */
 int asmc_smc_shard_state(asmc_smc_shard* shard, void* rows_host, double* log_w_host);
 

@@ -392,6 +392,49 @@ class SmcShard:
         self.close()
 
 
+class ZjaShard(SmcShard):
+    """One GPU's particle shard of a multi-GPU run_zja (asmc_zja_shard_* + the SMC
+    shard step/decide); see distributed.run_zja_multi."""
+
+    def __init__(self, target, kernel, n, p_begin, p_end, seed=0, round=1, max_steps=100000, exec_=None):
+        L = lib()
+        self._lib = L
+        for f in ("asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes"):
+            getattr(L, f).restype = C.c_uint64
+            getattr(L, f).argtypes = [C.c_void_p]
+        L.asmc_smc_shard_destroy.argtypes = [C.c_void_p]
+        L.asmc_smc_shard_destroy.restype = None
+        self.T = max_steps
+        self.n, self.p_begin, self.p_end = n, p_begin, p_end
+        self.exec_ = exec_ or abi.execopts(abi.RNG_PHILOX, abi.PREC_FP32)
+        self._target = target
+        h = C.c_void_p()
+        _check(L.asmc_zja_shard_create(C.byref(target), C.byref(kernel), C.c_uint64(n), C.c_uint64(p_begin),
+                                       C.c_uint64(p_end), C.c_uint64(seed), C.c_uint64(round),
+                                       C.c_int32(max_steps), C.byref(self.exec_), C.byref(h)))
+        self._h = h
+        self.chunks = L.asmc_smc_shard_chunks(h)
+        self.blocks = L.asmc_smc_shard_blocks(h)
+        self.row_bytes = L.asmc_smc_shard_row_bytes(h)
+
+    def eval(self):
+        _check(self._lib.asmc_zja_shard_eval(self._h))
+
+    def probe(self, beta, b2):
+        """(chunks, 2, 2) array: per chunk (m1, m2) as (max, sum)."""
+        out = np.zeros((self.chunks, 2, 2))
+        _check(self._lib.asmc_zja_shard_probe(self._h, C.c_double(beta), C.c_double(b2), _arr(out, C.c_double)))
+        return out
+
+    def set_beta(self, t, beta):
+        _check(self._lib.asmc_zja_shard_set_beta(self._h, C.c_int32(t), C.c_double(beta)))
+
+    def report(self, T=None):
+        rep, bufs = _report(self.T if T is None else T)
+        _check(self._lib.asmc_smc_shard_report(self._h, C.byref(rep)))
+        return _finish(rep, bufs, True)
+
+
 EXPORTED = [
     "asmc_last_error", "asmc_version", "asmc_device_count", "asmc_launch_count", "asmc_run_smc",
     "asmc_run_sais_single", "asmc_run_rounds", "asmc_fold_chunks", "asmc_sais_partials",
@@ -402,5 +445,6 @@ EXPORTED = [
     "asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes",
     "asmc_smc_shard_step", "asmc_smc_shard_decide", "asmc_smc_shard_plan", "asmc_smc_shard_pack",
     "asmc_smc_shard_accept", "asmc_smc_shard_report", "asmc_smc_shard_state", "asmc_run_zja",
-    "asmc_zja_next_beta", "asmc_run_pt", "asmc_profile_collect_drawn",
+    "asmc_zja_next_beta", "asmc_run_pt", "asmc_profile_collect_drawn", "asmc_zja_shard_create",
+    "asmc_zja_shard_eval", "asmc_zja_shard_probe", "asmc_zja_shard_set_beta",
 ]

@@ -1815,6 +1815,10 @@ struct asmc_smc_shard {
   DBuf<uint64_t> rank_blk, slot_dev;
   RoundBufs R;
   std::vector<uint64_t> slots;
+  // multi-GPU ZJA mode: open-ended schedule (betas[t] set per step), potential cache, probes
+  int zja = 0;
+  DBuf<double> lr, V;
+  DBuf<LogAcc> zpart, zchunk;
 };
 
 extern "C" {
@@ -1936,8 +1940,8 @@ int asmc_smc_shard_decide(asmc_smc_shard* h, int32_t t, const asmc_logacc* all_d
                 (unsigned long long)asmc_fold_chunks(0, h->n), (unsigned long long)all_chunks);
   cudaStream_t s = h->C.stream;
   LCH(launch_fold_chunk_major(reinterpret_cast<const LogAcc*>(all_dev), all_chunks, h->tot.p, s));
-  LCH(launch_smc_decide(h->tot.p, t, h->T, h->n, h->policy, h->rho, h->seed, h->round, h->ex.rng,
-                        h->R.rd.p, s));
+  LCH(launch_smc_decide(h->tot.p, t, h->zja ? -1 : h->T, h->n, h->policy, h->rho, h->seed, h->round, h->ex.rng,
+                        h->R.rd.p, s, h->zja ? h->betas.p : nullptr));
   LCH(launch_cdf_blocks(h->lw.p, h->n_local, h->R.st.p, h->cum.p, btot_dev, s));
   SmcState st;
   CU(cudaMemcpyAsync(&st, h->R.st.p, sizeof st, cudaMemcpyDeviceToHost, s));
@@ -2019,12 +2023,13 @@ int asmc_smc_shard_accept(asmc_smc_shard* h, const void* rows_dev) {
 
 int asmc_smc_shard_report(asmc_smc_shard* h, asmc_report* out) {
   if (!h || !out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null argument");
-  if (h->t_done != h->T || h->resampling)
+  const int T = h->zja ? h->t_done : h->T;
+  if (T < 1 || h->t_done != T || h->resampling)
     return fail(ASMC_ERR_INVALID_ARGUMENT, "report before step %d completed", h->T);
   SmcState st;
-  TRY(copy_round(h->C.stream, h->R, h->T, true, out, &st));
+  TRY(copy_round(h->C.stream, h->R, T, true, out, &st));
   TRY(device_error(st.err, st.err_step, st.err_val));
-  out->kernel_applications = h->n * (uint64_t)h->T;
+  out->kernel_applications = h->n * (uint64_t)T;
   return 0;
 }
 
@@ -2035,6 +2040,72 @@ int asmc_smc_shard_state(asmc_smc_shard* h, void* rows_host, double* lw_host) {
     CU(cudaMemcpyAsync(rows_host, h->x.p, h->n_local * h->row_bytes, cudaMemcpyDeviceToHost, s));
   if (lw_host) CU(cudaMemcpyAsync(lw_host, h->lw.p, h->n_local * sizeof(double), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  return 0;
+}
+
+}  // extern "C"
+
+// ====================================================== multi-GPU ZJA shards
+extern "C" {
+
+int asmc_zja_shard_create(const asmc_target_desc* target, const asmc_kernel_desc* kernel, uint64_t n,
+                          uint64_t p_begin, uint64_t p_end, uint64_t seed, uint64_t round, int32_t max_steps,
+                          const asmc_exec* exec, asmc_smc_shard** out) {
+  if (max_steps < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "max_steps must be at least 1");
+  TRY(check_pass_target(target, "asmc_zja_shard_create"));
+  std::vector<double> b(max_steps + 1);  // placeholder schedule; betas[t] are chosen per step
+  for (int t = 0; t <= max_steps; ++t) b[t] = (double)t / (double)max_steps;
+  b[0] = 0.0;
+  b[max_steps] = 1.0;
+  TRY(asmc_smc_shard_create(target, kernel, b.data(), max_steps, n, p_begin, p_end, ASMC_POLICY_NEVER, 0.5, seed,
+                            round, exec, out));
+  asmc_smc_shard* h = *out;
+  h->zja = 1;
+  cudaStream_t s = h->C.stream;
+  const int rc = [&]() -> int {
+    TRY(h->lr.alloc(h->n_local, s));
+    TRY(h->V.alloc(h->n_local, s));
+    TRY(h->zpart.alloc(2 * h->nblk, s));
+    TRY(h->zchunk.alloc((size_t)kNAcc * h->nch, s));
+    return 0;
+  }();
+  if (rc) {
+    asmc_smc_shard_destroy(h);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+// log eta / V at the shard's current particles (once per ZJA step, before the probes)
+int asmc_zja_shard_eval(asmc_smc_shard* h) {
+  if (!h || !h->zja) return fail(ASMC_ERR_INVALID_ARGUMENT, "not a ZJA shard");
+  LCH(launch_zja_eval(h->A.tg, false, h->xbuf.p, h->xcur.p, h->n_local, h->lr.p, h->V.p, &h->R.st.p->err,
+                      h->C.stream));
+  return 0;
+}
+
+// chunk partials of one probe: out[c * 2 + 0] = m1, [c * 2 + 1] = m2 of dhat(b2) over this
+// shard's chunks (b2 < 0: out[c * 2] = lse of the log-weights); host buffer, synchronous
+int asmc_zja_shard_probe(asmc_smc_shard* h, double beta, double b2, asmc_logacc* out) {
+  if (!h || !h->zja || !out) return fail(ASMC_ERR_INVALID_ARGUMENT, "not a ZJA shard or null output");
+  cudaStream_t s = h->C.stream;
+  LCH(launch_zja_probe_blocks(h->lw.p, h->V.p, h->n_local, beta, b2, h->zpart.p, h->nblk, s));
+  LCH(launch_fold_chunks(h->zpart.p, h->nblk, h->nblk, 0, 1, 2, h->nch, h->zchunk.p, s));
+  std::vector<LogAcc> c(2 * h->nch);
+  CU(cudaMemcpyAsync(c.data(), h->zchunk.p, c.size() * sizeof(LogAcc), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  for (uint64_t i = 0; i < h->nch; ++i) {
+    out[2 * i] = asmc_logacc{c[i].max, c[i].sum};
+    out[2 * i + 1] = asmc_logacc{c[h->nch + i].max, c[h->nch + i].sum};
+  }
+  return 0;
+}
+
+int asmc_zja_shard_set_beta(asmc_smc_shard* h, int32_t t, double beta) {
+  if (!h || !h->zja) return fail(ASMC_ERR_INVALID_ARGUMENT, "not a ZJA shard");
+  if (t < 1 || t > h->T) return fail(ASMC_ERR_EVALUATION, "online adaptation failed to reach beta = 1 within %d steps", h->T);
+  CU(cudaMemcpyAsync(h->betas.p + t, &beta, sizeof(double), cudaMemcpyHostToDevice, h->C.stream));
+  CU(cudaStreamSynchronize(h->C.stream));  // &beta is a host stack value
   return 0;
 }
 

@@ -226,6 +226,48 @@ cudaError_t launch_zja_eval(const TgtParams& T, bool fp64_state, const void* con
   return cudaGetLastError();
 }
 
+// Sharded probes (multi-GPU ZJA): per 256-particle block the pair (m1, m2) of
+// dhat(b2) -- or, with b2 < 0, the log-sum-exp of the log-weights in m1 -- as a fixed
+// tree (thread = particle, warp xor butterfly, warps in order), written to
+// part[a * stride + blk] (a = 0: m1, a = 1: m2); the caller folds blocks into chunks.
+__global__ void zja_probe_blocks_kernel(const double* lw, const double* V, uint64_t n, double beta, double b2,
+                                        LogAcc* part, uint64_t stride) {
+  const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  LogAcc m1 = lacc_empty(), m2 = lacc_empty();
+  if (p < n) {
+    if (b2 < 0.0) {
+      lacc_add(m1, lw[p]);
+    } else {
+      const double lg = (b2 - beta) * V[p];
+      lacc_add(m1, lw[p] + lg);
+      lacc_add(m2, lw[p] + 2.0 * lg);
+    }
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    lacc_combine(m1, shfl_xor_acc(m1, m));
+    lacc_combine(m2, shfl_xor_acc(m2, m));
+  }
+  __shared__ LogAcc w[2][8];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  if (lane == 0) {
+    w[0][wi] = m1;
+    w[1][wi] = m2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    LogAcc a = lacc_empty();
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) lacc_combine(a, w[threadIdx.x][i]);
+    part[(size_t)threadIdx.x * stride + blockIdx.x] = a;
+  }
+}
+
+cudaError_t launch_zja_probe_blocks(const double* lw, const double* V, uint64_t n, double beta, double b2,
+                                    LogAcc* part, uint64_t stride, cudaStream_t s) {
+  zja_probe_blocks_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lw, V, n, beta, b2, part, stride);
+  return cudaGetLastError();
+}
+
 int zja_grid_blocks(int device) {
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);

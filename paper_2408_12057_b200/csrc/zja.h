@@ -31,5 +31,8 @@ cudaError_t launch_zja_eval(const TgtParams& T, bool fp64_state, const void* con
 // zja_next_beta for step t; `grid_blocks` (cooperative mode) from zja_grid_blocks
 cudaError_t launch_zja_next_beta(const ZjaArgs& A, int grid_blocks, cudaStream_t s);
 int zja_grid_blocks(int device);
+// multi-GPU probes: block partials (m1, m2) of dhat(b2) (b2 < 0: lse of lw in m1)
+cudaError_t launch_zja_probe_blocks(const double* lw, const double* V, uint64_t n, double beta, double b2,
+                                    LogAcc* part, uint64_t stride, cudaStream_t s);
 
 }  // namespace asmcdev

@@ -288,3 +288,123 @@ def run_smc_multi(target, kernel, betas, n, policy=abi.POLICY_ADAPTIVE_ESS, rho=
     for s in shards:
         s.s.close()
     return reps
+
+
+# ------------------------------------------------------------------- ZJA
+# Multi-GPU run_zja (drivers.cpp:234-341; SURVEY 8e "ZJA: per-step allgathers inside
+# the bisection").  Every probe of zja_next_beta's bisection (schedule.cpp:219-264) is
+# one all-gather of the shards' per-chunk (m1, m2) partials, folded in chunk order on
+# every rank -- so all ranks take the same branches and choose the same beta, and the
+# result is the same for any GPU count.  ~50 collectives per annealing step, against
+# one per ROUND for SAIS: the paper's argument, made measurable.
+
+def _lacc_combine(a, b):
+    """LogAccumulator::combine (logsum.hpp:30-38) on (max, sum) pairs (host doubles)."""
+    am, asum = a
+    bm, bs = b
+    if bm == -math.inf:
+        return a
+    if bm <= am:
+        return (am, asum + bs * math.exp(bm - am))
+    return (bm, asum * math.exp(am - bm) + bs)
+
+
+def _lacc_total(a):
+    return -math.inf if a[0] == -math.inf else a[0] + math.log(a[1])
+
+
+def zja_search(dhat, beta, delta, tol=1e-10):
+    """zja_next_beta's search (schedule.cpp:233-263) over a dhat(b2) oracle."""
+    if dhat(1.0) <= delta:
+        return 1.0, False
+
+    def bisect(lo, hi):
+        while hi - lo > tol:
+            mid = 0.5 * (lo + hi)
+            if dhat(mid) <= delta:
+                lo = mid
+            else:
+                hi = mid
+        return lo
+
+    root = bisect(beta, 1.0)
+    for i in range(1, 16):
+        probe = beta + (root - beta) * float(i) / 16
+        if dhat(probe) > delta * (1.0 + 1e-12):
+            return bisect(beta, probe), True
+    return root, False
+
+
+def run_zja_multi(target, kernel, n, delta_star, seed=0, exec_=None, comm=None, rank=0, world=1, max_steps=100000,
+                  round=1, stats=None):
+    """run_zja's adaptive round (delta_star > 0) sharded over `world` GPUs; returns the
+    run report with the chosen schedule (`betas`) on every rank."""
+    import torch
+    from . import capi
+    if not delta_star > 0:
+        raise ValueError("run_zja_multi needs delta_star > 0 (calibrate with a sharded SAIS pilot)")
+    ex = exec_ or abi.execopts(abi.RNG_PHILOX, abi.PREC_FP32)
+    dev = torch.device("cuda", ex.device)
+    stream = torch.cuda.Stream(device=dev)
+    ex = abi.execopts(ex.rng, ex.precision, ex.device, ex.lanes, stream.cuda_stream)
+    bounds = [b for b, _ in chunk_partition(n, world)] + [n]
+    ranks = list(range(world)) if comm is None else [rank]
+    comm = comm or VirtualComm(world)
+    n_chunks = [chunks_of((bounds[r], bounds[r + 1])) for r in range(world)]
+    probes = 0
+    with torch.cuda.device(dev), torch.cuda.stream(stream):
+        shards = [capi.ZjaShard(target, kernel, n, bounds[r], bounds[r + 1], seed, round, max_steps, ex) for r in ranks]
+        parts = [torch.empty((s.chunks, abi.SHARD_NACC, 2), dtype=torch.float64, device=dev) for s in shards]
+        btots = [torch.empty((max(s.blocks, 1),), dtype=torch.float64, device=dev) for s in shards]
+
+        def gathered(local):  # all-gather host partials (chunks, 2, 2) in rank (= chunk) order
+            ts = [torch.from_numpy(a).to(dev) for a in local]
+            return [g.cpu().numpy() for g in comm.allgather(ts, n_chunks)][0]
+
+        def fold(allp, k):
+            acc = (-math.inf, 0.0)
+            for c in range(allp.shape[0]):
+                acc = _lacc_combine(acc, (float(allp[c, k, 0]), float(allp[c, k, 1])))
+            return acc
+
+        betas = [0.0]
+        warning = False
+        t = 0
+        while betas[-1] < 1.0:
+            t += 1
+            if t > max_steps:
+                raise capi.AsmcError(abi.ERR_EVALUATION,
+                                     f"online adaptation failed to reach beta = 1 within {max_steps} steps")
+            beta = betas[-1]
+            for s in shards:
+                s.eval()
+            log_m0 = _lacc_total(fold(gathered([s.probe(beta, -1.0) for s in shards]), 0))
+            if log_m0 == -math.inf:
+                raise capi.AsmcError(abi.ERR_DEGENERATE, "all log-weights are -inf")
+
+            def dhat(b2):
+                nonlocal probes
+                probes += 1
+                allp = gathered([s.probe(beta, b2) for s in shards])
+                raw = _lacc_total(fold(allp, 1)) - 2.0 * _lacc_total(fold(allp, 0)) + log_m0
+                return raw if raw > 0.0 else 0.0
+
+            b, w = zja_search(dhat, beta, delta_star)
+            warning = warning or w
+            betas.append(b)
+            for s, p in zip(shards, parts):
+                s.set_beta(t, b)
+                s.step(t, p.data_ptr())
+            allp = comm.allgather(parts, n_chunks)
+            for s, a, bt in zip(shards, allp, btots):
+                s.decide(t, a.data_ptr(), a.shape[0], bt.data_ptr())
+        reps = [s.report(t) for s in shards]
+    stream.synchronize()
+    for s in shards:
+        s.close()
+    for r in reps:
+        r.update(betas=np.array(betas), steps=t, warning=warning, delta_star=delta_star)
+    if stats is not None:
+        stats["probes"] = probes
+        stats["collectives"] = probes + 2 * t  # probes + log_m0 + step partials per step
+    return reps

@@ -95,3 +95,23 @@ def test_sharded_sais_partials_for_step_outer_targets(kind):
         for key in ("log_g0", "log_g1", "log_g2"):
             assert np.array_equal(rep[key], single[key]), (kind, world, key)
         assert rep["log_z_hat"] == single["log_z_hat"]
+
+
+def test_multi_gpu_zja_identical_for_any_shard_count():
+    """every bisection probe is an all-gather of per-chunk partials folded
+    in chunk order, so 1 and 3 shards choose the same schedule bit for bit; the result
+    matches the single-GPU asmc_run_zja (cooperative-grid tree) to fold-order rounding."""
+    tg = abi.gaussian_shift(0.0, 2.0, 1.0, 4)
+    k = abi.kernel(abi.KERNEL_RWMH, (0.1, 0.5, 1.0), 1)
+    ex = abi.execopts(PH, F32)
+    stats = {}
+    one = distributed.run_zja_multi(tg, k, N, 0.05, seed=3, exec_=ex, world=1)
+    three = distributed.run_zja_multi(tg, k, N, 0.05, seed=3, exec_=ex, world=3, stats=stats)
+    assert np.array_equal(one[0]["betas"], three[1]["betas"]) and one[0]["betas"][-1] == 1.0
+    for r in three:
+        assert r["log_z_hat"] == one[0]["log_z_hat"] and np.array_equal(r["log_g1"], one[0]["log_g1"])
+    single = capi.run_zja(tg, k, N, delta_star=0.05, seed=3, exec_=ex)
+    assert single["steps"] == one[0]["steps"]
+    assert np.max(np.abs(single["rounds"][-1]["betas"] - one[0]["betas"])) < 1e-6
+    assert abs(single["rounds"][-1]["log_z_hat"] - one[0]["log_z_hat"]) < 1e-6
+    assert stats["probes"] > 20 * one[0]["steps"]  # the communication the paper's SAIS avoids
