@@ -262,7 +262,7 @@ struct SmemOps {
   }
 
   // sum over this lane's quads of f_beta(x + s z) - f_beta(x).  Early rejection
-  // (exact): after 1, 2, 4 and 6 quad-iterations the group checks
+  // (exact): after each of the first 7 quad-iterations the group checks
   //   partial + sum over unprocessed coordinates of max_h dlg  <  log u
   // (with a rounding margin); then the proposal is rejected whatever the remaining
   // normals are, so they are not drawn.  Accepted proposals see the identical sum.
@@ -275,8 +275,8 @@ struct SmemOps {
     const int mmax = (nq + G - 1) / G;
     int q = lane;
 #pragma unroll 1
-    for (int seg = 0; seg < 5; ++seg) {
-      const int mend = seg == 4 ? mmax : min(mmax, seg == 0 ? 1 : (seg == 1 ? 2 : (seg == 2 ? 4 : 6)));
+    for (int seg = 0; seg < 8; ++seg) {  // checkpoints after quad-iterations 1..7, then the rest
+      const int mend = seg == 7 ? mmax : min(mmax, seg + 1);
       const int qend = min(nq, lane + G * mend);
 #pragma unroll 1
       for (; q < qend; q += G) {
