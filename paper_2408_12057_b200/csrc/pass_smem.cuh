@@ -308,7 +308,8 @@ struct SmemOps {
         }
       }
       const int m = mend;
-      if (!Tgt::kEarly || m >= mmax) break;
+      if (m >= mmax) break;
+      if (!Tgt::kEarly) continue;  // no bound for this target: every segment, no checks
       // partial + remaining bound + a margin dominating the fp32 rounding of both sums
       // (per-lane 1e-4 (|dl| + rem), summed, >= 1e-4 (|sum dl| + sum rem)): one reduction
       const float rem = bnd - bp;

@@ -32,7 +32,11 @@ def targets():
     return [("gauss10", abi.gaussian_shift(0.0, 1.0, 1.0, 10)),
             ("mix5", abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 5)),
             ("scale7", abi.scale_gaussian(1.0, 2.0, 7)),
-            ("gauss100", abi.gaussian_shift(0.0, 0.3, 1.0, 100))]
+            ("gauss100", abi.gaussian_shift(0.0, 0.3, 1.0, 100)),
+            # wide mixtures: several quad-iterations per lane (G = 4: d = 100; G = 32: d = 300),
+            # the multi-segment MH sums of the shared-memory pass without early rejection
+            ("mix100", abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100)),
+            ("mix300", abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 300))]
 
 
 def rel(a, b):
