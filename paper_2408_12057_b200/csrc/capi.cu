@@ -202,8 +202,13 @@ int check_target(const asmc_target_desc* t) {
   return 0;
 }
 
+// shared-memory words per particle quad of the RWMH pass for the target being launched
+// (pass_smem.cuh RowWords: two rows, x + cached vterm for the mixture); set by check_pair
+thread_local int g_row_words = 2;
+
 int check_pair(const asmc_target_desc* t, const asmc_kernel_desc* k) {
   TRY(check_target(t));
+  g_row_words = (t->kind == ASMC_TARGET_MIXTURE ? 2 : 1) * (k && k->kind == ASMC_KERNEL_HMC ? 1 : 2);
   TRY(check_kernel(k));
   if (k->kind == ASMC_KERNEL_IDEALIZED &&
       (t->kind == ASMC_TARGET_MIXTURE || t->kind == ASMC_TARGET_ISING || t->kind == ASMC_TARGET_LOGISTIC))
@@ -322,7 +327,7 @@ int choose_layout_impl(const asmc_exec& ex, int kind, uint64_t d, Layout* L) {
 // shared-memory budget of the many-lanes pass (x quads + per-warp step accumulators)
 int check_smem(Layout L, uint64_t d, int rows, int nacc) {
   if (L.lanes == 1) return 0;
-  const size_t bytes = smem_pass_bytes(L.lanes, d, rows - 1, nacc, 2);  // conservative: cached-v targets
+  const size_t bytes = smem_pass_bytes(L.lanes, d, rows - 1, nacc, g_row_words);
   if (bytes > 227 * 1024)
     return fail(ASMC_ERR_CAPABILITY,
                 "pass needs %zu B of shared memory (dim %llu, %d steps); limit 227 KB", bytes,

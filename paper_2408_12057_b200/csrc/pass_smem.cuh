@@ -39,7 +39,7 @@ struct CacheWords {
 // (no regeneration of its normals).  Same footprint as a cached target's x + vterm.
 template <class Tgt, bool kHmc>
 struct RowWords {
-  static constexpr bool kDual = !kHmc && !Tgt::kCacheV;
+  static constexpr bool kDual = !kHmc;
   static constexpr int value = CacheWords<Tgt>::value * (kDual ? 2 : 1);
 };
 
@@ -290,11 +290,23 @@ struct SmemOps {
           const float4 v = xq[nq + q];
           const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
+          float xp[4], vp[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            xp[e] = fmaf(s, z[e], xv[e]);
+            vp[e] = Tgt::vterm(kf, xp[e]);
+          }
+#pragma unroll
           for (int e = 0; e < 4; ++e)
             if (kAligned || 4 * q + e < d) {
-              dl += Tgt::dlg_cached(kf, xv[e], vv[e], fmaf(s, z[e], xv[e]));
+              const float sx = xv[e] * kf.inv_r, sp = xp[e] * kf.inv_r;
+              dl += fmaf(kf.beta, vp[e] - vv[e], 0.5f * (sx - sp) * (sx + sp));  // == dlg_cached
               if (Tgt::kEarly) bp += Tgt::dmax(kf, xv[e], vv[e]);
             }
+          if constexpr (kDual) {
+            xalt[q] = make_float4(xp[0], xp[1], xp[2], xp[3]);
+            xalt[nq + q] = make_float4(vp[0], vp[1], vp[2], vp[3]);
+          }
         } else {
 #pragma unroll
           for (int e = 0; e < 4; ++e)

@@ -36,7 +36,8 @@ def targets():
             # wide mixtures: several quad-iterations per lane (G = 4: d = 100; G = 32: d = 300),
             # the multi-segment MH sums of the shared-memory pass without early rejection
             ("mix100", abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100)),
-            ("mix300", abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 300))]
+            ("mix300", abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 300)),
+            ("scale300", abi.scale_gaussian(1.0, 2.0, 300))]
 
 
 def rel(a, b):
