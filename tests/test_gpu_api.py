@@ -186,3 +186,17 @@ def test_sharded_round_loop_matches_device_round_loop():
         assert np.array_equal(np.asarray(b["betas"][r]), a["betas"][r][: T + 1])
         assert np.array_equal(np.asarray(b["log_g1"][r]), a["log_g1"][r][: T + 1])
         assert b["log_z_hat"][r] == a["log_z_hat"][r]
+
+
+@pytest.mark.parametrize("width", ["mix100", "scale300"])
+def test_smc_step_mode_wide_targets_close_to_reference(width):
+    """SMC step mode (state loaded from / stored to HBM every step, dual rows, early
+    rejection for the scale family) at widths with several quad-iterations per lane."""
+    ref = oracle.load("ref", PH) if oracle.available("ref", PH) else oracle.load("restate", PH)
+    tg = abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100) if width == "mix100" else abi.scale_gaussian(1.0, 2.0, 300)
+    k = abi.kernel(abi.KERNEL_RWMH, (0.05, 0.2, 1.0), 1)
+    betas = np.linspace(0, 1, 9)
+    a = ref.run_smc(tg, k, betas, 2000, policy=abi.POLICY_NEVER, seed=5, round=1)
+    b = capi.run_smc(tg, k, betas, 2000, policy=abi.POLICY_NEVER, seed=5, round=1, exec_=abi.execopts(PH, F32))
+    assert np.max(np.abs(a["log_g1"][1:] - b["log_g1"][1:]) / np.abs(a["log_g1"][1:]).clip(1)) < 1e-3
+    assert abs(a["log_z_hat"] - b["log_z_hat"]) < 0.05 * max(1.0, abs(a["log_z_hat"]))
