@@ -20,24 +20,31 @@ struct LogAcc {
 
 __host__ __device__ __forceinline__ LogAcc lacc_empty() { return LogAcc{-__builtin_huge_val(), 0.0}; }
 
-// LogAccumulator::add (include/asmc/logsum.hpp:20-28)
+// LogAccumulator::add (include/asmc/logsum.hpp:20-28).  One exp whichever branch
+// is taken (the branches differ only in the argument and the update), so lanes that
+// disagree on the branch still share a single exp: the same bits as the reference's
+// two-branch form.
 __device__ __forceinline__ void lacc_add(LogAcc& a, double l) {
   if (l == -__builtin_huge_val()) return;
-  if (l <= a.max) {
-    a.sum += exp(l - a.max);
+  const bool below = l <= a.max;
+  const double e = exp(below ? l - a.max : a.max - l);
+  if (below) {
+    a.sum += e;
   } else {
-    a.sum = a.sum * exp(a.max - l) + 1.0;
+    a.sum = a.sum * e + 1.0;
     a.max = l;
   }
 }
 
-// SignedLogAccumulator::add (logsum.hpp:55-63)
+// SignedLogAccumulator::add (logsum.hpp:55-63); sign = 1 gives lacc_add's bits
 __device__ __forceinline__ void sacc_add(LogAcc& a, double log_abs, double sign) {
   if (log_abs == -__builtin_huge_val() || sign == 0.0) return;
-  if (log_abs <= a.max) {
-    a.sum += sign * exp(log_abs - a.max);
+  const bool below = log_abs <= a.max;
+  const double e = exp(below ? log_abs - a.max : a.max - log_abs);
+  if (below) {
+    a.sum += sign * e;
   } else {
-    a.sum = a.sum * exp(a.max - log_abs) + sign;
+    a.sum = a.sum * e + sign;
     a.max = log_abs;
   }
 }
@@ -47,10 +54,12 @@ __device__ __forceinline__ void sacc_add(LogAcc& a, double log_abs, double sign)
 // xor-butterfly trees below leave every lane with the identical value.
 __device__ __forceinline__ void lacc_combine(LogAcc& a, const LogAcc& o) {
   if (o.max == -__builtin_huge_val()) return;
-  if (o.max <= a.max) {
-    a.sum += o.sum * exp(o.max - a.max);
+  const bool below = o.max <= a.max;
+  const double e = exp(below ? o.max - a.max : a.max - o.max);
+  if (below) {
+    a.sum += o.sum * e;
   } else {
-    a.sum = a.sum * exp(a.max - o.max) + o.sum;
+    a.sum = a.sum * e + o.sum;
     a.max = o.max;
   }
 }

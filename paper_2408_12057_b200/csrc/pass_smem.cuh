@@ -84,9 +84,12 @@ struct SmemOps {
     refresh_v(T, lane, d, xq);
   }
 
-  __device__ static double weight(const TgtParams& T, int lane, int d, double b0, double b1,
-                                  const float4* xq) {
-    const typename Tgt::F32 kf = Tgt::f32(T, b1);
+  // this lane's sum of vpart(x) over its coordinates (quads lane, lane+G, ...; the
+  // order delta_pass accumulates the proposal's sum in).  vpart does not depend on
+  // beta for any target, so the pass carries the sum across steps and the weight is
+  // one group reduction: V(x) = v_from(sum over lanes).
+  __device__ static float vsum(const TgtParams& T, int lane, int d, const float4* xq) {
+    const typename Tgt::F32 kf = Tgt::f32(T, 0.0);
     const int nq = (d + 3) >> 2;
     float s = 0.f;
     for (int q = lane; q < nq; q += G) {
@@ -103,11 +106,17 @@ struct SmemOps {
       for (int e = 0; e < 4; ++e)
         if (4 * q + e < d) s += xv[e];
     }
-    return (b1 - b0) * Tgt::v_from(T, group_sum<G>((double)s));
+    return s;
   }
 
+  __device__ static double weight(const TgtParams& T, double b0, double b1, float vs) {
+    return (b1 - b0) * Tgt::v_from(T, group_sum<G>((double)vs));
+  }
+
+  // kernel.cpp:26-63 on this particle; vs (the lane's vpart sum) follows x
   __device__ static void move(const TgtParams& T, const KernelCfg& kc, int lane, int d,
-                              double beta, float4*& xq, float4*& xalt, const PhiloxKey& k, uint32_t& drawn) {
+                              double beta, float4*& xq, float4*& xalt, const PhiloxKey& k, uint32_t& drawn,
+                              float& vs) {
     const int nq = (d + 3) >> 2;
     if (kc.kind == ASMC_KERNEL_IDEALIZED) {
       const double mu = Tgt::exact_mu(T, beta);
@@ -119,6 +128,10 @@ struct SmemOps {
         for (int e = 0; e < 4; ++e) v[e] = (4 * q + e < d) ? (float)Tgt::exact_draw(T, mu, (double)z[e]) : 0.f;
         xq[q] = make_float4(v[0], v[1], v[2], v[3]);
       }
+      __syncwarp();
+      refresh_v(T, lane, d, xq);
+      __syncwarp();
+      vs = vsum(T, lane, d, xq);
       return;
     }
     if (kc.kind != (kHmc ? ASMC_KERNEL_HMC : ASMC_KERNEL_RWMH)) return;
@@ -147,6 +160,8 @@ struct SmemOps {
           else hmc_pass<false, true>(kf, k, lane, d, nq, base, eps, kc.leapfrog, xq);
         }
       }
+      __syncwarp();
+      vs = vsum(T, lane, d, xq);
       return;
     }
     // d % 4 == 0: every proposal's draw set starts on a Philox block, so the
@@ -154,9 +169,13 @@ struct SmemOps {
     // generator per loop: the loop body stays inside the L0 I-cache).
     const bool aligned = (d & 3) == 0;
     // early rejection: this lane's sum of max_h dlg(x_i, h) over its coordinates
-    float bnd = Tgt::kEarly ? bound_total(kf, lane, d, nq, xq) : 0.f;
+    // (targets with kBoundFromV derive it from vs inside delta_pass)
+    constexpr bool kBnd = Tgt::kEarly && !Tgt::kBoundFromV;
+    float bnd = kBnd ? bound_total(kf, lane, d, nq, xq) : 0.f;
+    int si = 0;  // p % n_steps
     for (int p = 0; p < nprop; ++p) {
-      const float s = (float)kc.steps[p % kc.n_steps];
+      const float s = (float)kc.steps[si];
+      si = si + 1 == kc.n_steps ? 0 : si + 1;
       const uint64_t base = (uint64_t)p * (uint64_t)d;
       if ((p % G) == 0) {
         const int pp = p + lane;
@@ -164,8 +183,11 @@ struct SmemOps {
       }
       const double log_u = __shfl_sync(0xffffffffu, lu_pre, gbase + (p % G));
       bool rejected = false;
-      const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, rejected, drawn)
-                               : delta_pass<false>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, rejected, drawn);
+      float vs_new = 0.f;
+      const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, rejected,
+                                                  vs_new, drawn)
+                               : delta_pass<false>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, rejected,
+                                                   vs_new, drawn);
       if (rejected) continue;  // certainly rejected: the remaining normals are never drawn
       const double delta = group_sum<G>((double)dl);
       if (log_u < delta) {  // kernel.cpp:35: accept
@@ -175,12 +197,14 @@ struct SmemOps {
           float4* t = xq;
           xq = xalt;
           xalt = t;
-          if (Tgt::kEarly) bnd = bound_total(kf, lane, d, nq, xq);
+          vs = vs_new;
+          if (kBnd) bnd = bound_total(kf, lane, d, nq, xq);
         } else {  // regenerate the proposal's normals
           const float nb = aligned ? accept_pass<true>(kf, k, lane, nq, base, s, xq)
                                    : accept_pass<false>(kf, k, lane, nq, base, s, xq);
           drawn += (uint32_t)((nq - lane + G - 1) / G);
-          if (Tgt::kEarly) bnd = nb;
+          if (kBnd) bnd = nb;
+          vs = vsum(T, lane, d, xq);
         }
       }
     }
@@ -261,76 +285,90 @@ struct SmemOps {
     return dl;
   }
 
-  // sum over this lane's quads of f_beta(x + s z) - f_beta(x).  Early rejection
-  // (exact): after each of the first 7 quad-iterations the group checks
+  // is the proposal certainly rejected?  v = this lane's partial MH sum + the bound of its
+  // unprocessed coordinates + a margin dominating the fp32 rounding of both sums
+  // (1e-4 (|dl| + rem) per lane, plus 1e-2 against log u).
+  //  G == 32 (one particle per warp): each lane's v rounded UP to a multiple of 2^-8
+  //    (clamped below at -4096, which only raises it; values above 65536 become 2^17,
+  //    which keeps the total positive), summed exactly by one REDUX: an upper bound of
+  //    the real sum, warp-uniform, no shuffle chain.
+  //  G < 32: an fp32 group butterfly and a warp vote (the exit must be warp-uniform).
+  __device__ static bool certainly_rejected(float dl, float rem, float lu) {
+    const float v = dl + rem + 1e-4f * (fabsf(dl) + rem);
+    if constexpr (G == 32) {
+      float c = fmaxf(v * 256.f, -0x1.0p20f);
+      c = c > 0x1.0p24f ? 0x1.0p25f : c;
+      const int S = __reduce_add_sync(0xffffffffu, __float2int_ru(c));
+      return S < __float2int_ru((lu - 1e-2f) * 256.f);
+    } else {
+      const float sum = group_sumf<G>(v);
+      return __all_sync(0xffffffffu, sum < lu - 1e-2f);
+    }
+  }
+
+  // sum over this lane's quads of f_beta(x + s z) - f_beta(x), writing x + s z to the
+  // spare row and its vpart sum to vs_new.  Early rejection (exact): after each of the
+  // first 7 quad-iterations the warp checks
   //   partial + sum over unprocessed coordinates of max_h dlg  <  log u
-  // (with a rounding margin); then the proposal is rejected whatever the remaining
-  // normals are, so they are not drawn.  Accepted proposals see the identical sum.
+  // (certainly_rejected); then the proposal is rejected whatever the remaining normals
+  // are, so they are not drawn.  Accepted proposals see the identical sum.
   template <bool kAligned>
   __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane, int d, int nq,
                                      uint64_t base, float s, const float4* xq, float4* xalt, double log_u,
-                                     float bnd, bool& rejected, uint32_t& drawn) {
-    float dl = 0.f, bp = 0.f;
+                                     float bnd, float vs, bool& rejected, float& vs_new, uint32_t& drawn) {
+    float dl = 0.f, bp = 0.f, vn = 0.f;
     const float lu = (float)log_u;
     const int mmax = (nq + G - 1) / G;
     int q = lane;
 #pragma unroll 1
-    for (int seg = 0; seg < 8; ++seg) {  // checkpoints after quad-iterations 1..7, then the rest
-      const int mend = seg == 7 ? mmax : min(mmax, seg + 1);
-      const int qend = min(nq, lane + G * mend);
-#pragma unroll 1
-      for (; q < qend; q += G) {
+    for (int m = 0; m < mmax; ++m, q += G) {
+      if (q < nq) {
         ++drawn;
         float z[4];
         if (kAligned) k.template normals4<float>((uint32_t)(base >> 2) + (uint32_t)q, z);
         else k.template normals4_at<float>(base + 4 * (uint64_t)q, z);
         const float4 x = xq[q];
         const float xv[4] = {x.x, x.y, x.z, x.w};
+        float xp[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) xp[e] = fmaf(s, z[e], xv[e]);
         if constexpr (kCache) {
           const float4 v = xq[nq + q];
           const float vv[4] = {v.x, v.y, v.z, v.w};
+          float vp[4];
 #pragma unroll
-          float xp[4], vp[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            xp[e] = fmaf(s, z[e], xv[e]);
-            vp[e] = Tgt::vterm(kf, xp[e]);
-          }
+          for (int e = 0; e < 4; ++e) vp[e] = Tgt::vterm(kf, xp[e]);
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (kAligned || 4 * q + e < d) {
               const float sx = xv[e] * kf.inv_r, sp = xp[e] * kf.inv_r;
               dl += fmaf(kf.beta, vp[e] - vv[e], 0.5f * (sx - sp) * (sx + sp));  // == dlg_cached
               if (Tgt::kEarly) bp += Tgt::dmax(kf, xv[e], vv[e]);
+              vn += vp[e];
             }
-          if constexpr (kDual) {
-            xalt[q] = make_float4(xp[0], xp[1], xp[2], xp[3]);
-            xalt[nq + q] = make_float4(vp[0], vp[1], vp[2], vp[3]);
-          }
+          if constexpr (kDual) xalt[nq + q] = make_float4(vp[0], vp[1], vp[2], vp[3]);
         } else {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (kAligned || 4 * q + e < d) {
               dl += Tgt::dlg(kf, xv[e], s * z[e]);
-              if (Tgt::kEarly) bp += Tgt::dmax(kf, xv[e], 0.f);
+              if (Tgt::kEarly) bp += Tgt::kBoundFromV ? Tgt::vpart(kf, xv[e]) : Tgt::dmax(kf, xv[e], 0.f);
+              vn += Tgt::vpart(kf, xp[e]);
             }
-          if constexpr (kDual)
-            xalt[q] = make_float4(fmaf(s, z[0], xv[0]), fmaf(s, z[1], xv[1]), fmaf(s, z[2], xv[2]),
-                                  fmaf(s, z[3], xv[3]));
+        }
+        if constexpr (kDual) xalt[q] = make_float4(xp[0], xp[1], xp[2], xp[3]);
+      }
+      if constexpr (Tgt::kEarly) {
+        if (m < 7 && m + 1 < mmax) {  // warp-uniform: every lane runs mmax iterations
+          const float rem = Tgt::kBoundFromV ? Tgt::bound_of_v(kf, vs - bp) : bnd - bp;
+          if (certainly_rejected(dl, rem, lu)) {
+            rejected = true;
+            return dl;
+          }
         }
       }
-      const int m = mend;
-      if (m >= mmax) break;
-      if (!Tgt::kEarly) continue;  // no bound for this target: every segment, no checks
-      // partial + remaining bound + a margin dominating the fp32 rounding of both sums
-      // (per-lane 1e-4 (|dl| + rem), summed, >= 1e-4 (|sum dl| + sum rem)): one reduction
-      const float rem = bnd - bp;
-      const float v = group_sumf<G>(dl + rem + 1e-4f * (fabsf(dl) + rem));
-      if (__all_sync(0xffffffffu, v < lu - 1e-2f)) {  // warp-uniform exit
-        rejected = true;
-        return dl;
-      }
     }
+    vs_new = vn;
     return dl;
   }
 
@@ -374,17 +412,20 @@ __device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_po
   const int ln = threadIdx.x & 31;
   if (G == 32) {
     // one particle per warp: lane a owns accumulator a (no tree, no serial chain)
+    // (lanes 0-4 share one signed add: lacc_add(l) == sacc_add(l, 1), one exp for all)
     if (ln < nacc && active) {
       LogAcc v = acc[ln];
-      switch (ln) {
-        case kAccG0: lacc_add(v, lw_pre); break;
-        case kAccG1: lacc_add(v, lw_pre + lg); break;
-        case kAccG2: lacc_add(v, lw_pre + 2.0 * lg); break;
-        case kAccElbo:
-          if (lg != 0.0) sacc_add(v, lw_pre + log(fabs(lg)), lg > 0.0 ? 1.0 : -1.0);
-          break;
-        case kAccSq: lacc_add(v, 2.0 * lw_post); break;
-        default: top2_add(v, lw_post); break;
+      if (ln == kAccTop2) {
+        top2_add(v, lw_post);
+      } else {
+        double l = ln == kAccG0 ? lw_pre : (ln == kAccG1 ? lw_pre + lg : lw_pre + 2.0 * lg);
+        double sign = 1.0;
+        if (ln == kAccSq) l = 2.0 * lw_post;
+        if (ln == kAccElbo) {
+          l = lg != 0.0 ? lw_pre + log(fabs(lg)) : -__builtin_huge_val();
+          sign = lg > 0.0 ? 1.0 : -1.0;
+        }
+        sacc_add(v, l, sign);
       }
       acc[ln] = v;
     }
@@ -445,6 +486,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
     const bool active = local < A.n_local;
     const uint64_t pid = A.mode == kModeTraj ? (active ? A.pids[local] : 0) : A.p_begin + local;
     double lw = 0.0;
+    float vs = 0.f;  // this lane's sum of vpart(x) (SmemOps::vsum)
     if (A.mode == kModeSmcStep) {
       const float4* src = reinterpret_cast<const float4*>(
           reinterpret_cast<const float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d);
@@ -471,6 +513,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
       Ops::init(A.tg, lane, d, xq, k, drawn);
     }
     __syncwarp();
+    vs = Ops::vsum(A.tg, lane, d, xq);
     if (A.mode == kModeSmcInit) {
       if (active) {
         float* dst = reinterpret_cast<float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d;
@@ -493,11 +536,11 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
     }
     for (int t = A.t_begin; t <= A.t_end; ++t) {
       const double b0 = A.betas[t - 1], b1 = A.betas[t];
-      const double lg = Ops::weight(A.tg, lane, d, b0, b1, xq);
+      const double lg = Ops::weight(A.tg, b0, b1, vs);
       PhiloxKey k;
       k.init(A.seed, A.round, pid, (uint64_t)t, 1);
       __syncwarp();
-      Ops::move(A.tg, A.kc, lane, d, b1, xq, xalt, k, drawn);
+      Ops::move(A.tg, A.kc, lane, d, b1, xq, xalt, k, drawn, vs);
       __syncwarp();
       const double pre = lw;
       lw += lg;

@@ -99,66 +99,52 @@ __device__ __forceinline__ uint4 philox10(uint4 c, uint32_t k0, uint32_t k1) {
   return c;
 }
 
-// ln(s) for normal s in [2^-32, 1]: Cephes-style logf without the special
-// cases the library logf carries (denormals, 0, inf, NaN cannot occur here).
-// s = 2^e m, m in [sqrt(1/2), sqrt(2)), log1p(m - 1) by a degree-8 polynomial.
-__device__ __forceinline__ float log_unit(float s) {
-  const int i = __float_as_int(s);
-  const int e = (i - 0x3f3504f3) >> 23;
-  const float m = __int_as_float(i - (e << 23));
-  const float t = m - 1.0f;
-  const float z = t * t;
-  float y = 7.0376836292E-2f;
-  y = fmaf(y, t, -1.1514610310E-1f);
-  y = fmaf(y, t, 1.1676998740E-1f);
-  y = fmaf(y, t, -1.2420140846E-1f);
-  y = fmaf(y, t, 1.4249322787E-1f);
-  y = fmaf(y, t, -1.6668057665E-1f);
-  y = fmaf(y, t, 2.0000714765E-1f);
-  y = fmaf(y, t, -2.4999993993E-1f);
-  y = fmaf(y, t, 3.3333331174E-1f);
-  y = (y * t) * z;
-  const float ef = (float)e;
-  y = fmaf(ef, -2.12194440e-4f, y);
-  y = fmaf(-0.5f, z, y);
-  return fmaf(ef, 0.693359375f, t + y);
+// MUFU (SFU) approximations, ftz: inputs here are never denormal.
+__device__ __forceinline__ float mufu_lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float mufu_sqrt(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float mufu_sin(float x) {
+  float y;
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float mufu_cos(float x) {
+  float y;
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // Box-Muller pair in fp32 from two 32-bit words -- the shadow stream's
 // u1 = (a+1) 2^-32, u2 = b 2^-32, r = sqrt(-2 ln u1), angle 2 pi u2
-// (oracle/shadow/asmc/rng.hpp) to fp32 accuracy:
-//  * ln u1 of the exactly rounded head plus a first-order tail, so u1 -> 1
-//    keeps full relative accuracy;
-//  * the angle's quadrant comes from the top two bits of b, the remaining 30
-//    bits give phi in [-pi/4, pi/4) where short sin/cos polynomials are exact
-//    to an ulp; the quadrant rotation is two selects and two sign flips, and
-//    the 1/sqrt(2) of the rotation is folded into r = sqrt(-ln u1) * sqrt(2)/sqrt(2).
+// (oracle/shadow/asmc/rng.hpp) -- on the SFU: 4 MUFU ops + ~20 ALU per pair.
+//  * -ln u1: for u1 <= 31/32, -ln2 * lg2(u1) (|log2 u1| >= 0.046, so the SFU's
+//    ~2^-22 absolute error is <= 6e-6 relative); for u1 > 31/32 the SFU loses
+//    relative accuracy, so t = 1 - u1 = (~a) 2^-32 (exact word arithmetic) and
+//    -ln(1 - t) = t (1 + t/2 + t^2/3 + t^3/4 + t^4/5) (truncation < t^5/6 < 2^-27);
+//  * the angle as a signed word: (int)b 2^-32 * 2 pi = 2 pi u2 - 2 pi [b >= 2^31]
+//    lies in [-pi, pi), the SFU's accurate range (2^-20.5 absolute), with the
+//    same sine and cosine.
+// Normals agree with the fp64 transform to ~1e-6 absolute (tests/test_gpu_parity.py).
 __device__ __forceinline__ void bm_pair_f32(uint32_t a, uint32_t b, float& n_cos, float& n_sin) {
-  const float fa = __uint2float_rz(a);
-  const uint32_t resid = a - __float2uint_rz(fa);          // 0..255, exact
-  const float A = fa * 0x1.0p-32f;                          // exact
-  const float E = __uint2float_rn(resid + 1u) * 0x1.0p-32f; // exact
-  const float s = A + E;
-  const float corr = E - (s - A);                           // Fast2Sum tail of u1
-  const float lnu = log_unit(s) + fmaf(-s, corr, 2.0f * corr);  // ~ ln s + corr / s
-  const float v = -lnu;
-  const float rk = v * rsqrtf(fmaxf(v, 1e-30f));           // sqrt(-ln u1) = r / sqrt(2)
-  const float phi = fmaf(__uint2float_rn(b & 0x3FFFFFFFu), 1.46291807926715968e-09f,
-                         -0.785398163397448310f);          // (pi/2)(f 2^-30 - 1/2)
-  const float z = phi * phi;
-  const float sp = fmaf(fmaf(-1.9515295891E-4f, z, 8.3321608736E-3f), z, -1.6666654611E-1f);
-  const float sn = fmaf(sp * z, phi, phi);
-  const float cp = fmaf(fmaf(2.443315711809948E-5f, z, -1.388731625493765E-3f), z,
-                        4.166664568298827E-2f);
-  const float cs = fmaf(cp * z, z, fmaf(-0.5f, z, 1.0f));
-  // angle = pi/4 + q pi/2 + phi, q = b >> 30
-  const float ap = cs + sn, bm = cs - sn;
-  const bool odd = (b >> 30) & 1u;
-  const float sv = odd ? bm : ap, cv = odd ? ap : bm;
-  const uint32_t ssgn = b & 0x80000000u;
-  const uint32_t csgn = (b ^ (b << 1)) & 0x80000000u;
-  n_sin = __int_as_float(__float_as_int(rk) ^ ssgn) * sv;
-  n_cos = __int_as_float(__float_as_int(rk) ^ csgn) * cv;
+  const float u1 = fmaf(__uint2float_rn(a), 0x1.0p-32f, 0x1.0p-32f);
+  const float v_log = -0.693147180559945309f * mufu_lg2(u1);
+  const float t = __uint2float_rn(~a) * 0x1.0p-32f;
+  float q = fmaf(t, 0.2f, 0.25f);
+  q = fmaf(t, q, 0.333333343f);
+  q = fmaf(t, q, 0.5f);
+  q = fmaf(t, q, 1.0f);
+  const float v = t < 0.03125f ? t * q : v_log;  // -ln u1
+  const float r = mufu_sqrt(v + v);
+  const float ang = __int2float_rn((int)b) * 1.46291807926715968e-09f;  // 2 pi 2^-32
+  n_cos = r * mufu_cos(ang);
+  n_sin = r * mufu_sin(ang);
 }
 
 __device__ __forceinline__ void bm_pair_f64(uint32_t a, uint32_t b, double& n_cos, double& n_sin) {

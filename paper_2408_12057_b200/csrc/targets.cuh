@@ -70,6 +70,8 @@ struct TgtGaussShift {
   __device__ static float vpart(const F32&, float x) { return x; }
   // early rejection: max over h of dlg(x, h) (a concave quadratic in h)
   static constexpr bool kEarly = true;
+  static constexpr bool kBoundFromV = false;
+  __device__ static float bound_of_v(const F32&, float) { return 0.f; }
   __device__ static float dmax(const F32& k, float x, float) {
     const float g = k.ba - (x - k.mu0) * k.inv_s2;
     return __fdividef(0.5f * g * g, k.inv_s2);
@@ -116,6 +118,8 @@ struct TgtMixture {
   // early rejection: f_beta(y) = beta (hi + log1p) - (1 - beta) sr^2 / 2 <= beta lmix, so
   // max_h dlg(x, h) <= beta (lmix - vterm(x)) + sr(x)^2 / 2  (v = the cached vterm(x))
   static constexpr bool kEarly = false;  // bound too loose at d = 100 to pay for its bookkeeping
+  static constexpr bool kBoundFromV = false;
+  __device__ static float bound_of_v(const F32&, float) { return 0.f; }
   __device__ static float dmax(const F32& k, float x, float v) {
     const float sr = x * k.inv_r;
     return fmaf(k.beta, k.lmix - v, 0.5f * sr * sr);
@@ -218,6 +222,10 @@ struct TgtScale {
   // early rejection: max over h of -tau h (x + h/2) = tau x^2 / 2
   static constexpr bool kEarly = true;
   __device__ static float dmax(const F32& k, float x, float) { return 0.5f * k.tau * x * x; }
+  // dmax summed over coordinates = (tau / 2) * sum vpart(x): the pass derives the bound of
+  // the unprocessed coordinates from the carried vpart sum, no separate bound pass
+  static constexpr bool kBoundFromV = true;
+  __device__ static float bound_of_v(const F32& k, float v) { return 0.5f * k.tau * v; }
   __device__ static double v_from(const TgtParams& T, double s) {
     return T.c[4] * s - (double)T.dim * T.c[5];
   }
