@@ -41,7 +41,10 @@ static cudaError_t go_smem_k(const PassArgs& A, uint64_t blocks, cudaStream_t s)
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  pass_smem_kernel<Tgt, G, kHmc><<<(unsigned)blocks, kBlock, bytes, s>>>(A);
+  PassArgs Ak = A;
+  philox_round_keys(A.seed, A.round, 0, Ak.rk[0]);
+  philox_round_keys(A.seed, A.round, 1, Ak.rk[1]);
+  pass_smem_kernel<Tgt, G, kHmc><<<(unsigned)blocks, kBlock, bytes, s>>>(Ak);
   return cudaGetLastError();
 }
 // HMC gets its own instantiation so the RWMH pass keeps its lean register allocation

@@ -64,6 +64,7 @@ struct PassArgs {
   double* rec_lw;        // kModeTraj: [i * (T+1) + t]
   int* err;
   unsigned long long* drawn;  // profiling: normals actually generated (null = off)
+  PhiloxRoundKeys rk[2];      // Philox round keys of (seed, round, substep 0 | 1): set at launch
 };
 
 // coordinate owned by (lane, slot k): quads of 4 consecutive coordinates dealt

@@ -49,7 +49,7 @@ struct SmemOps {
   static constexpr bool kDual = RowWords<Tgt, kHmc>::kDual;
 
   // normals 4q .. 4q+3 of the draw set based at `base`
-  __device__ static void quad(const PhiloxKey& k, uint64_t base, int q, float z[4]) {
+  __device__ static void quad(const PhiloxKeyC& k, uint64_t base, int q, float z[4]) {
     const uint64_t j0 = base + 4 * (uint64_t)q;
     if ((base & 3) == 0) k.template normals4<float>((uint32_t)(j0 >> 2), z);
     else k.template normals4_at<float>(j0, z);
@@ -69,7 +69,7 @@ struct SmemOps {
     }
   }
 
-  __device__ static void init(const TgtParams& T, int lane, int d, float4* xq, const PhiloxKey& k,
+  __device__ static void init(const TgtParams& T, int lane, int d, float4* xq, const PhiloxKeyC& k,
                               uint32_t& drawn) {
     const int nq = (d + 3) >> 2;
     for (int q = lane; q < nq; q += G) {
@@ -115,7 +115,7 @@ struct SmemOps {
 
   // kernel.cpp:26-63 on this particle; vs (the lane's vpart sum) follows x
   __device__ static void move(const TgtParams& T, const KernelCfg& kc, int lane, int d,
-                              double beta, float4*& xq, float4*& xalt, const PhiloxKey& k, uint32_t& drawn,
+                              double beta, float4*& xq, float4*& xalt, const PhiloxKeyC& k, uint32_t& drawn,
                               float& vs) {
     const int nq = (d + 3) >> 2;
     if (kc.kind == ASMC_KERNEL_IDEALIZED) {
@@ -172,16 +172,20 @@ struct SmemOps {
     // (targets with kBoundFromV derive it from vs inside delta_pass)
     constexpr bool kBnd = Tgt::kEarly && !Tgt::kBoundFromV;
     float bnd = kBnd ? bound_total(kf, lane, d, nq, xq) : 0.f;
+    double u_pre = 1.0;  // lane l holds u of proposal (q0 + l)
     int si = 0;  // p % n_steps
     for (int p = 0; p < nprop; ++p) {
       const float s = (float)kc.steps[si];
       si = si + 1 == kc.n_steps ? 0 : si + 1;
       const uint64_t base = (uint64_t)p * (uint64_t)d;
-      if ((p % G) == 0) {
+      if ((p % G) == 0) {  // lane l draws the uniform of proposal p + l
         const int pp = p + lane;
-        lu_pre = pp < nprop ? log(k.uniform((uint32_t)pp)) : 0.0;
+        u_pre = pp < nprop ? k.uniform((uint32_t)pp) : 1.0;
       }
-      const double log_u = __shfl_sync(0xffffffffu, lu_pre, gbase + (p % G));
+      const double u = __shfl_sync(0xffffffffu, u_pre, gbase + (p % G));
+      // log u on the SFU (|error| <= 1e-6 (1 + |log u|)); the fp64 log only when the
+      // decision is that close (accept_decision): decisions equal log(u) < delta exactly
+      const float log_u = sfu_lg2((float)u) * 0.693147180559945309f;
       bool rejected = false;
       float vs_new = 0.f;
       const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, rejected,
@@ -190,7 +194,7 @@ struct SmemOps {
                                                    vs_new, drawn);
       if (rejected) continue;  // certainly rejected: the remaining normals are never drawn
       const double delta = group_sum<G>((double)dl);
-      if (log_u < delta) {  // kernel.cpp:35: accept
+      if (accept_decision(u, log_u, delta)) {  // kernel.cpp:35: accept iff log u < delta
         if constexpr (kDual) {  // the proposal is already in the spare row
           // only this particle's lanes take the branch (G < 32: other groups may reject)
           __syncwarp(G == 32 ? 0xffffffffu : (((1u << G) - 1u) << gbase));
@@ -247,7 +251,7 @@ struct SmemOps {
   // HMC over this lane's quads: kWrite = false -> energy difference
   // H(x,p0) - H(x',p'); kWrite = true -> store the accepted x' (and vterm)
   template <bool kAligned, bool kWrite>
-  __device__ static float hmc_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane, int d,
+  __device__ static float hmc_pass(const typename Tgt::F32& kf, const PhiloxKeyC& k, int lane, int d,
                                    int nq, uint64_t base, float eps, int L, float4* xq) {
     float dl = 0.f;
 #pragma unroll 1
@@ -285,6 +289,14 @@ struct SmemOps {
     return dl;
   }
 
+  // log u < delta, with log u from the SFU unless the two are within its error bound
+  __device__ static bool accept_decision(double u, float log_u_sfu, double delta) {
+    const double tol = 1e-5 * (1.0 + fabs((double)log_u_sfu));
+    if (delta > (double)log_u_sfu + tol) return true;
+    if (delta < (double)log_u_sfu - tol) return false;
+    return log(u) < delta;
+  }
+
   // is the proposal certainly rejected?  v = this lane's partial MH sum + the bound of its
   // unprocessed coordinates + a margin dominating the fp32 rounding of both sums
   // (1e-4 (|dl| + rem) per lane, plus 1e-2 against log u).
@@ -313,11 +325,11 @@ struct SmemOps {
   // (certainly_rejected); then the proposal is rejected whatever the remaining normals
   // are, so they are not drawn.  Accepted proposals see the identical sum.
   template <bool kAligned>
-  __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane, int d, int nq,
-                                     uint64_t base, float s, const float4* xq, float4* xalt, double log_u,
+  __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKeyC& k, int lane, int d, int nq,
+                                     uint64_t base, float s, const float4* xq, float4* xalt, float log_u,
                                      float bnd, float vs, bool& rejected, float& vs_new, uint32_t& drawn) {
     float dl = 0.f, bp = 0.f, vn = 0.f;
-    const float lu = (float)log_u;
+    const float lu = log_u;
     const int mmax = (nq + G - 1) / G;
     int q = lane;
 #pragma unroll 1
@@ -373,7 +385,7 @@ struct SmemOps {
   }
 
   template <bool kAligned>
-  __device__ static float accept_pass(const typename Tgt::F32& kf, const PhiloxKey& k, int lane,
+  __device__ static float accept_pass(const typename Tgt::F32& kf, const PhiloxKeyC& k, int lane,
                                       int nq, uint64_t base, float s, float4* xq) {
     float b = 0.f;  // the new x's early-rejection bound (same order as bound_total)
 #pragma unroll 1
@@ -508,8 +520,8 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
       __syncwarp();
       Ops::refresh_v(A.tg, lane, d, xq);
     } else {
-      PhiloxKey k;
-      k.init(A.seed, A.round, pid, 0, 0);
+      PhiloxKeyC k;
+      k.init(A.rk[0], pid, 0);
       Ops::init(A.tg, lane, d, xq, k, drawn);
     }
     __syncwarp();
@@ -537,8 +549,8 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
     for (int t = A.t_begin; t <= A.t_end; ++t) {
       const double b0 = A.betas[t - 1], b1 = A.betas[t];
       const double lg = Ops::weight(A.tg, b0, b1, vs);
-      PhiloxKey k;
-      k.init(A.seed, A.round, pid, (uint64_t)t, 1);
+      PhiloxKeyC k;
+      k.init(A.rk[1], pid, (uint64_t)t);
       __syncwarp();
       Ops::move(A.tg, A.kc, lane, d, b1, xq, xalt, k, drawn, vs);
       __syncwarp();

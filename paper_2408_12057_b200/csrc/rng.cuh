@@ -13,7 +13,7 @@
 
 namespace asmcdev {
 
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   return z ^ (z >> 31);
@@ -167,16 +167,22 @@ __device__ __forceinline__ void bm_pair<double>(uint32_t a, uint32_t b, double& 
   bm_pair_f64(a, b, c, s);
 }
 
+// the Philox key of (seed, round, substep): the same for every particle and step
+__host__ __device__ __forceinline__ void philox_key(uint64_t seed, uint64_t round, uint64_t substep,
+                                                    uint32_t& k0, uint32_t& k1) {
+  uint64_t acc = mix64(seed + 0x9E3779B97F4A7C15ULL);
+  acc = mix64(acc ^ (round + 0xD1B54A32D192ED03ULL));
+  acc = mix64(acc ^ (substep + 0x9FB21C651E98DF25ULL));
+  k0 = (uint32_t)acc;
+  k1 = (uint32_t)(acc >> 32);
+}
+
 struct PhiloxKey {
   uint32_t k0, k1, c1, c2, c3;
 
   __device__ __forceinline__ void init(uint64_t seed, uint64_t round, uint64_t particle,
                                        uint64_t step, uint64_t substep) {
-    uint64_t acc = mix64(seed + 0x9E3779B97F4A7C15ULL);
-    acc = mix64(acc ^ (round + 0xD1B54A32D192ED03ULL));
-    acc = mix64(acc ^ (substep + 0x9FB21C651E98DF25ULL));
-    k0 = (uint32_t)acc;
-    k1 = (uint32_t)(acc >> 32);
+    philox_key(seed, round, substep, k0, k1);
     c1 = (uint32_t)step;
     c2 = (uint32_t)particle;
     c3 = (uint32_t)(particle >> 32) ^ ((uint32_t)(step >> 32) * 0x9E3779B9u);
@@ -199,6 +205,82 @@ struct PhiloxKey {
     bm_pair<Real>(w.z, w.w, out[2], out[3]);
   }
   // normals j0 .. j0+3 for an arbitrary (possibly unaligned) j0
+  template <typename Real>
+  __device__ __forceinline__ void normals4_at(uint64_t j0, Real out[4]) const {
+    const uint32_t b = (uint32_t)(j0 >> 2);
+    const int off = (int)(j0 & 3);
+    Real lo[4];
+    normals4<Real>(b, lo);
+    if (off == 0) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) out[e] = lo[e];
+      return;
+    }
+    Real hi[4];
+    normals4<Real>(b + 1, hi);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int w = off + e;
+      out[e] = w < 4 ? lo[w & 3] : hi[w & 3];
+    }
+  }
+};
+
+// Round keys of one launch-uniform Philox key (k0 + r W0, k1 + r W1, r = 0..9),
+// computed on the host: inside a kernel parameter they feed the round LOP3s as
+// constant-bank operands, so the hot loops carry no key schedule (no registers,
+// no adds).
+struct PhiloxRoundKeys {
+  uint32_t k0[10], k1[10];
+};
+
+inline void philox_round_keys(uint64_t seed, uint64_t round, uint64_t substep, PhiloxRoundKeys& rk) {
+  uint32_t k0, k1;
+  philox_key(seed, round, substep, k0, k1);
+  for (int r = 0; r < 10; ++r) {
+    rk.k0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+    rk.k1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+  }
+}
+
+__device__ __forceinline__ uint4 philox10_rk(uint4 c, const PhiloxRoundKeys& rk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t lo0, hi0, lo1, hi1;
+    mulwide(0xD2511F53u, c.x, lo0, hi0);
+    mulwide(0xCD9E8D57u, c.z, lo1, hi1);
+    c = make_uint4(hi1 ^ c.y ^ rk.k0[r], lo1, hi0 ^ c.w ^ rk.k1[r], lo0);
+  }
+  return c;
+}
+
+// PhiloxKey with the round keys read from a kernel parameter (same stream bits)
+struct PhiloxKeyC {
+  const PhiloxRoundKeys* rk;
+  uint32_t c1, c2, c3;
+
+  __device__ __forceinline__ void init(const PhiloxRoundKeys& keys, uint64_t particle, uint64_t step) {
+    rk = &keys;
+    c1 = (uint32_t)step;
+    c2 = (uint32_t)particle;
+    c3 = (uint32_t)(particle >> 32) ^ ((uint32_t)(step >> 32) * 0x9E3779B9u);
+  }
+  __device__ __forceinline__ uint4 block(uint32_t b) const {
+    return philox10_rk(make_uint4(b, c1, c2, c3), *rk);
+  }
+  __device__ __forceinline__ uint64_t u64(uint32_t k) const {
+    const uint4 w = philox10_rk(make_uint4(0x80000000u | k, c1, c2, c3), *rk);
+    return ((uint64_t)w.x << 32) | w.y;
+  }
+  __device__ __forceinline__ double uniform(uint32_t k) const {
+    return (double)(u64(k) >> 11) * 0x1.0p-53;
+  }
+  template <typename Real>
+  __device__ __forceinline__ void normals4(uint32_t b, Real out[4]) const {
+    const uint4 w = block(b);
+    bm_pair<Real>(w.x, w.y, out[0], out[1]);
+    bm_pair<Real>(w.z, w.w, out[2], out[3]);
+  }
   template <typename Real>
   __device__ __forceinline__ void normals4_at(uint64_t j0, Real out[4]) const {
     const uint32_t b = (uint32_t)(j0 >> 2);

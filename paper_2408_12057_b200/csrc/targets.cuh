@@ -18,6 +18,13 @@ namespace asmcdev {
 
 constexpr double kLogSqrt2Pi = 0.91893853320467274178;  // src/target.cpp:13
 
+// log2 on the SFU (lg2.approx: ~2^-22 absolute on [0.5, 2), relative elsewhere)
+__device__ __forceinline__ float sfu_lg2(float v) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 struct TgtParams {
   int kind;
   int pad;
