@@ -443,28 +443,37 @@ __device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_po
     }
     return;
   }
-  const bool leader = (ln % G) == 0;
-  for (int a = 0; a < nacc; ++a) {
-    LogAcc v = (a == kAccTop2) ? LogAcc{-__builtin_huge_val(), -__builtin_huge_val()} : lacc_empty();
-    if (leader && active) {
-      switch (a) {
-        case kAccG0: lacc_add(v, lw_pre); break;
-        case kAccG1: lacc_add(v, lw_pre + lg); break;
-        case kAccG2: lacc_add(v, lw_pre + 2.0 * lg); break;
-        case kAccElbo:
-          if (lg != 0.0) sacc_add(v, lw_pre + log(fabs(lg)), lg > 0.0 ? 1.0 : -1.0);
-          break;
-        case kAccSq: lacc_add(v, 2.0 * lw_post); break;
-        default: top2_add(v, lw_post); break;
+  // G < 32: the warp holds 32/G particles.  Lane l of every group evaluates accumulator
+  // a = a0 + l for its particle, the groups' values are combined by a max butterfly and
+  // one exp per lane followed by a sum butterfly (every lane ends with the same bits),
+  // and group 0's lane l merges the resulting (max, signed sum) into the warp's running
+  // accumulator: 2 fp64 exps per accumulator row instead of one per tree level.
+  const int l = ln % G;
+  const int nlog = nacc > kAccTop2 ? kAccTop2 : nacc;  // log-sum accumulators (top-2 below)
+  for (int a0 = 0; a0 < nlog; a0 += G) {
+    const int a = a0 + l;
+    double val = -__builtin_huge_val(), sign = 1.0;
+    if (active && a < nlog) {
+      val = a == kAccG0 ? lw_pre : (a == kAccG1 ? lw_pre + lg : lw_pre + 2.0 * lg);
+      if (a == kAccSq) val = 2.0 * lw_post;
+      if (a == kAccElbo) {
+        val = lg != 0.0 ? lw_pre + log(fabs(lg)) : -__builtin_huge_val();
+        sign = lg > 0.0 ? 1.0 : -1.0;
       }
     }
+    double mx = val;
 #pragma unroll
-    for (int m = G; m < 32; m <<= 1) {
-      const LogAcc o = shfl_xor_acc(v, m);
-      if (a == kAccTop2) top2_merge(v, o);
-      else lacc_combine(v, o);
-    }
-    if (ln == 0) acc_merge(a, acc[a], v);
+    for (int m = G; m < 32; m <<= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+    double e = val == -__builtin_huge_val() ? 0.0 : sign * exp(val - mx);
+#pragma unroll
+    for (int m = G; m < 32; m <<= 1) e += __shfl_xor_sync(0xffffffffu, e, m);
+    if (ln < G && a < nlog && mx != -__builtin_huge_val()) lacc_combine(acc[a], LogAcc{mx, e});
+  }
+  if (nacc > kAccTop2) {  // top-2 of the post-update log-weights (exact, order-free)
+    LogAcc v{active ? lw_post : -__builtin_huge_val(), -__builtin_huge_val()};
+#pragma unroll
+    for (int m = G; m < 32; m <<= 1) top2_merge(v, shfl_xor_acc(v, m));
+    if (ln == 0) top2_merge(acc[kAccTop2], v);
   }
 }
 
