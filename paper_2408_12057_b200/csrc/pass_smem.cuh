@@ -353,8 +353,7 @@ struct SmemOps {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (kAligned || 4 * q + e < d) {
-              const float sx = xv[e] * kf.inv_r, sp = xp[e] * kf.inv_r;
-              dl += fmaf(kf.beta, vp[e] - vv[e], 0.5f * (sx - sp) * (sx + sp));  // == dlg_cached
+              dl += Tgt::dlg_vv(kf, xv[e], vv[e], xp[e], vp[e]);  // == dlg_cached
               if (Tgt::kEarly) bp += Tgt::dmax(kf, xv[e], vv[e]);
               vn += vp[e];
             }

@@ -114,13 +114,22 @@ struct TgtMixture {
   struct F32 {
     float beta, inv_r, lw1, mu1, inv_s1, lw2, mu2, inv_s2;
     float lmix;  // log(e^lw1 + e^lw2) >= hi + log1p(e^(lo-hi)) for every x (early rejection)
+    // vterm in base-2 units: u_k = x c_k + d_k = sqrt(log2(e)/2) (x - mu_k)/s_k,
+    // a_k = L_k - u_k^2 = log2(e) (lw_k - ((x - mu_k)/s_k)^2 / 2), kr = log2(e) / (2 r^2)
+    float c1, d1, c2, d2, L1, L2, kr;
+    float hr;  // 1 / (2 r^2)
   };
   __device__ static F32 f32(const TgtParams& T, double beta) {
     // log-normal constants folded: log N(x; mu, s) = -0.5((x-mu)/s)^2 - log s - c
     const double l1 = T.c[1] - T.c[3] + T.c[0], l2 = T.c[2] - T.c[4] + T.c[0];
     const double lm = (l1 > l2 ? l1 : l2) + log1p(exp(-fabs(l1 - l2)));
+    const double log2e = 1.4426950408889634, h = sqrt(0.5 * log2e);
+    const double c1 = h / T.p[3], c2 = h / T.p[5];
     return F32{(float)beta, (float)(1.0 / T.p[0]), (float)l1, (float)T.p[2], (float)(1.0 / T.p[3]),
-               (float)l2, (float)T.p[4], (float)(1.0 / T.p[5]), (float)lm};
+               (float)l2, (float)T.p[4], (float)(1.0 / T.p[5]), (float)lm,
+               (float)c1, (float)(-T.p[2] * c1), (float)c2, (float)(-T.p[4] * c2),
+               (float)(l1 * log2e), (float)(l2 * log2e), (float)(0.5 * log2e / (T.p[0] * T.p[0])),
+               (float)(0.5 / (T.p[0] * T.p[0]))};
   }
   // early rejection: f_beta(y) = beta (hi + log1p) - (1 - beta) sr^2 / 2 <= beta lmix, so
   // max_h dlg(x, h) <= beta (lmix - vterm(x)) + sr(x)^2 / 2  (v = the cached vterm(x))
@@ -134,15 +143,13 @@ struct TgtMixture {
   // log_mix(x) - log eta(x) with the common -log(sqrt(2 pi)) - log(ref_sigma) folded out.
   // log1p(e^{lo-hi}) with lo <= hi: the MUFU ex2/lg2 pair is accurate to ~2e-7
   // absolute on (0, ln 2] (no cancellation: the argument of lg2 is in [1, 2]).
+  // Evaluated in base 2 with the constants folded (F32): 13 ALU + 2 MUFU per coordinate.
   __device__ static float vterm(const F32& k, float x) {
-    const float s1 = (x - k.mu1) * k.inv_s1;
-    const float s2 = (x - k.mu2) * k.inv_s2;
-    const float a = k.lw1 - 0.5f * s1 * s1;
-    const float b = k.lw2 - 0.5f * s2 * s2;
+    const float u1 = fmaf(x, k.c1, k.d1), u2 = fmaf(x, k.c2, k.d2);
+    const float a = fmaf(-u1, u1, k.L1), b = fmaf(-u2, u2, k.L2);
     const float hi = fmaxf(a, b), lo = fminf(a, b);
-    const float sr = x * k.inv_r;
-    const float e = exp2f_approx((lo - hi) * 1.4426950408889634f);
-    return hi + lg2f_approx(1.0f + e) * 0.69314718055994531f + 0.5f * sr * sr;
+    const float l = lg2f_approx(1.0f + exp2f_approx(lo - hi));
+    return (hi + fmaf(k.kr * x, x, l)) * 0.69314718055994531f;
   }
   __device__ static float exp2f_approx(float v) {
     float r;
@@ -182,8 +189,11 @@ struct TgtMixture {
   }
   // difference form with the cached potential term v = vterm(x): one evaluation
   __device__ static float dlg_cached(const F32& k, float x, float v, float p) {
-    const float sx = x * k.inv_r, sp = p * k.inv_r;
-    return fmaf(k.beta, vterm(k, p) - v, 0.5f * (sx - sp) * (sx + sp));
+    return dlg_vv(k, x, v, p, vterm(k, p));
+  }
+  // the same with vterm(p) already evaluated: beta (vp - v) + (x^2 - p^2) / (2 r^2)
+  __device__ static float dlg_vv(const F32& k, float x, float v, float p, float vp) {
+    return fmaf(k.beta, vp - v, ((x - p) * k.hr) * (x + p));
   }
   __device__ static float vpart(const F32& k, float x) { return vterm(k, x); }
   __device__ static double v_from(const TgtParams&, double s) { return s; }
