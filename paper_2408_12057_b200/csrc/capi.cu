@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -266,6 +267,9 @@ KernelCfg make_kcfg(const asmc_kernel_desc* k) {
   c.n_steps = k->n_step_sizes;
   c.sweeps = k->sweeps;
   c.leapfrog = k->leapfrog;
+  // test hook: exact early rejection off, so tests can show it never changes a decision
+  const char* ne = std::getenv("ASMC_NO_EARLY_REJECT");
+  c.no_early = ne && ne[0] == '1';
   for (int i = 0; i < k->n_step_sizes && i < ASMC_MAX_STEP_SIZES; ++i) c.steps[i] = k->step_sizes[i];
   if (c.kind == ASMC_KERNEL_SLICE) c.n_steps = 1;
   if (c.kind != ASMC_KERNEL_RWMH && c.kind != ASMC_KERNEL_HMC && c.kind != ASMC_KERNEL_SLICE) {

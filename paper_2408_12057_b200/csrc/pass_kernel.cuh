@@ -38,6 +38,8 @@ struct KernelCfg {
   int n_steps;
   int sweeps;
   int leapfrog;  // HMC
+  int no_early;  // test hook (env ASMC_NO_EARLY_REJECT=1): run every MH pass to the end
+  int pad;
   double steps[ASMC_MAX_STEP_SIZES];
 };
 

@@ -21,6 +21,7 @@
 namespace asmcdev {
 
 constexpr int kWarps = kBlock / 32;
+constexpr int kNoChecks = 99;  // SmemOps::delta_pass: no early-rejection checks
 
 // dynamic shared memory: [groups][words][nquads] float4 (x, and vterm(x) for targets
 // that cache it), then [kWarps][T+1][nacc] LogAcc
@@ -193,7 +194,7 @@ struct SmemOps {
       // at which the previous proposal of this step size was rejected (4-bit fields of hints,
       // 15 = not rejected).  Only where the exact check runs changes, never its outcome.
       const int hs = 4 * sc;
-      const int mfirst = G == 32 ? max(1, (int)((hints >> hs) & 15u) - 1) : 1;
+      const int mfirst = kc.no_early ? kNoChecks : (G == 32 ? max(1, (int)((hints >> hs) & 15u) - 1) : 1);
       int mrej = 15;
       const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst,
                                                   rejected, mrej, vs_new, drawn)
@@ -380,7 +381,7 @@ struct SmemOps {
       }
       if constexpr (Tgt::kEarly) {
         // warp-uniform: every lane runs mmax iterations (and mfirst is per warp for G == 32)
-        if (m < 7 && m + 1 < mmax && (m == 0 || m >= mfirst)) {
+        if (m < 7 && m + 1 < mmax && (m >= mfirst || (m == 0 && mfirst != kNoChecks))) {
           const float rem = Tgt::kBoundFromV ? Tgt::bound_of_v(kf, vs - bp) : bnd - bp;
           if (certainly_rejected(dl, rem, lu)) {
             rejected = true;
