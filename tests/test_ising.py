@@ -74,15 +74,16 @@ def test_restatement_hmc_estimates_exact_log_z():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("kname", ["identity", "rwmh", "hmc"])
-def test_ising_device_matches_oracle(kname):
-    tg = abi.ising(8, KC, 1.0, 1.0)
+@pytest.mark.parametrize("L,n", [(8, 512), (32, 256), (64, 64)])  # row kernel (8), 4x4 tiles (32, 64)
+def test_ising_device_matches_oracle(kname, L, n):
+    tg = abi.ising(L, KC, 1.0, 1.0)
     k = {"identity": abi.kernel(abi.KERNEL_IDENTITY),
          "rwmh": abi.kernel(abi.KERNEL_RWMH, (0.1, 0.3), 1),
          "hmc": abi.kernel(abi.KERNEL_HMC, (0.25,), 1, leapfrog=6)}[kname]
     o = oracle.load("restate", PH) if kname == "hmc" or not oracle.available("ref", PH) else oracle.load("ref", PH)
     betas = np.linspace(0, 1, 9)
-    a = o.run_sais_single(tg, k, betas, 512, seed=2, round=1)
-    b = capi.run_sais_single(tg, k, betas, 512, seed=2, round=1, exec_=abi.execopts(PH, F32))
+    a = o.run_sais_single(tg, k, betas, n, seed=2, round=1)
+    b = capi.run_sais_single(tg, k, betas, n, seed=2, round=1, exec_=abi.execopts(PH, F32))
     for g in ("log_g0", "log_g1", "log_g2"):
         assert np.max(np.abs(a[g][1:] - b[g][1:]) / np.abs(a[g][1:]).clip(1)) < 1e-6, g
     assert abs(a["log_z_hat"] - b["log_z_hat"]) < 1e-6 * abs(a["log_z_hat"])
