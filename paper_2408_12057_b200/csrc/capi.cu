@@ -543,6 +543,7 @@ int enqueue_smc_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs& 
 struct LgData {
   DBuf<float> raw;  // X (n x d) then y (n), fp32 as given
   DBuf<uint16_t> hi, lo;
+  DBuf<double> w;  // X^T y
   CUtensorMap mhi, mlo;
   uint64_t n = 0, n_pad = 0;
   int d = 0;
@@ -568,6 +569,8 @@ int lg_upload(DevCtx* C, const asmc_target_desc* t, LgData& D) {
   TRY(D.hi.alloc(D.n_pad * D.d, C->stream));
   TRY(D.lo.alloc(D.n_pad * D.d, C->stream));
   LCH(launch_lg_split(D.raw.p, D.n, D.d, D.n_pad, D.hi.p, D.lo.p, C->stream));
+  TRY(D.w.alloc(D.d, C->stream));
+  LCH(launch_lg_xty(D.raw.p, D.raw.p + D.n * (uint64_t)D.d, D.n, D.d, D.w.p, C->stream));
   CU(make_x_maps(D.hi.p, D.lo.p, D.n_pad, D.d, &D.mhi, &D.mlo));
   return 0;
 }
@@ -650,6 +653,7 @@ int enqueue_lg_round(DevCtx* C, const LgData& D, const asmc_target_desc* t, cons
   A.xcur = W.xcur.p;
   A.lw = W.lw.p;
   A.y = D.raw.p + D.n * (uint64_t)d;
+  A.w = D.w.p;
   A.n = D.n;
   A.n_local = n;
   A.d = d;

@@ -17,6 +17,11 @@
 //   precision                      : l = A_hi B_hi + A_hi B_lo + A_lo B_hi (3 MMAs per
 //                                    K step, fp32 accumulate; ~2^-17 relative products),
 //                                    softplus in fp32 (MUFU), V accumulated in fp64.
+//   epilogue                       : V = theta' . w - sum_j softplus(l_j) with w = X^T y
+//                                    (fp64, once per call): the linear term never touches
+//                                    the logits; sum_j log1p(e^-|l_j|) = log2 of a running
+//                                    product of (1 + e^-|l_j|) in [1, 2] over 32 logits
+//                                    (<= 2^32): one SFU ex2 per logit, one lg2 per 32.
 // Warp roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one
 // elected thread), warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM lanes
 // 0..127 = the CTA's particles), everyone builds A and writes accepted rows.
@@ -38,7 +43,8 @@ constexpr uint32_t LG_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(L
 size_t logistic_smem_bytes(int d) {
   const int kch = d / LG_KC;
   return 1024 /*align slack*/ + 2 * (size_t)kch * LG_CHUNK_BYTES + (size_t)LG_STAGES * LG_STAGE_BYTES +
-         1024 /*barriers, tmem slot, per-particle scalars*/ + 2 * LG_M * sizeof(float) + LG_M * sizeof(int);
+         1024 /*barriers, tmem slot, per-particle scalars*/ + 2 * LG_M * sizeof(double) +
+         2 * LG_M * sizeof(float) + LG_M * sizeof(int);
 }
 
 // ---------------------------------------------------------------- PTX --
@@ -106,14 +112,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ float softplus_f(float l) {
-  // max(l, 0) + log1p(exp(-|l|)), MUFU ex2/lg2 (argument of lg2 in [1, 2])
-  float e, g;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-fabsf(l) * 1.4426950408889634f));
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(1.0f + e));
-  return fmaxf(l, 0.0f) + g * 0.69314718055994531f;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -195,7 +193,8 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
   uint64_t* tfull = empty + LG_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* prior_d = reinterpret_cast<float*>(tmem_slot + 4);  // [2][LG_M]
+  double* lin = reinterpret_cast<double*>(tmem_slot + 4);  // [2][LG_M]: halves of theta' . w
+  float* prior_d = reinterpret_cast<float*>(lin + 2 * LG_M);  // [2][LG_M]
   int* accept = reinterpret_cast<int*>(prior_d + 2 * LG_M);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -231,6 +230,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
     k.init(A.seed, A.round, A.p_begin + local, (uint64_t)A.t, 1);
     const uint64_t base = (uint64_t)q * (uint64_t)d;
     float pd = 0.0f;
+    double ld = 0.0;  // this half of theta' . w
     const int i0 = half * (d / 2), i1 = i0 + d / 2;
     for (int i = i0; i < i1; i += 8) {
       float th[8];
@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       }
       float hv[8], lv[8];
 #pragma unroll
+      for (int e = 0; e < 8; ++e) ld = fma((double)th[e], A.w[i + e], ld);
+#pragma unroll
       for (int e = 0; e < 8; ++e) {
         hv[e] = __bfloat162float(__float2bfloat16_rn(th[e]));
         lv[e] = th[e] - hv[e];
@@ -268,6 +270,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       *reinterpret_cast<uint4*>(a_lo + off) = L;
     }
     prior_d[half * LG_M + r] = pd;
+    lin[half * LG_M + r] = ld;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   tc_fence_before();
@@ -324,27 +327,43 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       const int b = tile & 1;
       mbar_wait(&tfull[b], ((uint32_t)tile >> 1) & 1u);
       tc_fence_after();
-      float acc = 0.0f;
       const uint64_t row_base = (uint64_t)tile * LG_N;
+      const int valid_tile = A.n > row_base + LG_N ? LG_N : (int)(A.n - row_base);
+      float smax = 0.0f, slog2 = 0.0f;  // sum max(l, 0), sum log2(1 + e^-|l|)
 #pragma unroll 1
       for (int cc = 0; cc < LG_N / 32; ++cc) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(w * 32) << 16) + (uint32_t)(b * LG_N + cc * 32), v);
-        const uint64_t j0 = row_base + cc * 32;
-        const float yl = j0 + lane < A.n ? A.y[j0 + lane] : 0.0f;
-        const int valid = A.n > j0 + 32 ? 32 : (A.n > j0 ? (int)(A.n - j0) : 0);
+        float prod = 1.0f;
+        if (valid_tile == LG_N) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float yj = __shfl_sync(0xffffffffu, yl, j);
-          const float f = yj * v[j] - softplus_f(v[j]);
-          acc += j < valid ? f : 0.0f;
+          for (int j = 0; j < 32; ++j) {
+            float e;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fabsf(v[j]) * -1.4426950408889634f));
+            prod *= 1.0f + e;
+            smax += fmaxf(v[j], 0.0f);
+          }
+        } else {  // the last, partial tile: padded rows (l = 0) contribute nothing
+          const int valid = valid_tile - cc * 32;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float e;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(fabsf(v[j]) * -1.4426950408889634f));
+            prod *= j < valid ? 1.0f + e : 1.0f;
+            smax += j < valid ? fmaxf(v[j], 0.0f) : 0.0f;
+          }
         }
+        float g;
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(prod));
+        slog2 += g;
       }
+      const float acc = -fmaf(slog2, 0.69314718055994531f, smax);  // - sum softplus
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
       V += (double)acc;
     }
+    V += lin[r] + lin[LG_M + r];
     // ---- MH decision (kernel.cpp:35 in difference form) / V store
     const uint64_t local = p0 + r;
     int acc_flag = 0;
@@ -431,6 +450,26 @@ cudaError_t launch_lg_split(const float* X, uint64_t n, int d, uint64_t n_pad, v
   const uint64_t tot = n_pad * (uint64_t)d;
   lg_split_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(X, n, d, n_pad, (__nv_bfloat16*)hi,
                                                                 (__nv_bfloat16*)lo);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) lg_xty_kernel(const float* X, const float* y, uint64_t n, int d,
+                                                     double* w) {
+  __shared__ double red[256];
+  const int k = blockIdx.x;
+  double s = 0.0;
+  for (uint64_t j = threadIdx.x; j < n; j += 256) s = fma((double)y[j], (double)X[j * (uint64_t)d + k], s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if ((int)threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) w[k] = red[0];
+}
+
+cudaError_t launch_lg_xty(const float* X, const float* y, uint64_t n, int d, double* w, cudaStream_t s) {
+  lg_xty_kernel<<<d, 256, 0, s>>>(X, y, n, d, w);
   return cudaGetLastError();
 }
 

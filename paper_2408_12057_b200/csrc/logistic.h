@@ -15,6 +15,7 @@ struct LgArgs {
   const int* xcur;      // live buffer index
   double* lw;
   const float* y;
+  const double* w;   // X^T y (d): the linear part sum_j y_j l_j = theta . w
   uint64_t n;        // data rows
   uint64_t n_local;  // particles of this launch
   uint64_t p_begin;
@@ -33,6 +34,8 @@ cudaError_t make_x_maps(const void* hi, const void* lo, uint64_t n_pad, int d, C
 cudaError_t launch_lg_split(const float* X, uint64_t n, int d, uint64_t n_pad, void* hi, void* lo,
                             cudaStream_t s);
 cudaError_t launch_lg_init(const LgArgs& A, cudaStream_t s);
+// w = X^T y in fp64, fixed summation order (one CTA per column)
+cudaError_t launch_lg_xty(const float* X, const float* y, uint64_t n, int d, double* w, cudaStream_t s);
 cudaError_t launch_lg_weight(const LgArgs& A, const double* betas, int t, LogAcc* part, uint64_t stride,
                              cudaStream_t s);
 cudaError_t launch_lg_eval(const CUtensorMap& mhi, const CUtensorMap& mlo, const LgArgs& A, int mode,
