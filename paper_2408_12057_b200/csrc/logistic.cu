@@ -34,7 +34,7 @@
 
 namespace asmcdev {
 
-constexpr int LG_M = 128, LG_N = 128, LG_KC = 64, LG_STAGES = 2, LG_THREADS = 256;
+constexpr int LG_M = 128, LG_N = 128, LG_KC = 64, LG_STAGES = 3, LG_THREADS = 256;
 constexpr int LG_CHUNK_BYTES = LG_M * LG_KC * 2;  // 16 KB: one 128-row x 64-col bf16 tile
 constexpr int LG_STAGE_BYTES = 2 * LG_CHUNK_BYTES;  // hi + lo
 constexpr uint32_t LG_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LG_N >> 3) << 17) |
@@ -42,9 +42,11 @@ constexpr uint32_t LG_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(L
 
 size_t logistic_smem_bytes(int d) {
   const int kch = d / LG_KC;
-  return 1024 /*align slack*/ + 2 * (size_t)kch * LG_CHUNK_BYTES + (size_t)LG_STAGES * LG_STAGE_BYTES +
-         1024 /*barriers, tmem slot, per-particle scalars*/ + 2 * LG_M * sizeof(double) +
-         2 * LG_M * sizeof(float) + LG_M * sizeof(int);
+  // the dynamic window is 1024-aligned (__align__ below, no static shared memory), so no
+  // slack: A (hi + lo) + 3 stages = 224 KB at d = 256 leaves room only for the scalars
+  return 2 * (size_t)kch * LG_CHUNK_BYTES + (size_t)LG_STAGES * LG_STAGE_BYTES +
+         (2 * LG_STAGES + 4) * sizeof(uint64_t) + 16 /*tmem slot*/ + LG_M * sizeof(double) +
+         LG_M * sizeof(float) + LG_M * sizeof(int);
 }
 
 // ---------------------------------------------------------------- PTX --
@@ -182,8 +184,8 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
     lg_eval_kernel(const __grid_constant__ CUtensorMap tmap_hi, const __grid_constant__ CUtensorMap tmap_lo,
                    const __grid_constant__ LgArgs A, int mode, const double* betas, float step, int q) {
   const double beta = mode == 1 ? betas[A.t] : 0.0;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw;  // SWIZZLE_128B tiles need 1024-byte alignment (checked below)
   const int kch = A.d / LG_KC;
   unsigned char* a_hi = smem;
   unsigned char* a_lo = a_hi + (size_t)kch * LG_CHUNK_BYTES;
@@ -193,14 +195,22 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
   uint64_t* tfull = empty + LG_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  double* lin = reinterpret_cast<double*>(tmem_slot + 4);  // [2][LG_M]: halves of theta' . w
-  float* prior_d = reinterpret_cast<float*>(lin + 2 * LG_M);  // [2][LG_M]
-  int* accept = reinterpret_cast<int*>(prior_d + 2 * LG_M);
+  // first halves (threads 0..127) of theta' . w and of the prior difference; the second
+  // halves stay in the registers of threads 128..255, which are the epilogue threads
+  double* lin0 = reinterpret_cast<double*>(tmem_slot + 4);  // [LG_M]
+  float* prior0 = reinterpret_cast<float*>(lin0 + LG_M);    // [LG_M]
+  int* accept = reinterpret_cast<int*>(prior0 + LG_M);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t p0 = (uint64_t)blockIdx.x * LG_M;
   const int d = A.d;
   if (A.err && *(volatile int*)A.err) return;
+  if (smem_u32(smem_raw) & 1023u) {  // uniform across the CTA: fail loudly, never mis-swizzle
+    if (tid == 0) raise_error(A.err, ASMC_ERR_CUDA);
+    return;
+  }
+  float pd_own = 0.0f;   // this thread's half of theta'^2 - theta^2
+  double ld_own = 0.0;   // this thread's half of theta' . w
 
   if (tid == 0) {
     for (int s = 0; s < LG_STAGES; ++s) {
@@ -269,8 +279,12 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       *reinterpret_cast<uint4*>(a_hi + off) = H;
       *reinterpret_cast<uint4*>(a_lo + off) = L;
     }
-    prior_d[half * LG_M + r] = pd;
-    lin[half * LG_M + r] = ld;
+    if (half == 0) {
+      prior0[r] = pd;
+      lin0[r] = ld;
+    }
+    pd_own = pd;
+    ld_own = ld;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   tc_fence_before();
@@ -363,7 +377,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       if (lane == 0) mbar_arrive(&tempty[b]);
       V += (double)acc;
     }
-    V += lin[r] + lin[LG_M + r];
+    V += lin0[r] + ld_own;  // thread 128 + r built the second half of particle r
     // ---- MH decision (kernel.cpp:35 in difference form) / V store
     const uint64_t local = p0 + r;
     int acc_flag = 0;
@@ -373,7 +387,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       if (mode == 0) {
         *vrow = V;
       } else {
-        const double dprior = -0.5 * ((double)prior_d[r] + (double)prior_d[LG_M + r]) /
+        const double dprior = -0.5 * ((double)prior0[r] + (double)pd_own) /
                               (A.sigma_p * A.sigma_p);
         const double delta = dprior + beta * (V - *vrow);
         PhiloxKey k;
