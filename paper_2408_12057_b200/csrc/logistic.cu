@@ -37,8 +37,11 @@ namespace asmcdev {
 constexpr int LG_M = 128, LG_N = 128, LG_KC = 64, LG_STAGES = 3, LG_THREADS = 256;
 constexpr int LG_CHUNK_BYTES = LG_M * LG_KC * 2;  // 16 KB: one 128-row x 64-col bf16 tile
 constexpr int LG_STAGE_BYTES = 2 * LG_CHUNK_BYTES;  // hi + lo
-constexpr uint32_t LG_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LG_N >> 3) << 17) |
-                              ((uint32_t)(LG_M >> 4) << 24);  // bf16 x bf16 -> f32, K-major, 128x128
+// 2-SM pair (cta_group::2): M = 256 particles (128 per SM), N = 256 data rows (each SM
+// stages 128 of them), D = 128 x 256 fp32 per SM in TMEM
+constexpr int LG_PN = 2 * LG_N;  // data rows per pair tile
+constexpr uint32_t LG_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LG_PN >> 3) << 17) |
+                              ((uint32_t)((2 * LG_M) >> 4) << 24);  // bf16 x bf16 -> f32, K-major, 256x256
 
 size_t logistic_smem_bytes(int d) {
   const int kch = d / LG_KC;
@@ -72,12 +75,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %0;" ::"r"(bytes), "r"(smem_u32(bar)));
 }
+// 2-SM TMA: the box lands in this CTA's shared memory, the byte count is signalled on the
+// pair leader's barrier (bar_cluster = leader_addr(...))
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
+                                            uint32_t bar_cluster) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
           smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
 }
 // K-major SWIZZLE_128B UMMA smem descriptor: rows 128 B apart, 8-row groups 1024 B apart
@@ -89,12 +94,31 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(LG_IDESC), "r"(accumulate));
 }
+// arrive on the barrier at this offset in BOTH CTAs of the pair when the MMAs retire
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-      smem_u32(bar)));
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"((uint16_t)3));
+}
+// the peer-0 (leader) address of a shared-memory object in the cluster window
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;"); }
@@ -180,7 +204,7 @@ __global__ void __launch_bounds__(kBlock) lg_weight_kernel(LgArgs A, const doubl
 // One likelihood evaluation per particle of the CTA: mode 0 sets V(theta); mode 1
 // evaluates the RWMH proposal theta' = theta + s z (normals q d .. q d + d - 1 of
 // stream (p, t, explore)) and accepts it iff log u_q < dlog eta + beta (V' - V).
-__global__ void __launch_bounds__(LG_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LG_THREADS, 1)
     lg_eval_kernel(const __grid_constant__ CUtensorMap tmap_hi, const __grid_constant__ CUtensorMap tmap_lo,
                    const __grid_constant__ LgArgs A, int mode, const double* betas, float step, int q) {
   const double beta = mode == 1 ? betas[A.t] : 0.0;
@@ -202,7 +226,8 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
   int* accept = reinterpret_cast<int*>(prior0 + LG_M);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint64_t p0 = (uint64_t)blockIdx.x * LG_M;
+  const uint32_t crank = cluster_rank();  // 0 = pair leader (issues the MMAs)
+  const uint64_t p0 = (uint64_t)blockIdx.x * LG_M;  // pair (blockIdx.x / 2) holds 256 particles
   const int d = A.d;
   if (A.err && *(volatile int*)A.err) return;
   if (smem_u32(smem_raw) & 1023u) {  // uniform across the CTA: fail loudly, never mis-swizzle
@@ -219,15 +244,15 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], 8);  // the epilogue warps of both CTAs (leader's copy is used)
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(256));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
 
   // ---- A = theta' of the CTA's particles: thread (r, half) owns d/2 coordinates
@@ -288,10 +313,10 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // both CTAs' A halves, barriers and TMEM are ready before any MMA
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int ntiles = (int)((A.n + LG_N - 1) / LG_N);
+  const int ntiles = (int)((A.n + LG_PN - 1) / LG_PN);
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
@@ -299,21 +324,25 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
         for (int c = 0; c < kch; ++c) {
           const int it = tile * kch + c, s = it % LG_STAGES;
           const uint32_t ph = (uint32_t)(it / LG_STAGES) & 1u;
-          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_wait(&empty[s], ph ^ 1u);  // both CTAs' stage s retired (multicast commit)
           unsigned char* st = stages + (size_t)s * LG_STAGE_BYTES;
-          mbar_expect_tx(&full[s], LG_STAGE_BYTES);
-          tma_load_2d(st, &tmap_hi, c * LG_KC, tile * LG_N, &full[s]);
-          tma_load_2d(st + LG_CHUNK_BYTES, &tmap_lo, c * LG_KC, tile * LG_N, &full[s]);
+          // this CTA stages data rows [tile * 256 + 128 crank, +128); both halves count on
+          // the leader's full[s], which expects the pair's bytes
+          if (crank == 0) mbar_expect_tx(&full[s], 2 * LG_STAGE_BYTES);
+          const int row0 = tile * LG_PN + (int)crank * LG_N;
+          const uint32_t fb = leader_addr(&full[s]);
+          tma_load_2d(st, &tmap_hi, c * LG_KC, row0, fb);
+          tma_load_2d(st + LG_CHUNK_BYTES, &tmap_lo, c * LG_KC, row0, fb);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
+    if (lane == 0 && crank == 0) {  // ---- MMA issuer (pair leader only)
       for (int tile = 0; tile < ntiles; ++tile) {
         const int b = tile & 1;
         mbar_wait(&tempty[b], (((uint32_t)tile >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t dt = tmem + (uint32_t)(b * LG_N);
+        const uint32_t dt = tmem + (uint32_t)(b * LG_PN);
         for (int c = 0; c < kch; ++c) {
           const int it = tile * kch + c, s = it % LG_STAGES;
           mbar_wait(&full[s], (uint32_t)(it / LG_STAGES) & 1u);
@@ -329,27 +358,28 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
             umma_bf16(dt, ah, bl, 1u);
             umma_bf16(dt, al, bh, 1u);
           }
-          umma_commit(&empty[s]);  // frees the smem stage when these MMAs retire
+          umma_commit(&empty[s]);  // frees stage s in both CTAs when these MMAs retire
         }
-        umma_commit(&tfull[b]);  // accumulator ready for the epilogue
+        umma_commit(&tfull[b]);  // both CTAs' accumulator halves ready for their epilogues
       }
     }
   } else if (warp >= 4) {  // ---- epilogue: thread = particle row of D
     const int w = warp - 4, r = w * 32 + lane;
+    const uint32_t tempty_leader[2] = {leader_addr(&tempty[0]), leader_addr(&tempty[1])};
     double V = 0.0;
     for (int tile = 0; tile < ntiles; ++tile) {
       const int b = tile & 1;
       mbar_wait(&tfull[b], ((uint32_t)tile >> 1) & 1u);
       tc_fence_after();
-      const uint64_t row_base = (uint64_t)tile * LG_N;
-      const int valid_tile = A.n > row_base + LG_N ? LG_N : (int)(A.n - row_base);
+      const uint64_t row_base = (uint64_t)tile * LG_PN;  // D column c = data row row_base + c
+      const int valid_tile = A.n > row_base + LG_PN ? LG_PN : (int)(A.n - row_base);
       float smax = 0.0f, slog2 = 0.0f;  // sum max(l, 0), sum log2(1 + e^-|l|)
 #pragma unroll 1
-      for (int cc = 0; cc < LG_N / 32; ++cc) {
+      for (int cc = 0; cc < LG_PN / 32; ++cc) {
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(w * 32) << 16) + (uint32_t)(b * LG_N + cc * 32), v);
+        tmem_ld32(tmem + ((uint32_t)(w * 32) << 16) + (uint32_t)(b * LG_PN + cc * 32), v);
         float prod = 1.0f;
-        if (valid_tile == LG_N) {
+        if (valid_tile == LG_PN) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             float e;
@@ -374,7 +404,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       const float acc = -fmaf(slog2, 0.69314718055994531f, smax);  // - sum softplus
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
+      if (lane == 0) mbar_arrive_remote(tempty_leader[b]);  // the leader waits for all 8 warps
       V += (double)acc;
     }
     V += lin0[r] + ld_own;  // thread 128 + r built the second half of particle r
@@ -425,8 +455,12 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       }
     }
   }
+  // the leader's MMAs read this CTA's shared memory and both CTAs' TMEM is one
+  // allocation: neither CTA leaves before the other is done
+  tc_fence_before();
+  cluster_sync();
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -507,7 +541,8 @@ cudaError_t launch_lg_eval(const CUtensorMap& mhi, const CUtensorMap& mlo, const
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  lg_eval_kernel<<<(unsigned)((A.n_local + LG_M - 1) / LG_M), LG_THREADS, bytes, s>>>(mhi, mlo, A, mode, betas,
+  const unsigned pairs = (unsigned)((A.n_local + 2 * LG_M - 1) / (2 * LG_M));
+  lg_eval_kernel<<<2 * pairs, LG_THREADS, bytes, s>>>(mhi, mlo, A, mode, betas,
                                                                                        step, q);
   return cudaGetLastError();
 }
