@@ -52,6 +52,8 @@ def test_tensor_core_kernel_in_sass():
     name = sorted(set(re.findall(r"_ZN7asmcdev14lg_eval_kernel\w*?fi\b", elf.stdout)))[0]
     out = subprocess.run(["cuobjdump", "-sass", "-fun", name, so], capture_output=True, text=True)
     assert "UTCHMMA" in out.stdout and "UTMALDG" in out.stdout and "LDTM" in out.stdout
+    # the 2-SM pair forms: cta_group::2 MMA, 2-CTA TMA, multicast commit
+    assert "UTCHMMA.2CTA" in out.stdout and "UTMALDG.2D.2CTA" in out.stdout and "UTCBAR.2CTA.MULTICAST" in out.stdout
 
 
 @pytest.mark.gpu
