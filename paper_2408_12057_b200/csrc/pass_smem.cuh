@@ -328,11 +328,12 @@ struct SmemOps {
   }
 
   // sum over this lane's quads of f_beta(x + s z) - f_beta(x), writing x + s z to the
-  // spare row and its vpart sum to vs_new.  Early rejection (exact): after each of the
-  // first 7 quad-iterations the warp checks
+  // spare row and its vpart sum to vs_new.  Early rejection (exact): after quad-iteration
+  // m (m < 7, on the schedule move() passes as mfirst: m = 0 and every m >= mfirst) the
+  // warp checks
   //   partial + sum over unprocessed coordinates of max_h dlg  <  log u
   // (certainly_rejected); then the proposal is rejected whatever the remaining normals
-  // are, so they are not drawn.  Accepted proposals see the identical sum.
+  // are, so they are not drawn (mrej = m).  Accepted proposals see the identical sum.
   template <bool kAligned>
   __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKeyC& k, int lane, int d, int nq,
                                      uint64_t base, float s, const float4* xq, float4* xalt, float log_u,
