@@ -172,6 +172,25 @@ def load_profile_traffic():
     return None
 
 
+def load_profile_issue():
+    """Issue-slot utilisation of the bench's own pass launch from its ncu capture
+    (profiles/r1_bench_pass_ncu_full.json): the pass is ALU/SFU-issue bound, so this
+    is its hardware roofline fraction beside the generator-peak one."""
+    path = os.path.join(ROOT, "profiles", "r1_bench_pass_ncu_full.json")
+    try:
+        d = json.load(open(path))[0]
+    except (OSError, ValueError, IndexError, KeyError):
+        return None
+    def pct(key):
+        v = d.get(key)
+        return None if v is None else round(float(str(v).split()[0]) / 100.0, 4)
+    return {"issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "fma_pipe": pct("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+            "alu_pipe": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+            "xu_pipe": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+            "source": "profiles/r1_bench_pass_ncu_full.json (ncu --set full of bench.py's round-1 pass launch)"}
+
+
 def other_cpu_baselines():
     """The reference's CPU path beside configs 3-5, on bounded samples of each workload
     (same targets, kernels and rounds, smaller N): config 3 and 4 through the unmodified
@@ -422,6 +441,7 @@ def main():
                                   "remaining terms is already below log u; frac here is generator-issue "
                                   "efficiency, 'frac' above is the effective rate in algorithmic units"},
                 "traffic": traffic,
+                "ncu_issue": load_profile_issue(),
                 "hbm": {"achieved_gbs_if_step_outer": hbm_alg, "peak": hbm_peak,
                         "frac": hbm_alg / hbm_peak,
                         "note": "SAIS keeps particles in registers; this is the 8d+16 B/p-step a step-outer design would move"},
