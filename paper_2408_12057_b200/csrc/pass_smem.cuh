@@ -518,6 +518,19 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
   for (int r = 0; r < G; ++r) {
     const uint64_t local = blk * kBlock + (uint64_t)r * NG + g;
     const bool active = local < A.n_local;
+    if (A.mode == kModeSmcStep && tid == 0 && r + 1 < G) {
+      // the next round's NG particle rows are one contiguous span of the state buffer:
+      // one bulk L2 prefetch now, so their loads a particle-iteration later hit L2
+      const uint64_t nl = blk * kBlock + (uint64_t)(r + 1) * NG;
+      if (nl < A.n_local) {
+        const uint64_t cnt = A.n_local - nl < (uint64_t)NG ? A.n_local - nl : (uint64_t)NG;
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(
+            reinterpret_cast<const float*>(A.xbuf[*A.xcur]) + nl * (uint64_t)d);
+        const uintptr_t a1 = a0 + cnt * (uint64_t)d * sizeof(float);
+        const uintptr_t lo = a0 & ~(uintptr_t)15, hi = (a1 + 15) & ~(uintptr_t)15;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
+      }
+    }
     const uint64_t pid = A.mode == kModeTraj ? (active ? A.pids[local] : 0) : A.p_begin + local;
     double lw = 0.0;
     float vs = 0.f;  // this lane's sum of vpart(x) (SmemOps::vsum)
