@@ -448,19 +448,23 @@ __device__ void block_reduce(const double* s_lw, const double* s_lg, const doubl
     if (threadIdx.x < nacc) {
       const int a = threadIdx.x;
       LogAcc acc = (a == kAccTop2) ? LogAcc{-__builtin_huge_val(), -__builtin_huge_val()} : lacc_empty();
+      // lanes 0-4 share one code path (lacc_add(l) == sacc_add(l, 1) bit for bit), so the
+      // five sequential chains run side by side instead of one switch case after another
       for (int g = 0; g < NG; ++g) {
         if (!s_act[g]) continue;
         const double lw = s_lw[g], lg = s_lg[g];
-        switch (a) {
-          case kAccG0: lacc_add(acc, lw); break;
-          case kAccG1: lacc_add(acc, lw + lg); break;
-          case kAccG2: lacc_add(acc, lw + 2.0 * lg); break;
-          case kAccElbo:
-            if (lg != 0.0) sacc_add(acc, lw + log(fabs(lg)), lg > 0.0 ? 1.0 : -1.0);
-            break;
-          case kAccSq: lacc_add(acc, 2.0 * s_post[g]); break;
-          default: top2_add(acc, s_post[g]); break;
+        if (a == kAccTop2) {
+          top2_add(acc, s_post[g]);
+          continue;
         }
+        double l = a == kAccG0 ? lw : (a == kAccG1 ? lw + lg : lw + 2.0 * lg);
+        double sign = 1.0;
+        if (a == kAccSq) l = 2.0 * s_post[g];
+        if (a == kAccElbo) {
+          l = lg != 0.0 ? lw + log(fabs(lg)) : -__builtin_huge_val();
+          sign = lg > 0.0 ? 1.0 : -1.0;
+        }
+        sacc_add(acc, l, sign);
       }
       if (first) dst[a] = acc;
       else acc_merge(a, dst[a], acc);
