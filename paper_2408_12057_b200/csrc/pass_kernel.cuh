@@ -443,28 +443,85 @@ template <bool kExactOrder, int NG>
 __device__ void block_reduce(const double* s_lw, const double* s_lg, const double* s_post,
                              const int* s_act, int nacc, LogAcc* dst, bool first) {
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
-  if (kExactOrder) {
-    // engine_detail.hpp:122-140 / drivers.cpp:95-111: sequential in particle order
+  if constexpr (kExactOrder) {
+    // engine_detail.hpp:122-140 / drivers.cpp:95-111: sequential in particle order.
+    // lacc_add / sacc_add need, per element, only the running max BEFORE it: that is an
+    // exclusive prefix max, so the block scans it in parallel and every thread computes
+    // its element's exp (the same argument, the same exp -> the same bits); one thread
+    // per accumulator then replays the particle-order chain of adds, which is now only
+    // FADD/FMA (no exp on the sequential path).  Called by all NG == blockDim threads.
+    static_assert(NG == kBlock, "exact-order fold: one thread per particle of the block");
+    constexpr int kL = kAccTop2;  // log-sum accumulators g0, g1, g2, elbo, sq
+    __shared__ double s_e[kL][NG];
+    __shared__ unsigned char s_f[kL][NG];  // 0 = skipped, 1 = below the running max, 2 = new max
+    __shared__ double s_wmax[NG / 32][kL];
+    const int g = threadIdx.x;
+    const double lw = s_lw[g], lg = s_lg[g], post = s_post[g];
+    const bool act = s_act[g] != 0;
+    double l[kL], sg[kL];
+#pragma unroll
+    for (int k = 0; k < kL; ++k) sg[k] = 1.0;
+    l[kAccG0] = lw;
+    l[kAccG1] = lw + lg;
+    l[kAccG2] = lw + 2.0 * lg;
+    l[kAccElbo] = lg != 0.0 ? lw + log(fabs(lg)) : -__builtin_huge_val();
+    sg[kAccElbo] = lg > 0.0 ? 1.0 : -1.0;
+    l[kAccSq] = 2.0 * post;
+    const int nl = nacc < kL ? nacc : kL;
+    double inc[kL];
+#pragma unroll
+    for (int k = 0; k < kL; ++k) {
+      if (!act) l[k] = -__builtin_huge_val();
+      inc[k] = l[k];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double o = __shfl_up_sync(0xffffffffu, inc[k], off);
+        if (ln >= off) inc[k] = fmax(inc[k], o);
+      }
+      if (ln == 31) s_wmax[warp][k] = inc[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kL; ++k) {
+      double pre = -__builtin_huge_val();  // max over the earlier warps
+      for (int w = 0; w < warp; ++w) pre = fmax(pre, s_wmax[w][k]);
+      const double up = __shfl_up_sync(0xffffffffu, inc[k], 1);
+      const double ex = ln == 0 ? pre : fmax(pre, up);  // running max before element g
+      if (k >= nl || l[k] == -__builtin_huge_val()) {
+        s_f[k][g] = 0;
+        s_e[k][g] = 0.0;
+      } else {
+        const bool below = l[k] <= ex;
+        s_e[k][g] = exp(below ? l[k] - ex : ex - l[k]);
+        s_f[k][g] = below ? 1 : 2;
+      }
+    }
+    __syncthreads();
     if (threadIdx.x < nacc) {
       const int a = threadIdx.x;
       LogAcc acc = (a == kAccTop2) ? LogAcc{-__builtin_huge_val(), -__builtin_huge_val()} : lacc_empty();
-      // lanes 0-4 share one code path (lacc_add(l) == sacc_add(l, 1) bit for bit), so the
-      // five sequential chains run side by side instead of one switch case after another
-      for (int g = 0; g < NG; ++g) {
-        if (!s_act[g]) continue;
-        const double lw = s_lw[g], lg = s_lg[g];
-        if (a == kAccTop2) {
-          top2_add(acc, s_post[g]);
-          continue;
+      if (a == kAccTop2) {
+        for (int q = 0; q < NG; ++q)
+          if (s_act[q]) top2_add(acc, s_post[q]);
+      } else {
+        const double sign = a == kAccElbo ? 0.0 : 1.0;  // elbo: per-element sign below
+        double sum = 0.0, mx = -__builtin_huge_val();
+        for (int q = 0; q < NG; ++q) {
+          const unsigned char f = s_f[a][q];
+          if (f == 0) continue;
+          const double sq = a == kAccElbo ? (s_lg[q] > 0.0 ? 1.0 : -1.0) : sign;
+          if (f == 1) {
+            sum += sq * s_e[a][q];
+          } else {
+            sum = sum * s_e[a][q] + sq;
+            mx = a == kAccG0 ? s_lw[q]
+                 : a == kAccG1 ? s_lw[q] + s_lg[q]
+                 : a == kAccG2 ? s_lw[q] + 2.0 * s_lg[q]
+                 : a == kAccElbo ? s_lw[q] + log(fabs(s_lg[q]))
+                                 : 2.0 * s_post[q];
+          }
         }
-        double l = a == kAccG0 ? lw : (a == kAccG1 ? lw + lg : lw + 2.0 * lg);
-        double sign = 1.0;
-        if (a == kAccSq) l = 2.0 * s_post[g];
-        if (a == kAccElbo) {
-          l = lg != 0.0 ? lw + log(fabs(lg)) : -__builtin_huge_val();
-          sign = lg > 0.0 ? 1.0 : -1.0;
-        }
-        sacc_add(acc, l, sign);
+        acc = LogAcc{mx, sum};
       }
       if (first) dst[a] = acc;
       else acc_merge(a, dst[a], acc);
