@@ -13,23 +13,85 @@ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < 
 
 // ------------------------------------------------------------------ folds --
 // Exact order (reference): acc = ((e . b0) . b1) . ... over all blocks
-// (engine_detail.hpp:143-154, drivers.cpp:137-145).  One CTA per (row, acc);
-// the CTA stages tiles of partials in shared memory, thread 0 folds them.
-__global__ void fold_exact_kernel(const LogAcc* part, uint64_t stride, uint64_t nblk,
-                                  int row0, int nacc, LogAcc* out) {
+// (engine_detail.hpp:143-154, drivers.cpp:137-145).  One CTA per (row, acc).  As in the
+// pass's exact fold, each combine needs only the running max before it (an exclusive
+// prefix max of the partials' maxima, carried across tiles): the CTA scans it, computes
+// every partial's exp in parallel (same argument -> same bits), and thread 0 replays the
+// chain of adds in block order.  The top-2 row (no exps) is folded directly.
+__global__ void __launch_bounds__(256) fold_exact_kernel(const LogAcc* part, uint64_t stride, uint64_t nblk,
+                                                         int row0, int nacc, LogAcc* out) {
+  constexpr int kTile = 1024, kPer = kTile / 256;
   const int row = row0 + blockIdx.x / nacc, a = blockIdx.x % nacc;
   const LogAcc* src = part + ((size_t)row * kNAcc + a) * stride;
-  __shared__ LogAcc tile[1024];
+  __shared__ LogAcc tile[kTile];
+  __shared__ double e_s[kTile];
+  __shared__ unsigned char f_s[kTile];  // 0 = skipped (empty partial), 1 = below, 2 = new max
+  __shared__ double wmax[8];
+  const int tid = threadIdx.x, ln = tid & 31, w = tid >> 5;
   LogAcc acc = (a == kAccTop2) ? LogAcc{kNegInf, kNegInf} : lacc_empty();
-  for (uint64_t b0 = 0; b0 < nblk; b0 += 1024) {
-    const int m = (int)umin64((uint64_t)(1024), (uint64_t)(nblk - b0));
-    for (int i = threadIdx.x; i < m; i += blockDim.x) tile[i] = src[b0 + i];
+  double carried = kNegInf;  // running max after the previous tiles (all threads)
+  for (uint64_t b0 = 0; b0 < nblk; b0 += kTile) {
+    const int m = (int)umin64((uint64_t)kTile, (uint64_t)(nblk - b0));
+    for (int i = tid; i < m; i += blockDim.x) tile[i] = src[b0 + i];
     __syncthreads();
-    if (threadIdx.x == 0)
-      for (int i = 0; i < m; ++i) acc_merge(a, acc, tile[i]);
+    if (a == kAccTop2) {
+      if (tid == 0)
+        for (int i = 0; i < m; ++i) top2_merge(acc, tile[i]);
+      __syncthreads();
+      continue;
+    }
+    // thread t owns elements kPer t .. kPer t + kPer - 1 (in order)
+    double loc = kNegInf;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int i = kPer * tid + e;
+      if (i < m) loc = fmax(loc, tile[i].max);
+    }
+    double inc = loc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double o = __shfl_up_sync(0xffffffffu, inc, off);
+      if (ln >= off) inc = fmax(inc, o);
+    }
+    if (ln == 31) wmax[w] = inc;
+    __syncthreads();
+    double pre = carried;
+    for (int v = 0; v < w; ++v) pre = fmax(pre, wmax[v]);
+    const double up = __shfl_up_sync(0xffffffffu, inc, 1);
+    double run = ln == 0 ? pre : fmax(pre, up);  // running max before this thread's first element
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int i = kPer * tid + e;
+      if (i >= m) break;
+      const double om = tile[i].max;
+      if (om == kNegInf) {  // lacc_combine returns early
+        f_s[i] = 0;
+        continue;
+      }
+      const bool below = om <= run;
+      e_s[i] = exp(below ? om - run : run - om);
+      f_s[i] = below ? 1 : 2;
+      run = fmax(run, om);
+    }
+    double tot = carried;
+    for (int v = 0; v < 8; ++v) tot = fmax(tot, wmax[v]);
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 0; i < m; ++i) {
+        const unsigned char f = f_s[i];
+        if (f == 0) continue;
+        if (f == 1) {
+          acc.sum += tile[i].sum * e_s[i];
+        } else {
+          acc.sum = acc.sum * e_s[i] + tile[i].sum;
+          acc.max = tile[i].max;
+        }
+      }
+    }
+    carried = tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) out[(size_t)row * kNAcc + a] = acc;
+  if (tid == 0) out[(size_t)row * kNAcc + a] = acc;
 }
 
 // Fixed tree within a fold chunk of kChunkBlocks blocks: thread i folds blocks
