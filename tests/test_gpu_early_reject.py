@@ -79,3 +79,18 @@ def test_trajectories_bit_identical_without_early_rejection(monkeypatch):
     betas = np.linspace(0.0, 1.0, 5)
     a, b, _, _ = _both(monkeypatch, lambda: capi.trajectories(tg, RWMH, betas, 9, 1, pids, ex))
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("steps", [(1e-4, 1e2, 1e4), (3.0, 30.0, 300.0)])
+def test_extreme_step_sizes_bit_identical(monkeypatch, steps):
+    """Per-lane partial sums far outside the fixed-point window (clamped at -4096 below,
+    saturated above 65536) and near zero: decisions still equal the full evaluation's."""
+    tg = abi.scale_gaussian(1.0, 2.0, 1000)
+    k = abi.kernel(abi.KERNEL_RWMH, steps, 2)
+    ex = abi.execopts(PH, F32, lanes=32)
+    betas = np.linspace(0.0, 1.0, 4)
+    a, b, da, db = _both(monkeypatch, lambda: capi.run_sais_single(tg, k, betas, 2048, seed=11, round=1,
+                                                                     exec_=ex))
+    _same(a, b, ["log_g0", "log_g1", "log_g2", "log_z_hat", "elbo_hat"])
+    assert da < db
+
