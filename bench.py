@@ -440,7 +440,11 @@ def main():
                                   "the draws of proposals whose partial MH sum plus an upper bound on the "
                                   "remaining terms is already below log u; frac here is generator-issue "
                                   "efficiency, 'frac' above is the effective rate in algorithmic units"},
-                "traffic": traffic,
+                # dram__bytes_read.sum + dram__bytes_write.sum per pass launch (ncu --set full of
+                # the bench's own launch); the particles never touch HBM in SAIS
+                "traffic": (traffic["dram_read_bytes_per_launch"] + traffic["dram_write_bytes_per_launch"])
+                if traffic else None,
+                "traffic_detail": traffic,
                 "ncu_issue": load_profile_issue(),
                 "hbm": {"achieved_gbs_if_step_outer": hbm_alg, "peak": hbm_peak,
                         "frac": hbm_alg / hbm_peak,
