@@ -117,7 +117,7 @@ struct SmemOps {
   // kernel.cpp:26-63 on this particle; vs (the lane's vpart sum) follows x
   __device__ static void move(const TgtParams& T, const KernelCfg& kc, int lane, int d,
                               double beta, float4*& xq, float4*& xalt, const PhiloxKeyC& k, uint32_t& drawn,
-                              float& vs, uint32_t& hints) {
+                              float& vs) {
     const int nq = (d + 3) >> 2;
     if (kc.kind == ASMC_KERNEL_IDEALIZED) {
       const double mu = Tgt::exact_mu(T, beta);
@@ -176,8 +176,7 @@ struct SmemOps {
     double u_pre = 1.0;  // lane l holds u of proposal (q0 + l)
     int si = 0;  // p % n_steps
     for (int p = 0; p < nprop; ++p) {
-      const int sc = si;
-      const float s = (float)kc.steps[sc];
+      const float s = (float)kc.steps[si];
       si = si + 1 == kc.n_steps ? 0 : si + 1;
       const uint64_t base = (uint64_t)p * (uint64_t)d;
       if ((p % G) == 0) {  // lane l draws the uniform of proposal p + l
@@ -190,17 +189,12 @@ struct SmemOps {
       const float log_u = sfu_lg2((float)u) * 0.693147180559945309f;
       bool rejected = false;
       float vs_new = 0.f;
-      // check schedule (G == 32): after quad-iteration 1, then from one before the iteration
-      // at which the previous proposal of this step size was rejected (4-bit fields of hints,
-      // 15 = not rejected).  Only where the exact check runs changes, never its outcome.
-      const int hs = 4 * sc;
-      const int mfirst = kc.no_early ? kNoChecks : (G == 32 ? max(1, (int)((hints >> hs) & 15u) - 1) : 1);
-      int mrej = 15;
+      // checks after every quad-iteration up to the 7th (the test hook turns them off)
+      const int mfirst = kc.no_early ? kNoChecks : 1;
       const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst,
-                                                  rejected, mrej, vs_new, drawn)
+                                                  rejected, vs_new, drawn)
                                : delta_pass<false>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst,
-                                                   rejected, mrej, vs_new, drawn);
-      hints = (hints & ~(15u << hs)) | ((uint32_t)mrej << hs);
+                                                   rejected, vs_new, drawn);
       if (rejected) continue;  // certainly rejected: the remaining normals are never drawn
       const double delta = group_sum<G>((double)dl);
       if (accept_decision(u, log_u, delta)) {  // kernel.cpp:35: accept iff log u < delta
@@ -329,15 +323,14 @@ struct SmemOps {
 
   // sum over this lane's quads of f_beta(x + s z) - f_beta(x), writing x + s z to the
   // spare row and its vpart sum to vs_new.  Early rejection (exact): after quad-iteration
-  // m (m < 7, on the schedule move() passes as mfirst: m = 0 and every m >= mfirst) the
-  // warp checks
+  // m (m < 7; m = 0 and every m >= mfirst, kNoChecks = none) the warp checks
   //   partial + sum over unprocessed coordinates of max_h dlg  <  log u
   // (certainly_rejected); then the proposal is rejected whatever the remaining normals
-  // are, so they are not drawn (mrej = m).  Accepted proposals see the identical sum.
+  // are, so they are not drawn.  Accepted proposals see the identical sum.
   template <bool kAligned>
   __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKeyC& k, int lane, int d, int nq,
                                      uint64_t base, float s, const float4* xq, float4* xalt, float log_u,
-                                     float bnd, float vs, int mfirst, bool& rejected, int& mrej, float& vs_new,
+                                     float bnd, float vs, int mfirst, bool& rejected, float& vs_new,
                                      uint32_t& drawn) {
     float dl = 0.f, bp = 0.f, vn = 0.f;
     const float lu = log_u;
@@ -381,12 +374,11 @@ struct SmemOps {
         if constexpr (kDual) xalt[q] = make_float4(xp[0], xp[1], xp[2], xp[3]);
       }
       if constexpr (Tgt::kEarly) {
-        // warp-uniform: every lane runs mmax iterations (and mfirst is per warp for G == 32)
+        // warp-uniform: every lane runs mmax iterations
         if (m < 7 && m + 1 < mmax && (m >= mfirst || (m == 0 && mfirst != kNoChecks))) {
           const float rem = Tgt::kBoundFromV ? Tgt::bound_of_v(kf, vs - bp) : bnd - bp;
           if (certainly_rejected(dl, rem, lu)) {
             rejected = true;
-            mrej = m;
             return dl;
           }
         }
@@ -513,7 +505,6 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
                                          : lacc_empty();
   using Ops = SmemOps<Tgt, G, kHmc>;
   uint32_t drawn = 0;  // quads of normals this lane generated (profiling)
-  uint32_t hints = 0;  // early-rejection check schedule per step size (SmemOps::move)
 
   for (int r = 0; r < G; ++r) {
     const uint64_t local = blk * kBlock + (uint64_t)r * NG + g;
@@ -587,7 +578,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
       PhiloxKeyC k;
       k.init(A.rk[1], pid, (uint64_t)t);
       __syncwarp();
-      Ops::move(A.tg, A.kc, lane, d, b1, xq, xalt, k, drawn, vs, hints);
+      Ops::move(A.tg, A.kc, lane, d, b1, xq, xalt, k, drawn, vs);
       __syncwarp();
       const double pre = lw;
       lw += lg;
