@@ -483,7 +483,10 @@ __device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_po
 
 template <class Tgt, int G, bool kHmc = false>
 // RWMH passes: <= 85 registers (3 CTAs/SM; the dual-row footprint allows no more at d = 1000)
-__global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const __grid_constant__ PassArgs A) {
+// G = 4 RWMH on cached-potential targets: 4 rows per particle, so shared memory holds
+// 2 CTAs/SM anyway and the registers may grow to 128 (the row prefetch below)
+__global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ? 2 : 3))
+    pass_smem_kernel(const __grid_constant__ PassArgs A) {
   constexpr int NG = kBlock / G;
   const int tid = threadIdx.x, g = tid / G, lane = tid % G, warp = tid >> 5;
   const int d = (int)A.tg.dim;
@@ -506,6 +509,23 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
   using Ops = SmemOps<Tgt, G, kHmc>;
   uint32_t drawn = 0;  // quads of normals this lane generated (profiling)
 
+  // SMC step, G = 4: the next round's particle row is loaded into registers while this
+  // round's particle is processed, so its HBM latency is hidden behind the MH passes
+  constexpr bool kPre = G == 4 && Tgt::kCacheV && !kHmc;
+  constexpr int kPQ = kPre ? 8 : 1;  // quads per lane held (d <= 128)
+  float4 pre[kPQ];
+  const bool use_pre = kPre && A.mode == kModeSmcStep && (d & 3) == 0 && nq <= G * kPQ;
+  auto load_pre = [&](uint64_t loc) {
+    const bool act = loc < A.n_local;
+    const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A.xbuf[*A.xcur]) +
+                                                        (act ? loc : 0) * (uint64_t)d);
+#pragma unroll
+    for (int i = 0; i < kPQ; ++i) {
+      const int q = lane + G * i;
+      if (q < nq) pre[i] = act ? src[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  if (use_pre) load_pre(blk * kBlock + (uint64_t)g);
   for (int r = 0; r < G; ++r) {
     const uint64_t local = blk * kBlock + (uint64_t)r * NG + g;
     const bool active = local < A.n_local;
@@ -525,7 +545,17 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : 3) pass_smem_kernel(const _
     const uint64_t pid = A.mode == kModeTraj ? (active ? A.pids[local] : 0) : A.p_begin + local;
     double lw = 0.0;
     float vs = 0.f;  // this lane's sum of vpart(x) (SmemOps::vsum)
-    if (A.mode == kModeSmcStep) {
+    if (A.mode == kModeSmcStep && use_pre) {
+#pragma unroll
+      for (int i = 0; i < kPQ; ++i) {
+        const int q = lane + G * i;
+        if (q < nq) xq[q] = pre[i];
+      }
+      if (r + 1 < G) load_pre(blk * kBlock + (uint64_t)(r + 1) * NG + g);
+      lw = active ? A.lw[local] : 0.0;
+      __syncwarp();
+      Ops::refresh_v(A.tg, lane, d, xq);
+    } else if (A.mode == kModeSmcStep) {
       const float4* src = reinterpret_cast<const float4*>(
           reinterpret_cast<const float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d);
       const bool vec = (d & 3) == 0;
