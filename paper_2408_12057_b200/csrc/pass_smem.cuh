@@ -336,7 +336,10 @@ struct SmemOps {
     const float lu = log_u;
     const int mmax = (nq + G - 1) / G;
     int q = lane;
-#pragma unroll 1
+    // unrolled 4x: the quad-iterations' Philox chains interleave (A/B on one box, config 2:
+    // 1x 2.75e8, 2x 2.84e8, 4x 2.87e8, 8x 2.47e8 p-steps/s -- the fully unrolled loop
+    // leaves the instruction cache), same registers (<= 85, 3 CTAs/SM)
+#pragma unroll 4
     for (int m = 0; m < mmax; ++m, q += G) {
       if (q < nq) {
         ++drawn;
