@@ -336,10 +336,11 @@ struct SmemOps {
     const float lu = log_u;
     const int mmax = (nq + G - 1) / G;
     int q = lane;
-    // unrolled 4x: the quad-iterations' Philox chains interleave (A/B on one box, config 2:
-    // 1x 2.75e8, 2x 2.84e8, 4x 2.87e8, 8x 2.47e8 p-steps/s -- the fully unrolled loop
-    // leaves the instruction cache), same registers (<= 85, 3 CTAs/SM)
-#pragma unroll 4
+    // unrolled: the quad-iterations' Philox chains interleave (A/B on one box, config 2
+    // (G = 32): 1x 2.75e8, 2x 2.84e8, 4x 2.87e8, 8x 2.47e8 p-steps/s -- the fully unrolled
+    // loop leaves the instruction cache; config 3 (G = 4, mixture): 2x 8.92e8, 4x 8.78e8,
+    // 8x 8.81e8), same registers
+#pragma unroll (G == 4 ? 2 : 4)
     for (int m = 0; m < mmax; ++m, q += G) {
       if (q < nq) {
         ++drawn;
