@@ -61,28 +61,64 @@ struct SmemOps {
                        Tgt::vpart(kf, x.w));
   }
 
-  // vq[q] = vterm(x) for the cached-potential targets (after a load or a redraw)
-  __device__ static void refresh_v(const TgtParams& T, int lane, int d, float4* xq) {
+  // vq[q] = vterm(x) for the cached-potential targets (after a load or a redraw); returns
+  // this lane's sum of the vterms (== vsum for these targets, same order)
+  __device__ static float refresh_v(const TgtParams& T, int lane, int d, float4* xq) {
+    float s = 0.f;
     if constexpr (kCache) {
       const int nq = (d + 3) >> 2;
       const typename Tgt::F32 kf = Tgt::f32(T, 0.0);
-      for (int q = lane; q < nq; q += G) xq[nq + q] = vquad(kf, xq[q]);
+      for (int q = lane; q < nq; q += G) {
+        const float4 v = vquad(kf, xq[q]);
+        xq[nq + q] = v;
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (4 * q + e < d) s += vv[e];
+      }
     }
+    return s;
   }
 
-  __device__ static void init(const TgtParams& T, int lane, int d, float4* xq, const PhiloxKeyC& k,
-                              uint32_t& drawn) {
+  // x ~ eta for this lane's quads; returns the lane's vpart sum (vsum of the new x, same
+  // order), so no separate pass over the row
+  __device__ static float init(const TgtParams& T, int lane, int d, float4* xq, const PhiloxKeyC& k,
+                               uint32_t& drawn) {
     const int nq = (d + 3) >> 2;
-    for (int q = lane; q < nq; q += G) {
-      ++drawn;
-      float z[4];
-      quad(k, 0, q, z);
-      float v[4];
+    const typename Tgt::F32 kf = Tgt::f32(T, 0.0);
+    float s = 0.f;
+    if ((d & 3) == 0) {  // every quad full: no per-coordinate tail checks
+      for (int q = lane; q < nq; q += G) {
+        ++drawn;
+        float z[4];
+        k.template normals4<float>((uint32_t)q, z);
+        float v[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = (4 * q + e < d) ? Tgt::ref_draw32(T, z[e]) : 0.f;
-      xq[q] = make_float4(v[0], v[1], v[2], v[3]);
+        for (int e = 0; e < 4; ++e) v[e] = Tgt::ref_draw32(T, z[e]);
+        xq[q] = make_float4(v[0], v[1], v[2], v[3]);
+        if constexpr (!kCache) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s += Tgt::vpart(kf, v[e]);
+        }
+      }
+    } else {
+      for (int q = lane; q < nq; q += G) {
+        ++drawn;
+        float z[4];
+        quad(k, 0, q, z);
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (4 * q + e < d) ? Tgt::ref_draw32(T, z[e]) : 0.f;
+        xq[q] = make_float4(v[0], v[1], v[2], v[3]);
+        if constexpr (!kCache) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * q + e < d) s += Tgt::vpart(kf, v[e]);
+        }
+      }
     }
-    refresh_v(T, lane, d, xq);
+    if constexpr (kCache) s = refresh_v(T, lane, d, xq);
+    return s;
   }
 
   // this lane's sum of vpart(x) over its coordinates (quads lane, lane+G, ...; the
@@ -558,7 +594,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
       if (r + 1 < G) load_pre(blk * kBlock + (uint64_t)(r + 1) * NG + g);
       lw = active ? A.lw[local] : 0.0;
       __syncwarp();
-      Ops::refresh_v(A.tg, lane, d, xq);
+      vs = Ops::refresh_v(A.tg, lane, d, xq);  // the prefetch path is cached-target only
     } else if (A.mode == kModeSmcStep) {
       const float4* src = reinterpret_cast<const float4*>(
           reinterpret_cast<const float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d);
@@ -578,14 +614,13 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
       }
       lw = active ? A.lw[local] : 0.0;
       __syncwarp();
-      Ops::refresh_v(A.tg, lane, d, xq);
+      vs = Tgt::kCacheV ? Ops::refresh_v(A.tg, lane, d, xq) : Ops::vsum(A.tg, lane, d, xq);
     } else {
       PhiloxKeyC k;
       k.init(A.rk[0], pid, 0);
-      Ops::init(A.tg, lane, d, xq, k, drawn);
+      vs = Ops::init(A.tg, lane, d, xq, k, drawn);
     }
     __syncwarp();
-    vs = Ops::vsum(A.tg, lane, d, xq);
     if (A.mode == kModeSmcInit) {
       if (active) {
         float* dst = reinterpret_cast<float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d;
