@@ -298,7 +298,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n1", type=int, default=N1_PER_GPU, help="round-1 particles per GPU")
     ap.add_argument("--dim", type=int, default=D)
-    ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds per CPU sample")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds per CPU sample (10-30 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-target measurement")
     ap.add_argument("--ttt-seeds", type=int, default=1000)
