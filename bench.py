@@ -122,15 +122,14 @@ def cpu_reference_run(n1, dim, rounds, workers):
 
 
 def cpu_sample_n1(budget_s, dim, rounds, workers):
-    """Largest power-of-two N_1 whose 4-round run fits ~budget_s of wall time."""
+    """N_1 (a multiple of 256) whose 4-round run takes ~budget_s of wall time, from the
+    rate of a 1024-particle probe run."""
     n1 = 1024
     ka, dt = cpu_reference_run(n1, dim, rounds, workers)
     rate = ka / dt
     per_n1 = psteps(1 << 20, rounds, dim) / float(1 << 20)
     target = budget_s * rate / per_n1
-    while n1 * 2 <= target:
-        n1 *= 2
-    return n1
+    return max(n1, int(target) // 256 * 256)
 
 
 def run_reference_arm(args):
