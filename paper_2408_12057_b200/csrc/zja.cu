@@ -117,36 +117,56 @@ struct GridProbe {
   const ZjaArgs& A;
   double beta, log_m0;
   int parity;
-  LogAcc* s_w;    // [2 * 8] warp partials
-  double* s_out;  // broadcast slot
+  double* s_w;    // [2 accumulators][8 warps] scratch
+  double* s_out;  // unused (kept for the launch layout)
 
-  // CTA-wide fixed tree (xor butterfly in each warp, warps in order); the totals
-  // are broadcast to every thread of the CTA
+  // CTA-wide log-sum-exp of (max, sum) pairs in max-then-sum form: the CTA max by warp
+  // shuffles (fmax, exact), then every thread rescales its sum with ONE exp and the sums
+  // are added by a fixed tree (xor butterfly, warps in order).  Every thread receives the
+  // totals; the same inputs give the same bits in every CTA.
   __device__ void cta_fold2(LogAcc& a, LogAcc& b) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    constexpr int NW = kZjaThreads / 32;
+    double ma = a.max, mb = b.max;
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) {
-      lacc_combine(a, shfl_xor_acc(a, m));
-      lacc_combine(b, shfl_xor_acc(b, m));
+      ma = fmax(ma, __shfl_xor_sync(0xffffffffu, ma, m));
+      mb = fmax(mb, __shfl_xor_sync(0xffffffffu, mb, m));
     }
     if (lane == 0) {
-      s_w[w] = a;
-      s_w[8 + w] = b;
+      s_w[w] = ma;
+      s_w[NW + w] = mb;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      LogAcc x = lacc_empty(), y = lacc_empty();
-      for (int i = 0; i < kZjaThreads / 32; ++i) {
-        lacc_combine(x, s_w[i]);
-        lacc_combine(y, s_w[8 + i]);
-      }
-      s_w[16] = x;
-      s_w[17] = y;
+    ma = s_w[0];
+    mb = s_w[NW];
+#pragma unroll
+    for (int i = 1; i < NW; ++i) {
+      ma = fmax(ma, s_w[i]);
+      mb = fmax(mb, s_w[NW + i]);
     }
     __syncthreads();
-    a = s_w[16];
-    b = s_w[17];
+    double sa = (a.max == -__builtin_huge_val()) ? 0.0 : a.sum * exp(a.max - ma);
+    double sb = (b.max == -__builtin_huge_val()) ? 0.0 : b.sum * exp(b.max - mb);
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, m);
+      sb += __shfl_xor_sync(0xffffffffu, sb, m);
+    }
+    if (lane == 0) {
+      s_w[w] = sa;
+      s_w[NW + w] = sb;
+    }
     __syncthreads();
+    double ta = 0.0, tb = 0.0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      ta += s_w[i];
+      tb += s_w[NW + i];
+    }
+    __syncthreads();
+    a = LogAcc{ma, ta};
+    b = LogAcc{mb, tb};
   }
 
   // fold (a, b) over the grid in a fixed order; every thread receives the totals
@@ -170,23 +190,34 @@ struct GridProbe {
     tb = y;
   }
 
+  // per thread: the max of its particles' terms first, then one exp per particle with
+  // no dependence between them (the running-max form chains the exps)
   __device__ double dhat(double b2) {
-    LogAcc m1 = lacc_empty(), m2 = lacc_empty();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < A.n; p += stride) {
+    const uint64_t p0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double m1 = -__builtin_huge_val(), m2 = -__builtin_huge_val();
+    for (uint64_t p = p0; p < A.n; p += stride) {
       const double lg = (b2 - beta) * A.V[p];  // difference form of zja_lg
-      lacc_add(m1, A.lw[p] + lg);
-      lacc_add(m2, A.lw[p] + 2.0 * lg);
+      m1 = fmax(m1, A.lw[p] + lg);
+      m2 = fmax(m2, A.lw[p] + 2.0 * lg);
+    }
+    double s1 = 0.0, s2 = 0.0;
+    if (m1 != -__builtin_huge_val()) {
+      for (uint64_t p = p0; p < A.n; p += stride) {
+        const double lg = (b2 - beta) * A.V[p];
+        s1 += exp(A.lw[p] + lg - m1);
+        s2 += exp(A.lw[p] + 2.0 * lg - m2);
+      }
     }
     LogAcc t1, t2;
-    fold2(m1, m2, t1, t2);
+    fold2(LogAcc{m1, s1}, LogAcc{m2, s2}, t1, t2);
     const double raw = lacc_log_total(t2) - 2.0 * lacc_log_total(t1) + log_m0;
     return raw > 0.0 ? raw : 0.0;
   }
 };
 
 __global__ void __launch_bounds__(kZjaThreads) zja_coop_kernel(ZjaArgs A) {
-  __shared__ LogAcc s_w[18];
+  __shared__ double s_w[2 * (kZjaThreads / 32)];
   __shared__ double s_out[2];
   const int err0 = *(volatile int*)A.err;  // uniform across the grid (read before any write)
   if (err0) return;
