@@ -109,9 +109,25 @@ class ClockSampler:
 
 
 # -------------------------------------------------------- reference (CPU) --
+def host_cpu():
+    """nproc and the lscpu model of the box's host."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
 def cpu_reference_run(n1, dim, rounds, workers):
+    """The unmodified reference run_sais (oracle/_ref/libasmc_ref_release.so: the
+    reference's sources at its own Release flags, -O3 -DNDEBUG) on the host cores."""
     import oracle
-    ref = oracle.load("ref", abi.RNG_XOSHIRO)
+    ref = oracle.load("ref_release")
     tg = abi.scale_gaussian(SIGMA0, SIGMA1, dim)
     k = abi.kernel(abi.KERNEL_RWMH, STEPS, 1)
     t0 = time.perf_counter()
@@ -121,15 +137,21 @@ def cpu_reference_run(n1, dim, rounds, workers):
     return ka, dt
 
 
-def cpu_sample_n1(budget_s, dim, rounds, workers):
-    """N_1 (a multiple of 256) whose 4-round run takes ~budget_s of wall time, from the
-    rate of a 1024-particle probe run."""
-    n1 = 1024
+def cpu_sample(budget_s, dim, rounds, workers, window=None, tries=4):
+    """Size N_1 (a multiple of 256) so one 4-round run takes budget_s of wall time: start
+    from a 4096-particle run and rescale from each real sample (p-steps are linear in N_1)
+    until the sample lands inside `window`.  Returns (n1, kernel_applications, seconds,
+    inside_window)."""
+    if window is None:  # 10-30 s of CPU work at the default budget
+        window = (min(10.0, 0.8 * budget_s), max(30.0, 1.5 * budget_s))
+    n1 = 4096
     ka, dt = cpu_reference_run(n1, dim, rounds, workers)
-    rate = ka / dt
-    per_n1 = psteps(1 << 20, rounds, dim) / float(1 << 20)
-    target = budget_s * rate / per_n1
-    return max(n1, int(target) // 256 * 256)
+    for _ in range(tries):
+        if window[0] <= dt <= window[1]:
+            break
+        n1 = max(256, int(n1 * budget_s / max(dt, 1e-3)) // 256 * 256)
+        ka, dt = cpu_reference_run(n1, dim, rounds, workers)
+    return n1, ka, dt, window[0] <= dt <= window[1]
 
 
 def run_reference_arm(args):
@@ -137,27 +159,43 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     workers = os.cpu_count() or 1
-    n1 = cpu_sample_n1(args.cpu_budget, args.dim, ROUNDS, workers)
+    n1, _, _, _ = cpu_sample(args.cpu_budget, args.dim, ROUNDS, workers)
     for _ in range(args.warmup):
         cpu_reference_run(n1 // 4 or 1, args.dim, ROUNDS, workers)
-    tot_ka, tot_dt = 0, 0.0
+    tot_ka, tot_dt, dts = 0, 0.0, []
     for _ in range(args.steps):
         ka, dt = cpu_reference_run(n1, args.dim, ROUNDS, workers)
         tot_ka += ka
         tot_dt += dt
+        dts.append(round(dt, 2))
     value = tot_ka / tot_dt
-    sample = f"run_sais with N_1={n1} (same d={args.dim}, {ROUNDS} rounds, RWMH {list(STEPS)}), workers={workers}"
+    sample = (f"unmodified reference run_sais (Release -O3) with N_1={n1} (same d={args.dim}, {ROUNDS} rounds, "
+              f"RWMH {list(STEPS)}), workers={workers}; per-step seconds {dts}")
     line = {"metric": METRIC, "value": value, "unit": "particle-steps/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(workload(n1, args.dim), note="reference CPU path, bounded sample of the workload"),
             "cpu_baseline": {"value": value, "unit": "particle-steps/s", "cores": workers,
-                             "kind": "reference", "sample": sample},
+                             "kind": "reference", "sample": sample, "host": host_cpu(),
+                             "build": "oracle/_ref/libasmc_ref_release.so (-O3 -DNDEBUG -std=gnu++20)"},
             "e2e": {"value": value, "unit": "particle-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    mapped = repo_objects_mapped()
+    if mapped:  # the reference arm must run none of this repo's native code
+        raise RuntimeError(f"reference arm mapped the repo's own libraries: {mapped}")
     print(json.dumps(line), flush=True)
     return 0
+
+
+def repo_objects_mapped():
+    """Shared objects of this package mapped into the process (Linux /proc/self/maps)."""
+    pkg = os.path.join(ROOT, "paper_2408_12057_b200")
+    try:
+        maps = open("/proc/self/maps").read().splitlines()
+    except OSError:
+        return []
+    return sorted({ln.split()[-1] for ln in maps if ln.split() and ln.split()[-1].startswith(pkg)})
 
 
 # ------------------------------------------------------------- our path --
@@ -199,7 +237,7 @@ def other_cpu_baselines():
     from paper_2408_12057_b200 import exact
     workers = os.cpu_count() or 1
     out = {}
-    ref = oracle.load("ref", abi.RNG_XOSHIRO) if oracle.available("ref", abi.RNG_XOSHIRO) else None
+    ref = oracle.load("ref_release") if oracle.available("ref_release") else None
     if ref is not None:
         tg = abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100)
         t0 = time.perf_counter()
@@ -405,11 +443,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             workers = os.cpu_count() or 1
-            nc = cpu_sample_n1(args.cpu_budget, args.dim, ROUNDS, workers)
-            ka, dt = cpu_reference_run(nc, args.dim, ROUNDS, workers)
+            nc, ka, dt, inside = cpu_sample(args.cpu_budget, args.dim, ROUNDS, workers)
             cpu = {"value": ka / dt, "unit": "particle-steps/s", "cores": workers,
-                   "kind": "reference",
-                   "sample": f"unmodified reference run_sais (oracle/_ref) N_1={nc}, d={args.dim}, "
+                   "kind": "reference", "host": host_cpu(), "sample_seconds": dt,
+                   "sample_in_window": inside,
+                   "build": "oracle/_ref/libasmc_ref_release.so (-O3 -DNDEBUG -std=gnu++20)",
+                   "sample": f"unmodified reference run_sais (Release -O3) N_1={nc}, d={args.dim}, "
                              f"{ROUNDS} rounds, workers={workers}, {dt:.1f}s"}
         except Exception as exc:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "particle-steps/s", "cores": None, "kind": "reference",

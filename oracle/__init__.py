@@ -7,6 +7,8 @@ Loads the CPU checkers built by oracle/Makefile into oracle/_ref/:
                       (oracle/ref_harness.cpp), keyed-xoshiro streams.
 * ``ref_philox``   -- libasmc_ref_philox.so: the same reference sources compiled
                       against the Philox shadow header oracle/shadow/asmc/rng.hpp.
+* ``ref_release``  -- libasmc_ref_release.so: the unmodified reference at its own
+                      Release flags (-O3 -DNDEBUG), the CPU baseline bench.py times.
 * ``restate``      -- liborarestate.so: oracle/restate.c, the plain-C
                       restatement of the path (both stream families), pinned
                       bit-for-bit against the two above by tests/test_oracle.py.
@@ -259,12 +261,15 @@ _cache = {}
 
 def load(which="restate", rng=abi.RNG_XOSHIRO):
     """which: 'ref' (unmodified reference; rng picks xoshiro or the Philox shadow
-    build) or 'restate' (oracle/restate.c, rng selects the stream family)."""
+    build), 'ref_release' (the same sources at the reference's Release -O3, for timing)
+    or 'restate' (oracle/restate.c, rng selects the stream family)."""
     key = (which, rng)
     if key not in _cache:
         if which == "ref":
             name = "libasmc_ref.so" if rng == abi.RNG_XOSHIRO else "libasmc_ref_philox.so"
             _cache[key] = Oracle(os.path.join(REF_DIR, name))
+        elif which == "ref_release":  # the timed CPU baseline: reference Release flags (-O3)
+            _cache[key] = Oracle(os.path.join(REF_DIR, "libasmc_ref_release.so"))
         elif which == "restate":
             _cache[key] = Oracle(os.path.join(REF_DIR, "liborarestate.so"), rng=rng)
         else:
@@ -273,6 +278,6 @@ def load(which="restate", rng=abi.RNG_XOSHIRO):
 
 
 def available(which="ref", rng=abi.RNG_XOSHIRO):
-    name = {("ref", 0): "libasmc_ref.so", ("ref", 1): "libasmc_ref_philox.so"}.get(
-        (which, rng), "liborarestate.so")
+    name = {("ref", 0): "libasmc_ref.so", ("ref", 1): "libasmc_ref_philox.so",
+            ("ref_release", 0): "libasmc_ref_release.so"}.get((which, rng), "liborarestate.so")
     return os.path.exists(os.path.join(REF_DIR, name))
