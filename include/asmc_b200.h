@@ -234,12 +234,13 @@ int asmc_fold_partials(const asmc_logacc* partials, uint64_t chunks, int32_t ste
  *                             chunk-major: partials[c * ASMC_SHARD_NACC + a]
  *   2. caller all-gathers the partials of all shards in rank order
  *   3. asmc_smc_shard_decide  fold + ESS + policy (engine.cpp:82-95,140-160);
- *                             if *resample, writes this shard's block CDF totals
- *                             (asmc_smc_shard_blocks entries) to block_totals
- *   4. (resample) caller all-gathers the block totals in rank order
- *   5. asmc_smc_shard_plan    global CDF offsets (scanned IN PLACE in the gathered
- *                             totals buffer, which this rank must own); slot_begin[r] (host, world+1)
- *                             = first output slot whose ancestor lies in shard r
+ *                             if *resample, copies this shard's log-weights
+ *                             (asmc_smc_shard_exchange_len entries) to lw_out
+ *   4. (resample) caller all-gathers the log-weights in rank order (8 B/particle)
+ *   5. asmc_smc_shard_plan    every rank builds the reference's sequential CDF over
+ *                             all n log-weights (engine.cpp:61-80, bit for bit) and the
+ *                             global ancestors; slot_begin[r] (host, world+1) = first
+ *                             output slot whose ancestor lies in shard r
  *   6. asmc_smc_shard_pack    rows of the ancestors of slots [slot_begin[me],
  *                             slot_begin[me+1]) in slot order (row_bytes each)
  *   7. caller all-to-all: shard r's packed rows for slots in shard q go to q
@@ -255,12 +256,12 @@ int asmc_smc_shard_create(const asmc_target_desc* target, const asmc_kernel_desc
                           asmc_smc_shard** out);
 void asmc_smc_shard_destroy(asmc_smc_shard* shard);
 uint64_t asmc_smc_shard_chunks(const asmc_smc_shard* shard);
-uint64_t asmc_smc_shard_blocks(const asmc_smc_shard* shard);
+uint64_t asmc_smc_shard_exchange_len(const asmc_smc_shard* shard);
 uint64_t asmc_smc_shard_row_bytes(const asmc_smc_shard* shard);
 int asmc_smc_shard_step(asmc_smc_shard* shard, int32_t t, asmc_logacc* partials_dev);
 int asmc_smc_shard_decide(asmc_smc_shard* shard, int32_t t, const asmc_logacc* all_partials_dev,
-                          uint64_t all_chunks, double* block_totals_dev, int32_t* resample);
-int asmc_smc_shard_plan(asmc_smc_shard* shard, double* all_block_totals_dev, uint64_t all_blocks,
+                          uint64_t all_chunks, double* lw_out_dev, int32_t* resample);
+int asmc_smc_shard_plan(asmc_smc_shard* shard, const double* all_log_weights_dev, uint64_t n_all,
                         int32_t world, const uint64_t* shard_p_begin, uint64_t* slot_begin);
 int asmc_smc_shard_pack(asmc_smc_shard* shard, void* rows_dev);
 int asmc_smc_shard_accept(asmc_smc_shard* shard, const void* rows_dev);
@@ -362,11 +363,20 @@ int asmc_trajectories(const asmc_target_desc* target, const asmc_kernel_desc* ke
                       const uint64_t* particles, uint64_t count, const asmc_exec* exec,
                       double* x_out, double* log_w_out);
 
-/* Systematic resampling on the device (engine.cpp:61-80) with the blocked,
- * deterministic CDF described in DESIGN.md; u is the uniform the reference
+/* Systematic resampling on the device (engine.cpp:61-80): the reference's SEQUENTIAL
+ * fp64 CDF reproduced bit for bit by a parallel exact scan:
+ * l1 = logsumexp (logsum.hpp:97-101), cum_j = fl(cum_{j-1} + exp(lw_j - l1)),
+ * a_m = first j with !(cum_j < (m + u)/n), clamped.  u is the uniform the reference
  * draws from key (seed, round, 0, t, resample). */
 int asmc_systematic_resample(const double* log_weights, uint64_t n, double u, int32_t device,
                              uint32_t* ancestors);
+/* parity hooks: the CDF the search runs on (n doubles) and l1; logsumexp alone
+ * (asmc::logsumexp, logsum.hpp:97-101; -inf for an empty or all -inf input) */
+int asmc_resample_cdf(const double* log_weights, uint64_t n, int32_t device, double* cum_out,
+                      double* l1_out);
+int asmc_logsumexp(const double* log_weights, uint64_t n, int32_t device, double* out);
+/* parity hook: which = 0 -> the device's glibc-exact exp, 1 -> its correctly rounded log */
+int asmc_exact_math(int32_t which, const double* x, uint64_t n, int32_t device, double* out);
 int asmc_ess(const double* log_weights, uint64_t n, int32_t device, double* out);
 
 /* ---- schedule adaptation (device kernels, bit-exact with the host oracle) ---- */

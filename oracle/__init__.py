@@ -53,9 +53,6 @@ class Oracle:
         self.rng = rng
         L = self.lib
         L.ora_last_error.restype = C.c_char_p
-        if hasattr(L, "ora_exp_det"):
-            L.ora_exp_det.restype = C.c_double
-            L.ora_exp_det.argtypes = [C.c_double]
 
     # -- plumbing -------------------------------------------------------
     def _call(self, name, *args):
@@ -96,16 +93,6 @@ class Oracle:
         self._call("ora_run_smc", C.byref(target), C.byref(kernel), _arr(betas, C.c_double),
                    C.c_int32(T), C.c_uint64(n), C.c_int32(policy), C.c_double(rho),
                    C.c_uint64(seed), C.c_uint64(round), C.c_int32(workers), C.byref(rep))
-        return self._finish(rep, bufs)
-
-    def run_smc_blocked(self, target, kernel, betas, n, policy=abi.POLICY_ADAPTIVE_ESS, rho=0.5,
-                        seed=0, round=0):
-        betas = np.ascontiguousarray(betas, dtype=np.float64)
-        T = len(betas) - 1
-        rep, bufs = self._report(T)
-        self._call("ora_run_smc_blocked", C.byref(target), C.byref(kernel),
-                   _arr(betas, C.c_double), C.c_int32(T), C.c_uint64(n), C.c_int32(policy),
-                   C.c_double(rho), C.c_uint64(seed), C.c_uint64(round), C.byref(rep))
         return self._finish(rep, bufs)
 
     def run_pt(self, target, kernel, betas, iterations=1024, burn_in=-1, seed=0, round=1, replicas=1):
@@ -204,15 +191,36 @@ class Oracle:
                    self._key(key), _arr(out, C.c_uint32))
         return out
 
-    def systematic_resample_blocked(self, log_w, u):
+    def systematic_resample_u(self, log_w, u):
+        """engine.cpp:61-80 with the uniform given (restatement only)."""
         lw = np.ascontiguousarray(log_w, dtype=np.float64)
         out = np.zeros(len(lw), np.uint32)
-        self._call("ora_systematic_resample_blocked", _arr(lw, C.c_double), C.c_uint64(len(lw)),
+        self._call("ora_systematic_resample_u", _arr(lw, C.c_double), C.c_uint64(len(lw)),
                    C.c_double(u), _arr(out, C.c_uint32))
         return out
 
-    def exp_det(self, x):
-        return self.lib.ora_exp_det(C.c_double(x))
+    def resample_cdf(self, log_w):
+        """(cum, l1): the sequential CDF engine.cpp:64-75 walks (restatement only)."""
+        lw = np.ascontiguousarray(log_w, dtype=np.float64)
+        cum = np.zeros(len(lw))
+        l1 = C.c_double()
+        self._call("ora_resample_cdf", _arr(lw, C.c_double), C.c_uint64(len(lw)), _arr(cum, C.c_double),
+                   C.byref(l1))
+        return cum, l1.value
+
+    def cdf_given_l1(self, log_w, l1):
+        lw = np.ascontiguousarray(log_w, dtype=np.float64)
+        cum = np.zeros(len(lw))
+        self._call("ora_cdf_given_l1", _arr(lw, C.c_double), C.c_uint64(len(lw)), C.c_double(l1),
+                   _arr(cum, C.c_double))
+        return cum
+
+    def libm(self, which, x):
+        """The host libm's exp (which=0) / log (which=1), element-wise."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.zeros(len(x))
+        self._call("ora_libm", C.c_int(which), _arr(x, C.c_double), C.c_uint64(len(x)), _arr(out, C.c_double))
+        return out
 
     def ess(self, log_w):
         lw = np.ascontiguousarray(log_w, dtype=np.float64)

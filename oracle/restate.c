@@ -11,9 +11,9 @@
  * restates (paths relative to /root/reference/proj/).  Two stream families:
  *   rng 0 = keyed xoshiro256++     include/asmc/rng.hpp:27-86
  *   rng 1 = keyed Philox4x32-10    oracle/shadow/asmc/rng.hpp (shadow header)
- * plus the device's deterministic blocked-CDF systematic resampling
- * (ora_systematic_resample_blocked), which the B200 kernel reproduces bit for
- * bit and which differs from engine.cpp:61-80 only in CDF summation order.
+ * Systematic resampling is the reference's own sequential-CDF rule
+ * (engine.cpp:61-80); the device reproduces its CDF bit for bit (csrc/refcdf.cu),
+ * and ora_resample_cdf exposes the CDF so the tests compare it value by value.
  */
 #include <float.h>
 #include <math.h>
@@ -596,71 +596,46 @@ static int systematic_resample_seq(const double* lw, uint64_t n, double u, uint3
   return 0;
 }
 
-/* ---- deterministic exp shared with the device (csrc/detexp.cuh) ---------
- * exp(x) for x <= 0 from +,-,* only (Cody-Waite reduction + degree-13 Taylor),
- * so that host and device produce identical bits without relying on libm. */
-static double exp_det(double x) {
-  if (x == -INFINITY || x < -745.2) return 0.0;
-  const double kLn2Hi = 6.93147180369123816490e-01;
-  const double kLn2Lo = 1.90821492927058770002e-10;
-  const double kInvLn2 = 1.44269504088896338700e+00;
-  double kf = x * kInvLn2;
-  kf = kf < 0.0 ? (double)(int64_t)(kf - 0.5) : (double)(int64_t)(kf + 0.5);
-  const double r = (x - kf * kLn2Hi) - kf * kLn2Lo;
-  double p = 1.0 / 6227020800.0;
-  p = p * r + 1.0 / 479001600.0;
-  p = p * r + 1.0 / 39916800.0;
-  p = p * r + 1.0 / 3628800.0;
-  p = p * r + 1.0 / 362880.0;
-  p = p * r + 1.0 / 40320.0;
-  p = p * r + 1.0 / 5040.0;
-  p = p * r + 1.0 / 720.0;
-  p = p * r + 1.0 / 120.0;
-  p = p * r + 1.0 / 24.0;
-  p = p * r + 1.0 / 6.0;
-  p = p * r + 0.5;
-  p = p * r + 1.0;
-  p = p * r + 1.0;
-  int k = (int)kf;
-  /* scale by 2^k in two steps to stay normal until the final multiply */
-  if (k < -1000) { p *= 0x1.0p-1000; k += 1000; }
-  union { double d; uint64_t u; } s;
-  s.u = (uint64_t)(k + 1023) << 52;
-  return p * s.d;
-}
-double ora_exp_det(double x) { return exp_det(x); }
-
-/* Device systematic resampling (csrc/resample.cu): max-shifted weights
- * w_j = exp_det(lw_j - max), per-256-block sequential inclusive sums, a
- * sequential exclusive scan of block totals, cum_j = offset_b + blocksum_j;
- * pos_m = ((m + u) / n) * total; a_m = first j with !(cum_j < pos_m), clamped
- * to n-1 -- the search rule of engine.cpp:72-76. */
-int ora_systematic_resample_blocked(const double* lw, uint64_t n, double u, uint32_t* anc) {
+/* engine.cpp:61-80 with a given uniform (the reference draws u from key
+ * (seed, round, 0, t, resample) inside systematic_resample) */
+int ora_systematic_resample_u(const double* lw, uint64_t n, double u, uint32_t* anc) {
   if (n == 0) FAIL(ASMC_ERR_INVALID_ARGUMENT, "cannot resample an empty system");
-  double mx = -INFINITY;
-  for (uint64_t i = 0; i < n; ++i) mx = lw[i] > mx ? lw[i] : mx;
-  if (mx == -INFINITY) FAIL(ASMC_ERR_DEGENERATE, "all log-weights are -inf");
-  double* cum = malloc(n * sizeof(double));
-  const uint64_t nb = block_count(n);
-  double offset = 0.0;
-  for (uint64_t b = 0; b < nb; ++b) {
-    double s = 0.0;
-    const uint64_t lo = b * KBLOCK, hi = lo + KBLOCK < n ? lo + KBLOCK : n;
-    for (uint64_t j = lo; j < hi; ++j) {
-      s += exp_det(lw[j] - mx);
-      cum[j] = s;
-    }
-    for (uint64_t j = lo; j < hi; ++j) cum[j] += offset;
-    offset += s;
+  return systematic_resample_seq(lw, n, u, anc);
+}
+
+/* The CDF systematic_resample walks (engine.cpp:64-75), every value: l1 =
+ * logsumexp(lw) (logsum.hpp:97-101), cum_0 = exp(lw_0 - l1), cum_j = cum_{j-1} +
+ * exp(lw_j - l1) in particle order. */
+int ora_resample_cdf(const double* lw, uint64_t n, double* cum, double* l1_out) {
+  if (n == 0) FAIL(ASMC_ERR_INVALID_ARGUMENT, "cannot resample an empty system");
+  lacc_t a = LACC0;
+  for (uint64_t i = 0; i < n; ++i) lacc_add(&a, lw[i]);
+  const double l1 = lacc_total(&a);
+  if (l1_out) *l1_out = l1;
+  if (l1 == -INFINITY) FAIL(ASMC_ERR_DEGENERATE, "all log-weights are -inf");
+  double c = exp(lw[0] - l1);
+  cum[0] = c;
+  for (uint64_t j = 1; j < n; ++j) {
+    c += exp(lw[j] - l1);
+    cum[j] = c;
   }
-  const double total = cum[n - 1];
-  uint64_t j = 0;
-  for (uint64_t m = 0; m < n; ++m) {
-    const double pos = (((double)m + u) / (double)n) * total;
-    while (cum[j] < pos && j + 1 < n) ++j;
-    anc[m] = (uint32_t)j;
+  return 0;
+}
+
+/* the CDF for a given l1 (isolates the chain of adds from the one log) */
+int ora_cdf_given_l1(const double* lw, uint64_t n, double l1, double* cum) {
+  double c = exp(lw[0] - l1);
+  cum[0] = c;
+  for (uint64_t j = 1; j < n; ++j) {
+    c += exp(lw[j] - l1);
+    cum[j] = c;
   }
-  free(cum);
+  return 0;
+}
+
+/* the host libm the reference links (glibc): which 0 = exp, 1 = log */
+int ora_libm(int which, const double* x, uint64_t n, double* out) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = which == 0 ? exp(x[i]) : log(x[i]);
   return 0;
 }
 
@@ -693,7 +668,7 @@ static int check_degenerate(uint64_t n, double ess_t, double m1, double m2, int 
 
 static int run_smc_impl(const asmc_target_desc* tg, const asmc_kernel_desc* k, const double* betas,
                         int T, uint64_t n, int policy, double rho, uint64_t seed, uint64_t round,
-                        int resample_blocked, asmc_report* out) {
+                        asmc_report* out) {
   TRY(validate_schedule(betas, T));
   if (n < 1) FAIL(ASMC_ERR_INVALID_ARGUMENT, "n_particles must be at least 1");
   if (!(rho >= 0.0 && rho <= 1.0)) FAIL(ASMC_ERR_INVALID_ARGUMENT, "rho must lie in [0, 1]");
@@ -774,8 +749,7 @@ static int run_smc_impl(const asmc_target_desc* tg, const asmc_kernel_desc* k, c
         stream_t rs;
         stream_init(&rs, seed, round, 0, (uint64_t)t, 2);
         const double u = uniform(&rs);
-        rc = resample_blocked ? ora_systematic_resample_blocked(lw, n, u, anc)
-                              : systematic_resample_seq(lw, n, u, anc);
+        rc = systematic_resample_seq(lw, n, u, anc);
         if (rc) break;
         for (uint64_t p = 0; p < n; ++p) memcpy(xb + p * d, xs + (uint64_t)anc[p] * d, d * sizeof(double));
         double* tmp = xs; xs = xb; xb = tmp;
@@ -802,14 +776,7 @@ int ora_run_smc(const asmc_target_desc* target, const asmc_kernel_desc* kernel, 
                 int32_t steps, uint64_t n, int32_t policy, double rho, uint64_t seed, uint64_t round,
                 int32_t workers, asmc_report* out) {
   (void)workers;
-  return run_smc_impl(target, kernel, betas, steps, n, policy, rho, seed, round, 0, out);
-}
-
-/* run_smc with the device's blocked-CDF resampling (what the B200 path computes) */
-int ora_run_smc_blocked(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
-                        const double* betas, int32_t steps, uint64_t n, int32_t policy, double rho,
-                        uint64_t seed, uint64_t round, asmc_report* out) {
-  return run_smc_impl(target, kernel, betas, steps, n, policy, rho, seed, round, 1, out);
+  return run_smc_impl(target, kernel, betas, steps, n, policy, rho, seed, round, out);
 }
 
 /* drivers.cpp:72-182: per particle, init then t = 1..T into per-(block, t)
@@ -1275,7 +1242,7 @@ int ora_run_zja(const asmc_target_desc* tg, const asmc_kernel_desc* k, const asm
     for (int t = 0; t <= K; ++t) pb[t] = (double)t / (double)K;
     pb[0] = 0.0;
     pb[K] = 1.0;
-    int rc = run_smc_impl(tg, k, pb, K, n, ASMC_POLICY_NEVER, 0.5, o->seed, 1, 0, &out->pilot);
+    int rc = run_smc_impl(tg, k, pb, K, n, ASMC_POLICY_NEVER, 0.5, o->seed, 1, &out->pilot);
     if (!rc) rc = ora_barrier_estimate(out->pilot.log_g0, out->pilot.log_g1, out->pilot.log_g2, pb, K, lam);
     if (!rc) {
       if (out->pilot_lambda) memcpy(out->pilot_lambda, lam, (size_t)(K + 1) * sizeof(double));

@@ -216,6 +216,33 @@ def systematic_resample(log_w, u, device=0):
     return out
 
 
+def resample_cdf(log_w, device=0):
+    """(cum, l1): the sequential CDF engine.cpp:64-75 walks, built on the device."""
+    lw = np.ascontiguousarray(log_w, dtype=np.float64)
+    cum = np.zeros(len(lw))
+    l1 = C.c_double()
+    _check(lib().asmc_resample_cdf(_arr(lw, C.c_double), C.c_uint64(len(lw)), C.c_int32(device),
+                                   _arr(cum, C.c_double), C.byref(l1)))
+    return cum, l1.value
+
+
+def logsumexp(log_w, device=0):
+    """asmc::logsumexp (logsum.hpp:97-101) on the device."""
+    lw = np.ascontiguousarray(log_w, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().asmc_logsumexp(_arr(lw, C.c_double), C.c_uint64(len(lw)), C.c_int32(device), C.byref(out)))
+    return out.value
+
+
+def exact_math(which, x, device=0):
+    """The device's glibc-exact exp (which=0) / correctly rounded log (which=1)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros(len(x))
+    _check(lib().asmc_exact_math(C.c_int32(which), _arr(x, C.c_double), C.c_uint64(len(x)), C.c_int32(device),
+                                 _arr(out, C.c_double)))
+    return out
+
+
 def ess(log_w, device=0):
     lw = np.ascontiguousarray(log_w, dtype=np.float64)
     out = C.c_double()
@@ -326,7 +353,7 @@ class SmcShard:
                  rho=0.5, seed=0, round=0, exec_=None):
         L = lib()
         self._lib = L
-        for f in ("asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes"):
+        for f in ("asmc_smc_shard_chunks", "asmc_smc_shard_exchange_len", "asmc_smc_shard_row_bytes"):
             getattr(L, f).restype = C.c_uint64
             getattr(L, f).argtypes = [C.c_void_p]
         L.asmc_smc_shard_destroy.argtypes = [C.c_void_p]
@@ -344,24 +371,27 @@ class SmcShard:
                                        C.byref(h)))
         self._h = h
         self.chunks = L.asmc_smc_shard_chunks(h)
-        self.blocks = L.asmc_smc_shard_blocks(h)
+        self.exchange_len = L.asmc_smc_shard_exchange_len(h)
         self.row_bytes = L.asmc_smc_shard_row_bytes(h)
 
     def step(self, t, partials_ptr):
         _check(self._lib.asmc_smc_shard_step(self._h, C.c_int32(t), C.c_void_p(partials_ptr)))
 
-    def decide(self, t, all_partials_ptr, all_chunks, block_totals_ptr):
+    def decide(self, t, all_partials_ptr, all_chunks, lw_out_ptr):
+        """Fold + decision; on a resampling step copies this shard's log-weights
+        (exchange_len doubles) to lw_out_ptr for the caller's all-gather."""
         flag = C.c_int32(0)
         _check(self._lib.asmc_smc_shard_decide(self._h, C.c_int32(t), C.c_void_p(all_partials_ptr),
-                                                C.c_uint64(all_chunks), C.c_void_p(block_totals_ptr),
+                                                C.c_uint64(all_chunks), C.c_void_p(lw_out_ptr),
                                                 C.byref(flag)))
         return bool(flag.value)
 
-    def plan(self, all_block_totals_ptr, all_blocks, shard_p_begin):
+    def plan(self, all_lw_ptr, n_all, shard_p_begin):
+        """Global reference CDF over the all-gathered log-weights -> slot_begin."""
         b = np.ascontiguousarray(shard_p_begin, dtype=np.uint64)
         out = np.zeros(len(b), np.uint64)
-        _check(self._lib.asmc_smc_shard_plan(self._h, C.c_void_p(all_block_totals_ptr),
-                                              C.c_uint64(all_blocks), C.c_int32(len(b) - 1),
+        _check(self._lib.asmc_smc_shard_plan(self._h, C.c_void_p(all_lw_ptr),
+                                              C.c_uint64(n_all), C.c_int32(len(b) - 1),
                                               _arr(b, C.c_uint64), _arr(out, C.c_uint64)))
         return [int(v) for v in out]
 
@@ -399,7 +429,7 @@ class ZjaShard(SmcShard):
     def __init__(self, target, kernel, n, p_begin, p_end, seed=0, round=1, max_steps=100000, exec_=None):
         L = lib()
         self._lib = L
-        for f in ("asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes"):
+        for f in ("asmc_smc_shard_chunks", "asmc_smc_shard_exchange_len", "asmc_smc_shard_row_bytes"):
             getattr(L, f).restype = C.c_uint64
             getattr(L, f).argtypes = [C.c_void_p]
         L.asmc_smc_shard_destroy.argtypes = [C.c_void_p]
@@ -414,7 +444,7 @@ class ZjaShard(SmcShard):
                                        C.c_int32(max_steps), C.byref(self.exec_), C.byref(h)))
         self._h = h
         self.chunks = L.asmc_smc_shard_chunks(h)
-        self.blocks = L.asmc_smc_shard_blocks(h)
+        self.exchange_len = L.asmc_smc_shard_exchange_len(h)
         self.row_bytes = L.asmc_smc_shard_row_bytes(h)
 
     def eval(self):
@@ -439,10 +469,11 @@ EXPORTED = [
     "asmc_last_error", "asmc_version", "asmc_device_count", "asmc_launch_count", "asmc_run_smc",
     "asmc_run_sais_single", "asmc_run_rounds", "asmc_fold_chunks", "asmc_sais_partials",
     "asmc_fold_partials", "asmc_rng_u64", "asmc_rng_uniform", "asmc_rng_normal",
-    "asmc_trajectories", "asmc_systematic_resample", "asmc_ess", "asmc_barrier_estimate",
+    "asmc_trajectories", "asmc_systematic_resample", "asmc_resample_cdf", "asmc_logsumexp",
+    "asmc_exact_math", "asmc_ess", "asmc_barrier_estimate",
     "asmc_generate_schedule", "asmc_local_barrier", "asmc_budget", "asmc_profile_enable",
     "asmc_profile_collect", "asmc_peak_normals", "asmc_smc_shard_create", "asmc_smc_shard_destroy",
-    "asmc_smc_shard_chunks", "asmc_smc_shard_blocks", "asmc_smc_shard_row_bytes",
+    "asmc_smc_shard_chunks", "asmc_smc_shard_exchange_len", "asmc_smc_shard_row_bytes",
     "asmc_smc_shard_step", "asmc_smc_shard_decide", "asmc_smc_shard_plan", "asmc_smc_shard_pack",
     "asmc_smc_shard_accept", "asmc_smc_shard_report", "asmc_smc_shard_state", "asmc_run_zja",
     "asmc_zja_next_beta", "asmc_run_pt", "asmc_profile_collect_drawn", "asmc_zja_shard_create",

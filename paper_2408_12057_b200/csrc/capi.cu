@@ -119,6 +119,16 @@ double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// Systematic resampling with the reference's sequential CDF (refcdf.cu): one cooperative
+// launch, returns at once on steps whose decision did not fire.  work: refcdf_work_bytes(n).
+cudaError_t launch_resample_ref(DevCtx* C, const double* lw, uint64_t n, SmcState* st, void* work,
+                                double* cum, uint32_t* anc, int gated = 1) {
+  RefCdfWork w;
+  refcdf_work_carve(work, n, &w);
+  return launch_refcdf(lw, n, st, gated, &w, cum, anc, 1, C->sms, C->stream);
+}
+uint64_t refcdf_work_doubles(uint64_t n) { return (refcdf_work_bytes(n) + 7) / 8; }
+
 // ---------------------------------------------------------------- checks --
 // Schedule::validate (src/engine.cpp:29-39)
 int check_schedule(const double* b, int T) {
@@ -496,7 +506,7 @@ int enqueue_smc_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs& 
   TRY(W.xcur.alloc(1, C->stream));
   TRY(W.lw.alloc(n, C->stream));
   TRY(W.cum.alloc(n, C->stream));
-  TRY(W.btot.alloc(nblk, C->stream));
+  TRY(W.btot.alloc(refcdf_work_doubles(n), C->stream));  // refcdf scratch
   TRY(W.anc.alloc(n, C->stream));
   TRY(W.part.alloc((size_t)kNAcc * nblk, C->stream));
   TRY(W.chunk.alloc((size_t)kNAcc * nchunks, C->stream));
@@ -529,8 +539,7 @@ int enqueue_smc_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs& 
     LCH(launch_pass(ex, L, A, nblk, C->stream));
     LCH(launch_fold(exact, W.part.p, nblk, nblk, 0, 1, kNAcc, W.chunk.p, W.tot.p, C->stream));
     LCH(launch_smc_decide(W.tot.p, t, T, n, policy, rho, seed, round, ex.rng, d_rd, C->stream));
-    LCH(launch_resample(W.lw.p, n, d_st, W.cum.p, W.btot.p, W.anc.p, C->stream));
-    g_launches += 3;  // launch_resample issues four kernels
+    LCH(launch_resample_ref(C, W.lw.p, n, d_st, W.btot.p, W.cum.p, W.anc.p));
     LCH(launch_gather(W.anc.p, n, d * real, W.xbuf.p, W.xcur.p, W.lw.p, d_st, C->sms, C->stream));
     g_launches += 1;
   }
@@ -638,7 +647,7 @@ int enqueue_lg_round(DevCtx* C, const LgData& D, const asmc_target_desc* t, cons
   TRY(W.xcur.alloc(1, C->stream));
   TRY(W.lw.alloc(n, C->stream));
   TRY(W.cum.alloc(n, C->stream));
-  TRY(W.btot.alloc(nblk, C->stream));
+  TRY(W.btot.alloc(refcdf_work_doubles(n), C->stream));  // refcdf scratch
   TRY(W.anc.alloc(n, C->stream));
   TRY(W.part.alloc((size_t)kNAcc * nblk, C->stream));
   TRY(W.chunk.alloc((size_t)kNAcc * nchunks, C->stream));
@@ -680,8 +689,7 @@ int enqueue_lg_round(DevCtx* C, const LgData& D, const asmc_target_desc* t, cons
     LCH(launch_smc_decide(W.tot.p, s, T, n, policy, rho, seed, round, ASMC_RNG_PHILOX, d_rd, C->stream));
     for (int q = 0; q < nprop; ++q)  // kernel.cpp:31-40 at beta_t
       TRY(lg_eval(C, D, A, 1, d_betas, (float)k->step_sizes[q % k->n_step_sizes], q));
-    LCH(launch_resample(W.lw.p, n, d_st, W.cum.p, W.btot.p, W.anc.p, C->stream));
-    g_launches += 3;
+    LCH(launch_resample_ref(C, W.lw.p, n, d_st, W.btot.p, W.cum.p, W.anc.p));
     LCH(launch_gather(W.anc.p, n, (uint64_t)row * sizeof(float), reinterpret_cast<void* const*>(W.sbuf.p),
                       W.xcur.p, W.lw.p, d_st, C->sms, C->stream));
     g_launches += 1;
@@ -734,7 +742,7 @@ int enqueue_is_round(DevCtx* C, const asmc_target_desc* t, const asmc_kernel_des
   TRY(W.xcur.alloc(1, C->stream));
   TRY(W.lw.alloc(n, C->stream));
   TRY(W.cum.alloc(n, C->stream));
-  TRY(W.btot.alloc(nblk, C->stream));
+  TRY(W.btot.alloc(refcdf_work_doubles(n), C->stream));  // refcdf scratch
   TRY(W.anc.alloc(n, C->stream));
   TRY(W.part.alloc((size_t)kNAcc * nblk, C->stream));
   TRY(W.chunk.alloc((size_t)kNAcc * nchunks, C->stream));
@@ -771,8 +779,7 @@ int enqueue_is_round(DevCtx* C, const asmc_target_desc* t, const asmc_kernel_des
     LCH(launch_fold(false, W.part.p, nblk, nblk, 0, 1, kNAcc, W.chunk.p, W.tot.p, C->stream));
     LCH(launch_smc_decide(W.tot.p, s, T, n, policy, rho, seed, round, ASMC_RNG_PHILOX, d_rd, C->stream));
     TRY(is_move(C, I, 1, d_betas, s));  // kernel.cpp:26-63 at beta_t
-    LCH(launch_resample(W.lw.p, n, d_st, W.cum.p, W.btot.p, W.anc.p, C->stream));
-    g_launches += 3;
+    LCH(launch_resample_ref(C, W.lw.p, n, d_st, W.btot.p, W.cum.p, W.anc.p));
     LCH(launch_gather(W.anc.p, n, (uint64_t)row * sizeof(float), reinterpret_cast<void* const*>(W.sbuf.p),
                       W.xcur.p, W.lw.p, d_st, C->sms, C->stream));
     g_launches += 1;
@@ -1313,18 +1320,20 @@ int asmc_rng_normal(int32_t rng, int32_t precision, const uint64_t key[5], uint6
   return rng_common(rng, 2, precision, key, count, out);
 }
 
-int asmc_systematic_resample(const double* log_w, uint64_t n, double u, int32_t device,
-                             uint32_t* ancestors) {
+// engine.cpp:61-80 on the device (refcdf.cu): the reference's sequential CDF bit for bit
+// (cum_out, optional: the n CDF values; l1_out, optional: logsumexp(log_w)).
+static int resample_common(const double* log_w, uint64_t n, double u, int32_t device, uint32_t* ancestors,
+                           double* cum_out, double* l1_out, int what) {
   if (n == 0) return fail(ASMC_ERR_INVALID_ARGUMENT, "cannot resample an empty system");
   if (n > 0xffffffffull) return fail(ASMC_ERR_CAPABILITY, "ancestor indices are 32-bit");
   DevCtx* C;
   TRY(get_ctx(device, &C));
-  DBuf<double> lw, cum, btot;
+  DBuf<double> lw, cum, work;
   DBuf<uint32_t> anc;
   DBuf<SmcState> st;
   TRY(lw.alloc(n, C->stream));
   TRY(cum.alloc(n, C->stream));
-  TRY(btot.alloc(nblocks(n), C->stream));
+  TRY(work.alloc(refcdf_work_doubles(n), C->stream));
   TRY(anc.alloc(n, C->stream));
   TRY(st.alloc(1, C->stream));
   SmcState h;
@@ -1333,12 +1342,56 @@ int asmc_systematic_resample(const double* log_w, uint64_t n, double u, int32_t 
   h.u = u;
   CU(cudaMemcpyAsync(st.p, &h, sizeof h, cudaMemcpyHostToDevice, C->stream));
   CU(cudaMemcpyAsync(lw.p, log_w, sizeof(double) * n, cudaMemcpyHostToDevice, C->stream));
-  LCH(launch_max(lw.p, n, st.p, C->stream));
-  LCH(launch_resample(lw.p, n, st.p, cum.p, btot.p, anc.p, C->stream));
-  CU(cudaMemcpyAsync(ancestors, anc.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, C->stream));
+  RefCdfWork w;
+  refcdf_work_carve(work.p, n, &w);
+  LCH(launch_refcdf(lw.p, n, st.p, 0, &w, cum.p, anc.p, what, C->sms, C->stream));
+  if (ancestors && what == 1)
+    CU(cudaMemcpyAsync(ancestors, anc.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, C->stream));
+  if (cum_out && what >= 0)
+    CU(cudaMemcpyAsync(cum_out, cum.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C->stream));
+  double l1 = 0.0;
+  CU(cudaMemcpyAsync(&l1, w.l1, sizeof(double), cudaMemcpyDeviceToHost, C->stream));
   CU(cudaMemcpyAsync(&h, st.p, sizeof h, cudaMemcpyDeviceToHost, C->stream));
   CU(cudaStreamSynchronize(C->stream));
+  if (l1_out) *l1_out = l1;
   if (h.err) return fail(ASMC_ERR_DEGENERATE, "all log-weights are -inf");
+  return 0;
+}
+
+int asmc_systematic_resample(const double* log_w, uint64_t n, double u, int32_t device,
+                             uint32_t* ancestors) {
+  return resample_common(log_w, n, u, device, ancestors, nullptr, nullptr, 1);
+}
+
+int asmc_resample_cdf(const double* log_w, uint64_t n, int32_t device, double* cum_out, double* l1_out) {
+  return resample_common(log_w, n, 0.0, device, nullptr, cum_out, l1_out, 0);
+}
+
+int asmc_logsumexp(const double* log_w, uint64_t n, int32_t device, double* out) {
+  if (n == 0) {  // logsum.hpp:40-42 on an empty accumulator
+    if (out) *out = -__builtin_huge_val();
+    return 0;
+  }
+  const int rc = resample_common(log_w, n, 0.0, device, nullptr, nullptr, out, -1);
+  if (rc == ASMC_ERR_DEGENERATE) {  // an all -inf input is a value here, not an error
+    if (out) *out = -__builtin_huge_val();
+    return 0;
+  }
+  return rc;
+}
+
+int asmc_exact_math(int32_t which, const double* x, uint64_t n, int32_t device, double* out) {
+  if (which != 0 && which != 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "which must be 0 (exp) or 1 (log)");
+  if (n == 0) return 0;
+  DevCtx* C;
+  TRY(get_ctx(device, &C));
+  DBuf<double> a, b;
+  TRY(a.alloc(n, C->stream));
+  TRY(b.alloc(n, C->stream));
+  CU(cudaMemcpyAsync(a.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, C->stream));
+  LCH(launch_exact_math(which, a.p, n, b.p, C->stream));
+  CU(cudaMemcpyAsync(out, b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, C->stream));
+  CU(cudaStreamSynchronize(C->stream));
   return 0;
 }
 
@@ -1826,6 +1879,7 @@ struct asmc_smc_shard {
   DBuf<uint32_t> anc;
   DBuf<LogAcc> part, chunk, tot;
   DBuf<uint64_t> rank_blk, slot_dev;
+  DBuf<double> cum_all, work;  // resampling: global CDF + refcdf scratch (allocated on first event)
   RoundBufs R;
   std::vector<uint64_t> slots;
   // multi-GPU ZJA mode: open-ended schedule (betas[t] set per step), potential cache, probes
@@ -1887,7 +1941,6 @@ int asmc_smc_shard_create(const asmc_target_desc* target, const asmc_kernel_desc
     TRY(h->xbuf.alloc(2, s));
     TRY(h->xcur.alloc(1, s));
     TRY(h->lw.alloc(nl, s));
-    TRY(h->cum.alloc(nl, s));
     TRY(h->part.alloc((size_t)kNAcc * h->nblk, s));
     TRY(h->chunk.alloc((size_t)kNAcc * h->nch, s));
     TRY(h->tot.alloc(kNAcc, s));
@@ -1926,7 +1979,7 @@ void asmc_smc_shard_destroy(asmc_smc_shard* h) {
 }
 
 uint64_t asmc_smc_shard_chunks(const asmc_smc_shard* h) { return h ? h->nch : 0; }
-uint64_t asmc_smc_shard_blocks(const asmc_smc_shard* h) { return h ? h->nblk : 0; }
+uint64_t asmc_smc_shard_exchange_len(const asmc_smc_shard* h) { return h ? h->n_local : 0; }
 uint64_t asmc_smc_shard_row_bytes(const asmc_smc_shard* h) { return h ? h->row_bytes : 0; }
 
 int asmc_smc_shard_step(asmc_smc_shard* h, int32_t t, asmc_logacc* partials_dev) {
@@ -1945,8 +1998,8 @@ int asmc_smc_shard_step(asmc_smc_shard* h, int32_t t, asmc_logacc* partials_dev)
 }
 
 int asmc_smc_shard_decide(asmc_smc_shard* h, int32_t t, const asmc_logacc* all_dev, uint64_t all_chunks,
-                          double* btot_dev, int32_t* resample) {
-  if (!h || !all_dev || !btot_dev || !resample) return fail(ASMC_ERR_INVALID_ARGUMENT, "null argument");
+                          double* lw_out_dev, int32_t* resample) {
+  if (!h || !all_dev || !lw_out_dev || !resample) return fail(ASMC_ERR_INVALID_ARGUMENT, "null argument");
   if (t != h->t_done + 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "decide for step %d out of order", t);
   if (all_chunks != asmc_fold_chunks(0, h->n))
     return fail(ASMC_ERR_INVALID_ARGUMENT, "expected %llu chunk partials, got %llu",
@@ -1955,35 +2008,34 @@ int asmc_smc_shard_decide(asmc_smc_shard* h, int32_t t, const asmc_logacc* all_d
   LCH(launch_fold_chunk_major(reinterpret_cast<const LogAcc*>(all_dev), all_chunks, h->tot.p, s));
   LCH(launch_smc_decide(h->tot.p, t, h->zja ? -1 : h->T, h->n, h->policy, h->rho, h->seed, h->round, h->ex.rng,
                         h->R.rd.p, s, h->zja ? h->betas.p : nullptr));
-  LCH(launch_cdf_blocks(h->lw.p, h->n_local, h->R.st.p, h->cum.p, btot_dev, s));
   SmcState st;
   CU(cudaMemcpyAsync(&st, h->R.st.p, sizeof st, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   TRY(device_error(st.err, st.err_step, st.err_val));
+  if (st.resample_now)  // this shard's log-weights, for the caller's all-gather
+    CU(cudaMemcpyAsync(lw_out_dev, h->lw.p, h->n_local * sizeof(double), cudaMemcpyDeviceToDevice, s));
   h->t_done = t;
   h->resampling = st.resample_now;
   *resample = st.resample_now;
   return 0;
 }
 
-int asmc_smc_shard_plan(asmc_smc_shard* h, double* all_btot_dev, uint64_t all_blocks, int32_t world,
+int asmc_smc_shard_plan(asmc_smc_shard* h, const double* all_lw_dev, uint64_t all_len, int32_t world,
                         const uint64_t* shard_p_begin, uint64_t* slot_begin) {
-  if (!h || !all_btot_dev || !shard_p_begin || !slot_begin)
+  if (!h || !all_lw_dev || !shard_p_begin || !slot_begin)
     return fail(ASMC_ERR_INVALID_ARGUMENT, "null argument");
   if (!h->resampling) return fail(ASMC_ERR_INVALID_ARGUMENT, "plan without a resampling decision");
   if (world < 1 || world > 1023) return fail(ASMC_ERR_INVALID_ARGUMENT, "world size must be in [1, 1023]");
-  if (all_blocks != nblocks(h->n))
-    return fail(ASMC_ERR_INVALID_ARGUMENT, "expected %llu block totals, got %llu",
-                (unsigned long long)nblocks(h->n), (unsigned long long)all_blocks);
+  if (all_len != h->n)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "expected %llu log-weights, got %llu", (unsigned long long)h->n,
+                (unsigned long long)all_len);
   if (shard_p_begin[0] != 0 || shard_p_begin[world] != h->n)
     return fail(ASMC_ERR_INVALID_ARGUMENT, "shard boundaries must span [0, n_particles)");
   h->me = -1;
-  std::vector<uint64_t> rb(world + 1);
-  for (int r = 0; r <= world; ++r) {
-    if (r < world && (shard_p_begin[r] > shard_p_begin[r + 1] || shard_p_begin[r] % ASMC_FOLD_CHUNK))
+  for (int r = 0; r < world; ++r) {
+    if (shard_p_begin[r] > shard_p_begin[r + 1] || shard_p_begin[r] % ASMC_FOLD_CHUNK)
       return fail(ASMC_ERR_INVALID_ARGUMENT, "shard boundaries must be ordered multiples of ASMC_FOLD_CHUNK");
-    rb[r] = nblocks(shard_p_begin[r]);
-    if (r < world && shard_p_begin[r] == h->p_begin && shard_p_begin[r + 1] == h->p_begin + h->n_local) h->me = r;
+    if (shard_p_begin[r] == h->p_begin && shard_p_begin[r + 1] == h->p_begin + h->n_local) h->me = r;
   }
   if (h->me < 0) return fail(ASMC_ERR_INVALID_ARGUMENT, "this shard's range is not among the shard boundaries");
   cudaStream_t s = h->C.stream;
@@ -1996,10 +2048,17 @@ int asmc_smc_shard_plan(asmc_smc_shard* h, double* all_btot_dev, uint64_t all_bl
     TRY(h->slot_dev.alloc(world + 1, s));
     h->slots.assign(world + 1, 0);
   }
-  CU(cudaMemcpyAsync(h->rank_blk.p, rb.data(), sizeof(uint64_t) * (world + 1), cudaMemcpyHostToDevice, s));
-  LCH(launch_shard_plan(all_btot_dev, all_blocks, h->cum.p, h->n_local, nblocks(h->p_begin), h->rank_blk.p,
-                        world, h->n, h->R.st.p, h->slot_dev.p, s));
-  g_launches += 2;
+  if (!h->cum_all.p) {  // the global CDF and ancestors, identical on every rank
+    TRY(h->cum_all.alloc(h->n, s));
+    TRY(h->work.alloc(refcdf_work_doubles(h->n), s));
+    TRY(h->anc.alloc(h->n, s));
+    h->anc_cap = h->n;
+  }
+  CU(cudaMemcpyAsync(h->rank_blk.p, shard_p_begin, sizeof(uint64_t) * (world + 1), cudaMemcpyHostToDevice, s));
+  RefCdfWork w;
+  refcdf_work_carve(h->work.p, h->n, &w);
+  LCH(launch_refcdf(all_lw_dev, h->n, h->R.st.p, 1, &w, h->cum_all.p, h->anc.p, 1, h->C.sms, s));
+  LCH(launch_slot_bounds(h->anc.p, h->n, h->rank_blk.p, world, h->R.st.p, h->slot_dev.p, s));
   CU(cudaMemcpyAsync(h->slots.data(), h->slot_dev.p, sizeof(uint64_t) * (world + 1), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   std::memcpy(slot_begin, h->slots.data(), sizeof(uint64_t) * (world + 1));
@@ -2010,16 +2069,7 @@ int asmc_smc_shard_pack(asmc_smc_shard* h, void* rows_dev) {
   if (!h || h->me < 0 || !h->resampling) return fail(ASMC_ERR_INVALID_ARGUMENT, "pack before plan");
   const uint64_t lo = h->slots[h->me], count = h->slots[h->me + 1] - lo;
   if (count && !rows_dev) return fail(ASMC_ERR_INVALID_ARGUMENT, "null row buffer");
-  cudaStream_t s = h->C.stream;
-  if (count > h->anc_cap) {
-    h->anc.~DBuf();
-    new (&h->anc) DBuf<uint32_t>();
-    TRY(h->anc.alloc(count, s));
-    h->anc_cap = count;
-  }
-  LCH(launch_shard_pack(h->cum.p, h->n_local, h->R.st.p, lo, count, h->n, h->anc.p, h->row_bytes, h->x.p,
-                        rows_dev, h->C.sms, s));
-  if (count) g_launches += 1;
+  LCH(launch_pack_rows(h->anc.p + lo, count, h->p_begin, h->row_bytes, h->x.p, rows_dev, h->C.sms, h->C.stream));
   return 0;
 }
 

@@ -91,34 +91,6 @@ __device__ __forceinline__ LogAcc shfl_xor_acc(const LogAcc& v, int m, unsigned 
   return LogAcc{__shfl_xor_sync(mask, v.max, m), __shfl_xor_sync(mask, v.sum, m)};
 }
 
-// Deterministic exp for x <= 0 from +,-,* only: identical bits to
-// oracle/restate.c:exp_det.  The __d*_rn intrinsics are never contracted into
-// FMA, so the result does not depend on -fmad.  Used for the resampling CDF so
-// the ancestor search is reproducible bit for bit on the host.
-__device__ __forceinline__ double exp_det(double x) {
-  if (x == -__builtin_huge_val() || x < -745.2) return 0.0;
-  const double kLn2Hi = 6.93147180369123816490e-01;
-  const double kLn2Lo = 1.90821492927058770002e-10;
-  const double kInvLn2 = 1.44269504088896338700e+00;
-  double kf = __dmul_rn(x, kInvLn2);
-  kf = kf < 0.0 ? (double)(long long)__dsub_rn(kf, 0.5) : (double)(long long)__dadd_rn(kf, 0.5);
-  const double r = __dsub_rn(__dsub_rn(x, __dmul_rn(kf, kLn2Hi)), __dmul_rn(kf, kLn2Lo));
-  const double c[13] = {1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0,
-                        1.0 / 40320.0,     1.0 / 5040.0,     1.0 / 720.0,     1.0 / 120.0,
-                        1.0 / 24.0,        1.0 / 6.0,        0.5,             1.0,
-                        1.0};
-  double p = 1.0 / 6227020800.0;
-#pragma unroll
-  for (int i = 0; i < 13; ++i) p = __dadd_rn(__dmul_rn(p, r), c[i]);
-  int k = (int)kf;
-  if (k < -1000) {
-    p = __dmul_rn(p, 0x1.0p-1000);
-    k += 1000;
-  }
-  const double s = __longlong_as_double((long long)(k + 1023) << 52);
-  return __dmul_rn(p, s);
-}
-
 // Error word: the first failing particle records its code (ASMC_ERR_*).
 __device__ __forceinline__ void raise_error(int* err, int code) {
   if (err) atomicCAS(err, 0, code);

@@ -283,75 +283,7 @@ __global__ void smc_decide_kernel(const LogAcc* tot, int t, int T_in, uint64_t n
 }
 
 // ------------------------------------------------------- resampling --
-// Blocked deterministic CDF (oracle/restate.c:ora_systematic_resample_blocked):
-// w_j = exp_det(lw_j - max), sequential inclusive sums inside each 256-block.
-__global__ void cdf_block_kernel(const double* lw, uint64_t n, const SmcState* st, double* cum,
-                                 double* btot) {
-  if (!st->resample_now) return;
-  const uint64_t b = blockIdx.x;
-  __shared__ double w[kBlock];
-  const uint64_t j = b * kBlock + threadIdx.x;
-  const double mx = st->max_lw;
-  w[threadIdx.x] = j < n ? exp_det(lw[j] - mx) : 0.0;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    const int m = (int)umin64((uint64_t)(kBlock), (uint64_t)(n - b * kBlock));
-    for (int i = 0; i < m; ++i) {
-      s = __dadd_rn(s, w[i]);
-      w[i] = s;
-    }
-    btot[b] = s;
-  }
-  __syncthreads();
-  if (j < n) cum[j] = w[threadIdx.x];
-}
-
-// Sequential exclusive scan of block totals (one CTA, tiles staged in smem).
-__global__ void cdf_scan_kernel(double* btot, uint64_t nblk, SmcState* st) {
-  if (!st->resample_now) return;
-  __shared__ double tile[2048];
-  double off = 0.0;
-  for (uint64_t b0 = 0; b0 < nblk; b0 += 2048) {
-    const int m = (int)umin64((uint64_t)(2048), (uint64_t)(nblk - b0));
-    for (int i = threadIdx.x; i < m; i += blockDim.x) tile[i] = btot[b0 + i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < m; ++i) {
-        const double v = tile[i];
-        tile[i] = off;
-        off = __dadd_rn(off, v);
-      }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < m; i += blockDim.x) btot[b0 + i] = tile[i];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) st->total = off;
-}
-
-__global__ void cdf_offset_kernel(double* cum, const double* boff, uint64_t n, const SmcState* st) {
-  if (!st->resample_now) return;
-  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) cum[j] = __dadd_rn(cum[j], boff[j / kBlock]);
-}
-
-// a_m = first j with !(cum_j < pos_m), clamped to n-1 (engine.cpp:72-76)
-__global__ void ancestor_kernel(const double* cum, uint64_t n, const SmcState* st, uint32_t* anc) {
-  if (!st->resample_now) return;
-  const uint64_t m = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= n) return;
-  const double total = st->total;
-  const double pos = __dmul_rn(__ddiv_rn(__dadd_rn((double)m, st->u), (double)n), total);
-  uint64_t lo = 0, hi = n;  // lower_bound
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (cum[mid] < pos) lo = mid + 1;
-    else hi = mid;
-  }
-  anc[m] = (uint32_t)(lo < n ? lo : n - 1);
-}
-
+// Ancestors: refcdf.cu (the reference's sequential CDF, bit for bit).
 // x_new[m] = x[a_m] (row copy, 16-byte vectors when the row allows), lw <- 0
 __global__ void gather_kernel(const uint32_t* anc, uint64_t n, uint64_t row_bytes,
                               void* const* xbuf, int* xcur, double* lw, const SmcState* st) {
@@ -611,20 +543,6 @@ __global__ void ess_kernel(const double* lw, uint64_t n, double* out, int* err) 
 }
 
 // max of log-weights (exact; order-free)
-__global__ void max_kernel(const double* lw, uint64_t n, SmcState* st) {
-  __shared__ double w[32];
-  double m = kNegInf;
-  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, lw[i]);
-  for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double r = kNegInf;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = fmax(r, w[i]);
-    st->max_lw = r;
-    if (r == kNegInf) st->err = ASMC_ERR_DEGENERATE;
-  }
-}
 
 // ============================================================ launchers ===
 #define LAUNCH_OK() cudaGetLastError()
@@ -672,16 +590,6 @@ cudaError_t launch_smc_decide(const LogAcc* tot_row, int t, int T, uint64_t n, i
   return LAUNCH_OK();
 }
 
-cudaError_t launch_resample(const double* lw_in, uint64_t n, SmcState* st, double* cum,
-                            double* btot, uint32_t* anc, cudaStream_t s) {
-  const uint64_t nblk = (n + kBlock - 1) / kBlock;
-  cdf_block_kernel<<<(unsigned)nblk, kBlock, 0, s>>>(lw_in, n, st, cum, btot);
-  cdf_scan_kernel<<<1, 1024, 0, s>>>(btot, nblk, st);
-  cdf_offset_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cum, btot, n, st);
-  ancestor_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cum, n, st, anc);
-  return LAUNCH_OK();
-}
-
 cudaError_t launch_gather(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,
                           int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s) {
   gather_kernel<<<sms * 8, 256, 0, s>>>(anc, n, row_bytes, xbuf, xcur, lw, st);
@@ -691,10 +599,6 @@ cudaError_t launch_gather(const uint32_t* anc, uint64_t n, uint64_t row_bytes, v
   return LAUNCH_OK();
 }
 
-cudaError_t launch_max(const double* lw, uint64_t n, SmcState* st, cudaStream_t s) {
-  max_kernel<<<1, 1024, 0, s>>>(lw, n, st);
-  return LAUNCH_OK();
-}
 
 cudaError_t launch_generate_schedule(const double* lambda, const double* beta, int knots, int t_new,
                                      double* out, double* scratch, int* err, cudaStream_t s) {
@@ -746,60 +650,38 @@ __global__ void fold_chunk_major_kernel(const LogAcc* in, uint64_t nch, LogAcc* 
   tot[a] = acc;
 }
 
-// pos_m of engine.cpp:68-70, in the operation order of ancestor_kernel
-__device__ __forceinline__ double slot_pos(uint64_t m, double u, uint64_t n, double total) {
-  return __dmul_rn(__ddiv_rn(__dadd_rn((double)m, u), (double)n), total);
-}
-
-// Output slot m lands in shard r's particles iff cum[p_r - 1] < pos_m <= cum[p_{r+1} - 1];
-// cum[p_r - 1] equals the exclusive block offset boff[rank_blk[r]] (same dadd of the
-// same two operands), so every rank derives the same slot ranges from the scan.
-__global__ void shard_bounds_kernel(const double* boff, uint64_t nblk_all, const uint64_t* rank_blk,
-                                    int world, uint64_t n, const SmcState* st, uint64_t* slot_begin) {
+// Output slot m lands in shard r iff its ancestor does: a_m is non-decreasing in m, so
+// shard r's slots are [first m with a_m >= p_r, first m with a_m >= p_{r+1}).
+__global__ void slot_bounds_kernel(const uint32_t* anc, uint64_t n, const uint64_t* shard_p, int world,
+                                   const SmcState* st, uint64_t* slot_begin) {
   const int r = threadIdx.x;
-  if (r > world) return;
-  if (r == 0) { slot_begin[0] = 0; return; }
-  if (r == world) { slot_begin[world] = n; return; }
-  const double total = st->total, u = st->u;
-  const double thr = rank_blk[r] < nblk_all ? boff[rank_blk[r]] : total;
-  uint64_t lo = 0, hi = n;  // first m with pos_m > thr (pos is non-decreasing in m)
+  if (r > world || !st->resample_now) return;
+  const uint64_t p = shard_p[r];
+  uint64_t lo = 0, hi = n;
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
-    if (slot_pos(mid, u, n, total) <= thr) lo = mid + 1;
+    if ((uint64_t)anc[mid] < p) lo = mid + 1;
     else hi = mid;
   }
-  slot_begin[r] = lo;
+  slot_begin[r] = r == world ? n : lo;
 }
 
-__global__ void shard_ancestor_kernel(const double* cum, uint64_t n_local, const SmcState* st,
-                                      uint64_t slot_lo, uint64_t count, uint64_t n, uint32_t* anc) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
-  const double pos = slot_pos(slot_lo + i, st->u, n, st->total);
-  uint64_t lo = 0, hi = n_local;
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (cum[mid] < pos) lo = mid + 1;
-    else hi = mid;
-  }
-  anc[i] = (uint32_t)(lo < n_local ? lo : n_local - 1);
-}
-
-__global__ void pack_rows_kernel(const uint32_t* anc, uint64_t count, uint64_t row_bytes,
+// rows of global ancestors anc[0..count) (this shard starts at particle p0), slot order
+__global__ void pack_rows_kernel(const uint32_t* anc, uint64_t count, uint64_t p0, uint64_t row_bytes,
                                  const char* src, char* dst) {
   if (row_bytes % 16 == 0) {
     const uint64_t vec = row_bytes / 16, total = count * vec;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x) {
       const uint64_t m = i / vec, v = i % vec;
-      ((uint4*)(dst + m * row_bytes))[v] = ((const uint4*)(src + (uint64_t)anc[m] * row_bytes))[v];
+      ((uint4*)(dst + m * row_bytes))[v] = ((const uint4*)(src + ((uint64_t)anc[m] - p0) * row_bytes))[v];
     }
   } else {
     const uint64_t w4 = row_bytes / 4, total = count * w4;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x) {
       const uint64_t m = i / w4, v = i % w4;
-      ((uint32_t*)(dst + m * row_bytes))[v] = ((const uint32_t*)(src + (uint64_t)anc[m] * row_bytes))[v];
+      ((uint32_t*)(dst + m * row_bytes))[v] = ((const uint32_t*)(src + ((uint64_t)anc[m] - p0) * row_bytes))[v];
     }
   }
 }
@@ -815,29 +697,16 @@ cudaError_t launch_fold_chunk_major(const LogAcc* in, uint64_t nch, LogAcc* tot,
   return LAUNCH_OK();
 }
 
-cudaError_t launch_cdf_blocks(const double* lw, uint64_t n, const SmcState* st, double* cum,
-                              double* btot, cudaStream_t s) {
-  cdf_block_kernel<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(lw, n, st, cum, btot);
+cudaError_t launch_slot_bounds(const uint32_t* anc, uint64_t n, const uint64_t* shard_p, int world,
+                               const SmcState* st, uint64_t* slot_begin, cudaStream_t s) {
+  slot_bounds_kernel<<<1, 1024, 0, s>>>(anc, n, shard_p, world, st, slot_begin);
   return LAUNCH_OK();
 }
 
-cudaError_t launch_shard_plan(double* btot_all, uint64_t nblk_all, double* cum, uint64_t n_local,
-                              uint64_t blk_begin, const uint64_t* rank_blk, int world, uint64_t n,
-                              SmcState* st, uint64_t* slot_begin, cudaStream_t s) {
-  cdf_scan_kernel<<<1, 1024, 0, s>>>(btot_all, nblk_all, st);
-  if (n_local)
-    cdf_offset_kernel<<<(unsigned)((n_local + 255) / 256), 256, 0, s>>>(cum, btot_all + blk_begin, n_local, st);
-  shard_bounds_kernel<<<1, 1024, 0, s>>>(btot_all, nblk_all, rank_blk, world, n, st, slot_begin);
-  return LAUNCH_OK();
-}
-
-cudaError_t launch_shard_pack(const double* cum, uint64_t n_local, const SmcState* st,
-                              uint64_t slot_lo, uint64_t count, uint64_t n, uint32_t* anc,
-                              uint64_t row_bytes, const void* x, void* dst, int sms, cudaStream_t s) {
+cudaError_t launch_pack_rows(const uint32_t* anc, uint64_t count, uint64_t p0, uint64_t row_bytes, const void* x,
+                             void* dst, int sms, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
-  shard_ancestor_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(cum, n_local, st, slot_lo,
-                                                                       count, n, anc);
-  pack_rows_kernel<<<sms * 8, 256, 0, s>>>(anc, count, row_bytes, (const char*)x, (char*)dst);
+  pack_rows_kernel<<<sms * 8, 256, 0, s>>>(anc, count, p0, row_bytes, (const char*)x, (char*)dst);
   return LAUNCH_OK();
 }
 

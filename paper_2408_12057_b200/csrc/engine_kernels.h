@@ -14,8 +14,8 @@ namespace asmcdev {
 struct SmcState {
   double log_z, elbo, acc_dhat, den_log;
   double u;       // resampling uniform of the current step
-  double max_lw;  // max post-update log-weight (CDF shift)
-  double total;   // CDF total
+  double max_lw;  // max post-update log-weight
+  double total;   // CDF total cum[n-1]
   double err_val;
   int resample_now;
   int n_resample;
@@ -37,6 +37,34 @@ struct RoundDev {
   SmcState* state;
 };
 
+// Scratch of the reference-CDF resampler (refcdf.cu), per 256-particle block.
+struct RefCdfWork {
+  double* bmax;    // block max -> exclusive prefix max (l1 pass)
+  double* ba;      // approximate block composite s -> ba s + bb
+  double* bb;
+  double* sstart;  // approximate running value at each block start (nblk + 1)
+  unsigned long long* tot;  // exact integer total of a stable block at its binade
+  unsigned long long* pw;   // exclusive prefix of the totals inside the block's run
+  double* shead;   // exact running value at each run's first block
+  int* kb;         // binade of a stable block, or unstable
+  int* hid;        // run index of each block
+  int* heads;      // first block of each run (+ sentinel)
+  double* gmax;    // max log-weight
+  double* l1;      // logsumexp of the log-weights (the reference's bits)
+  int* nheads;
+};
+size_t refcdf_work_bytes(uint64_t n);
+void refcdf_work_carve(void* base, uint64_t n, RefCdfWork* w);
+// Systematic resampling (engine.cpp:61-80) with the reference's sequential CDF, bit for
+// bit: st->u is the uniform, ancestors to anc (want_anc), the CDF to cum (n doubles),
+// st->total = cum[n-1].  gated: return at once unless st->resample_now.  One cooperative
+// launch.
+cudaError_t launch_refcdf(const double* lw, uint64_t n, SmcState* st, int gated, const RefCdfWork* w,
+                          double* cum, uint32_t* anc, int want_anc, int sms, cudaStream_t s);
+
+// parity hook: which = 0 -> gexp (glibc's exp), 1 -> crlog (correctly rounded log)
+cudaError_t launch_exact_math(int which, const double* x, uint64_t n, double* out, cudaStream_t s);
+
 cudaError_t launch_fold(bool exact, const LogAcc* part, uint64_t stride, uint64_t nblk, int row0,
                         int nrows, int nacc, LogAcc* chunk_scratch, LogAcc* out, cudaStream_t s);
 cudaError_t launch_fold_chunks(const LogAcc* part, uint64_t stride, uint64_t nblk, int row0,
@@ -48,11 +76,8 @@ cudaError_t launch_sais_report(const LogAcc* tot, int T, uint64_t n, RoundDev* r
 cudaError_t launch_smc_decide(const LogAcc* tot_row, int t, int T, uint64_t n, int policy,
                               double rho, uint64_t seed, uint64_t round, int rng, RoundDev* rd,
                               cudaStream_t s, const double* zja_betas = nullptr);
-cudaError_t launch_resample(const double* lw_in, uint64_t n, SmcState* st, double* cum,
-                            double* btot, uint32_t* anc, cudaStream_t s);
 cudaError_t launch_gather(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,
                           int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s);
-cudaError_t launch_max(const double* lw, uint64_t n, SmcState* st, cudaStream_t s);
 cudaError_t launch_generate_schedule(const double* lambda, const double* beta, int knots, int t_new,
                                      double* out, double* scratch, int* err, cudaStream_t s);
 cudaError_t launch_local_barrier(const double* lambda, const double* beta, int knots, double* out,
@@ -69,19 +94,13 @@ cudaError_t launch_ess(const double* lw, uint64_t n, double* out, int* err, cuda
 cudaError_t launch_chunk_major(const LogAcc* in, uint64_t nch, LogAcc* out, cudaStream_t s);
 // sequential fold of [C][a] chunk partials into tot[a] (== fold_chunks_final order)
 cudaError_t launch_fold_chunk_major(const LogAcc* in, uint64_t nch, LogAcc* tot, cudaStream_t s);
-// local block CDF (no-op unless st->resample_now)
-cudaError_t launch_cdf_blocks(const double* lw, uint64_t n, const SmcState* st, double* cum,
-                              double* btot, cudaStream_t s);
-// scan the all-gathered block totals (in place -> exclusive offsets, st->total),
-// shift the local CDF by this shard's offsets, and find every shard's output-slot
-// range: slot_begin[r] = #{m : pos_m <= boff[rank_blk[r]]}
-cudaError_t launch_shard_plan(double* btot_all, uint64_t nblk_all, double* cum, uint64_t n_local,
-                              uint64_t blk_begin, const uint64_t* rank_blk, int world, uint64_t n,
-                              SmcState* st, uint64_t* slot_begin, cudaStream_t s);
-// ancestors of output slots [slot_lo, slot_lo + count) within the local CDF,
-// rows gathered into dst in slot order
-cudaError_t launch_shard_pack(const double* cum, uint64_t n_local, const SmcState* st,
-                              uint64_t slot_lo, uint64_t count, uint64_t n, uint32_t* anc,
-                              uint64_t row_bytes, const void* x, void* dst, int sms, cudaStream_t s);
+// resampling exchange: every rank runs launch_refcdf on the all-gathered log-weights
+// (the global CDF and ancestors a_m, identical on every rank); shard r's output slots are
+// [slot_begin[r], slot_begin[r+1]) = the slots whose ancestor it owns (a_m non-decreasing)
+cudaError_t launch_slot_bounds(const uint32_t* anc, uint64_t n, const uint64_t* shard_p, int world,
+                               const SmcState* st, uint64_t* slot_begin, cudaStream_t s);
+// rows x[anc[i] - p0] for i < count into dst, in slot order
+cudaError_t launch_pack_rows(const uint32_t* anc, uint64_t count, uint64_t p0, uint64_t row_bytes, const void* x,
+                             void* dst, int sms, cudaStream_t s);
 
 }  // namespace asmcdev

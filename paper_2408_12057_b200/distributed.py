@@ -124,11 +124,11 @@ def io_bytes(ts):
 # (6 accumulators x 16 B per 262144 particles) and folds them in chunk order, so
 # ESS, the resampling decision and the uniform are the same on every rank and
 # equal to the single-GPU run.  On a resampling event:
-#   * block CDF totals (8 B per 256 particles) are all-gathered and scanned
-#     redundantly, giving each shard the global offset of its CDF;
-#   * output slot m's ancestor lies in shard r iff cum[p_r - 1] < pos_m <= cum[p_{r+1} - 1],
-#     so shard r computes the ancestors of one contiguous slot range and packs their
-#     rows in slot order;
+#   * the log-weights (8 B per particle) are all-gathered and every rank builds the
+#     reference's sequential CDF over all of them (engine.cpp:61-80, bit for bit, by the
+#     parallel exact scan of csrc/refcdf.cu) and the global ancestors a_m;
+#   * a_m is non-decreasing, so the slots whose ancestor lies in shard r form one
+#     contiguous range; shard r packs those rows in slot order;
 #   * one all-to-all-v moves each packed row to the shard owning its slot.
 # Weight mass that stays balanced across shards keeps most rows on their GPU
 # (the self part of the all-to-all is a local copy).
@@ -197,17 +197,17 @@ class DeviceShard:
 
     def __init__(self, shard, device):
         self.s, self.device = shard, device
-        self.chunks, self.blocks, self.row_bytes = shard.chunks, shard.blocks, shard.row_bytes
+        self.chunks, self.exchange_len, self.row_bytes = shard.chunks, shard.exchange_len, shard.row_bytes
         self.T = shard.T
 
     def step(self, t, partials):
         self.s.step(t, partials.data_ptr())
 
-    def decide(self, t, all_partials, block_totals):
-        return self.s.decide(t, all_partials.data_ptr(), all_partials.shape[0], block_totals.data_ptr())
+    def decide(self, t, all_partials, lw_out):
+        return self.s.decide(t, all_partials.data_ptr(), all_partials.shape[0], lw_out.data_ptr())
 
-    def plan(self, all_block_totals, bounds):
-        return self.s.plan(all_block_totals.data_ptr(), all_block_totals.shape[0], bounds)
+    def plan(self, all_lw, bounds):
+        return self.s.plan(all_lw.data_ptr(), all_lw.shape[0], bounds)
 
     def pack(self, rows):
         self.s.pack(rows.data_ptr())
@@ -220,7 +220,7 @@ class DeviceShard:
 
 
 def run_smc_sharded(shards, ranks, comm, bounds, stats=None, nacc=abi.SHARD_NACC,
-                    chunk=abi.FOLD_CHUNK, block=abi.BLOCK):
+                    chunk=abi.FOLD_CHUNK):
     """Drive local shards (one per process with TorchComm; all of them with
     VirtualComm) through steps 1..T in lockstep; returns each shard's report.
 
@@ -231,18 +231,18 @@ def run_smc_sharded(shards, ranks, comm, bounds, stats=None, nacc=abi.SHARD_NACC
     T = shards[0].T
     dev = shards[0].device
     n_chunks = [chunks_of((bounds[r], bounds[r + 1]), chunk) for r in range(G)]
-    n_blocks = [-(-(bounds[r + 1] - bounds[r]) // block) for r in range(G)]
+    n_ex = [bounds[r + 1] - bounds[r] for r in range(G)]  # log-weights per shard
     parts = [torch.empty((s.chunks, nacc, 2), dtype=torch.float64, device=dev) for s in shards]
-    btots = [torch.empty((max(s.blocks, 1),), dtype=torch.float64, device=dev) for s in shards]
+    lws = [torch.empty((max(s.exchange_len, 1),), dtype=torch.float64, device=dev) for s in shards]
     for t in range(1, T + 1):
         for s, p in zip(shards, parts):
             s.step(t, p)
         allp = comm.allgather(parts, n_chunks)
-        flags = [s.decide(t, a, b) for s, a, b in zip(shards, allp, btots)]
+        flags = [s.decide(t, a, b) for s, a, b in zip(shards, allp, lws)]
         if not flags[0]:
             continue
-        allb = comm.allgather([b[: s.blocks] for s, b in zip(shards, btots)], n_blocks)
-        slots = [s.plan(a, bounds) for s, a in zip(shards, allb)]
+        alll = comm.allgather([b[: s.exchange_len] for s, b in zip(shards, lws)], n_ex)
+        slots = [s.plan(a, bounds) for s, a in zip(shards, alll)]
         splits = exchange_splits(slots[0], bounds)
         sends = []
         for s, r, sl in zip(shards, ranks, slots):
@@ -355,7 +355,7 @@ def run_zja_multi(target, kernel, n, delta_star, seed=0, exec_=None, comm=None, 
     with torch.cuda.device(dev), torch.cuda.stream(stream):
         shards = [capi.ZjaShard(target, kernel, n, bounds[r], bounds[r + 1], seed, round, max_steps, ex) for r in ranks]
         parts = [torch.empty((s.chunks, abi.SHARD_NACC, 2), dtype=torch.float64, device=dev) for s in shards]
-        btots = [torch.empty((max(s.blocks, 1),), dtype=torch.float64, device=dev) for s in shards]
+        lws = [torch.empty((max(s.exchange_len, 1),), dtype=torch.float64, device=dev) for s in shards]
 
         def gathered(local):  # all-gather host partials (chunks, 2, 2) in rank (= chunk) order
             ts = [torch.from_numpy(a).to(dev) for a in local]
@@ -396,7 +396,7 @@ def run_zja_multi(target, kernel, n, delta_star, seed=0, exec_=None, comm=None, 
                 s.set_beta(t, b)
                 s.step(t, p.data_ptr())
             allp = comm.allgather(parts, n_chunks)
-            for s, a, bt in zip(shards, allp, btots):
+            for s, a, bt in zip(shards, allp, lws):  # policy never: no exchange
                 s.decide(t, a.data_ptr(), a.shape[0], bt.data_ptr())
         reps = [s.report(t) for s in shards]
     stream.synchronize()

@@ -6,7 +6,7 @@
   fp32 Philox path;
 * GPU-count invariance: chunk partials of any particle split fold to the same
   bits as the single-launch pass (the virtual-shard mode of SURVEY 4);
-* SSMC fp64 Philox vs the oracle's blocked-CDF restatement (same resampling rule).
+* SSMC fp64 Philox vs the oracle's restatement (the reference's resampling rule).
 """
 import math
 
@@ -144,11 +144,11 @@ def test_chunk_partials_are_shard_invariant():
 
 # ---- SSMC on the device ----------------------------------------------------
 @pytest.mark.parametrize("policy", [abi.POLICY_ALWAYS, abi.POLICY_ADAPTIVE_ESS])
-def test_ssmc_fp64_philox_matches_blocked_restatement(policy):
+def test_ssmc_fp64_philox_matches_restatement(policy):
     rs = oracle.load("restate", PH)
     tg = abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 3)
     betas = np.linspace(0, 1, 11)
-    a = rs.run_smc_blocked(tg, abi.kernel(abi.KERNEL_RWMH), betas, 3000, policy=policy, seed=8, round=1)
+    a = rs.run_smc(tg, abi.kernel(abi.KERNEL_RWMH), betas, 3000, policy=policy, seed=8, round=1)
     b = capi.run_smc(tg, abi.kernel(abi.KERNEL_RWMH), betas, 3000, policy=policy, seed=8, round=1,
                      exec_=abi.execopts(PH, F64))
     assert a["resample_times"] == b["resample_times"]

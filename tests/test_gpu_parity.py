@@ -139,13 +139,15 @@ def test_run_smc_fp64_matches_reference(policy):
 
 
 def test_systematic_resample_bit_exact():
+    """engine.cpp:61-80 for given log-weights and u: the device's ancestors equal the
+    reference rule's (restatement, pinned to the reference in test_oracle.py)."""
     rs = oracle.load("restate")
     g = np.random.default_rng(0)
     for n in (1, 2, 255, 256, 257, 10000, 1 << 20):
         lw = g.normal(0, 3, n)
         for u in (0.0, 0.3, 0.999):
             dev = capi.systematic_resample(lw, u)
-            assert (dev == rs.systematic_resample_blocked(lw, u)).all(), (n, u)
+            assert (dev == rs.systematic_resample_u(lw, u)).all(), (n, u)
 
 
 def test_schedule_bit_exact():

@@ -1,13 +1,13 @@
 """Multi-GPU SSMC host logic (paper_2408_12057_b200/distributed.py run_smc_sharded)
-on CPU: the chunk-partial allgather, the block-total allgather, the slot-range
-rule and the all-to-all-v of resampled rows -- with a stand-in shard whose
-weights and states are deterministic functions of the GLOBAL particle id, so the
-only thing that can differ between world sizes is the exchange itself.
+on CPU: the chunk-partial allgather, the log-weight allgather, the slot-range rule
+and the all-to-all-v of resampled rows -- with a stand-in shard whose weights and
+states are deterministic functions of the GLOBAL particle id, so the only thing that
+can differ between world sizes is the exchange itself.
 
-The property the device path relies on: systematic resampling over shards
-(each shard resolving the output slots whose position falls in its part of the
-CDF, engine.cpp:61-80) picks exactly the ancestors of one global lower_bound,
-and the rows land in slot order on the shard that owns the slot."""
+The property the device path relies on: every rank builds the same global sequential
+CDF (engine.cpp:61-80) from the all-gathered log-weights, the ancestors a_m are
+non-decreasing in m, so the slots whose ancestor lies in shard r are one contiguous
+range, and the rows land in slot order on the shard that owns the slot."""
 import bisect
 import math
 import socket
@@ -17,11 +17,30 @@ import pytest
 
 from paper_2408_12057_b200 import distributed
 
-CHUNK, BLOCK = 64, 8
+CHUNK = 64
 
 
-def pos(m, u, n, total):  # engine.cpp:68-70 operation order (IEEE double, as on device)
-    return ((m + u) / n) * total
+def ref_ancestors(lw, u):
+    """engine.cpp:61-80 in plain Python floats (IEEE double, sequential order)."""
+    n = len(lw)
+    mx, sm = -math.inf, 0.0  # LogAccumulator (logsum.hpp:18-45)
+    for v in lw:
+        if v == -math.inf:
+            continue
+        if v <= mx:
+            sm += math.exp(v - mx)
+        else:
+            sm = sm * math.exp(mx - v) + 1.0
+            mx = v
+    l1 = mx + math.log(sm)
+    out, cum, j = [], math.exp(lw[0] - l1), 0
+    for m in range(n):
+        p = (m + u) / n
+        while cum < p and j + 1 < n:
+            j += 1
+            cum += math.exp(lw[j] - l1)
+        out.append(j)
+    return out
 
 
 class FakeShard:
@@ -33,7 +52,7 @@ class FakeShard:
         self.n, self.p0, self.p1, self.T, self.seed = n, p0, p1, T, seed
         self.nl = p1 - p0
         self.chunks = -(-self.nl // CHUNK)
-        self.blocks = -(-self.nl // BLOCK)
+        self.exchange_len = self.nl
         self.row_bytes = 16
         self.device = "cpu"
         self.state = torch.stack([torch.arange(p0, p1, dtype=torch.float64),
@@ -50,45 +69,20 @@ class FakeShard:
             seg = self.lw[c * CHUNK:(c + 1) * CHUNK]
             partials[c, 0, 0] = max(seg)
 
-    def decide(self, t, allp, btot):
-        self.gmax = float(allp[:, 0, 0].max())
+    def decide(self, t, allp, lw_out):
         self.u = (math.sin(17.0 * t + self.seed) + 1.0) / 2.0 * 0.999
         fire = t % 2 == 0 or t == self.T
         if fire:
             self.resample_times.append(t)
-            self.cum = [0.0] * self.nl
-            for b in range(self.blocks):
-                s = 0.0
-                for j in range(b * BLOCK, min(self.nl, (b + 1) * BLOCK)):
-                    s += math.exp(self.lw[j] - self.gmax)
-                    self.cum[j] = s
-                btot[b] = s
+            for j in range(self.nl):
+                lw_out[j] = self.lw[j]
         return fire
 
-    def plan(self, allb, bounds):
-        vals = [float(v) for v in allb]
-        boff, off = [], 0.0
-        for v in vals:  # cdf_scan_kernel: sequential exclusive scan
-            boff.append(off)
-            off += v
-        total = off
-        b0 = self.p0 // BLOCK
-        self.cum = [c + boff[b0 + j // BLOCK] for j, c in enumerate(self.cum)]
+    def plan(self, all_lw, bounds):
+        self.anc = ref_ancestors([float(v) for v in all_lw], self.u)
         G = len(bounds) - 1
-        slots = [0] * (G + 1)
-        slots[G] = self.n
-        for r in range(1, G):  # shard_bounds_kernel
-            rb = bounds[r] // BLOCK
-            thr = boff[rb] if rb < len(boff) else total
-            lo, hi = 0, self.n
-            while lo < hi:
-                mid = (lo + hi) // 2
-                if pos(mid, self.u, self.n, total) <= thr:
-                    lo = mid + 1
-                else:
-                    hi = mid
-            slots[r] = lo
-        self.total, self.slots = total, slots
+        slots = [bisect.bisect_left(self.anc, bounds[r]) for r in range(G)] + [self.n]
+        self.slots = slots
         self.me = bounds.index(self.p0)
         return slots
 
@@ -96,8 +90,9 @@ class FakeShard:
         lo, hi = self.slots[self.me], self.slots[self.me + 1]
         out = rows.view(self.torch.float64).reshape(-1, 2)
         for i, m in enumerate(range(lo, hi)):
-            j = bisect.bisect_left(self.cum, pos(m, self.u, self.n, self.total))
-            out[i] = self.state[min(j, self.nl - 1)]
+            j = self.anc[m] - self.p0
+            assert 0 <= j < self.nl
+            out[i] = self.state[j]
             out[i, 1] += 1
 
     def accept(self, rows):
@@ -113,33 +108,23 @@ def run(rank, world, n, T, seed, comm=None):
     if comm is None:  # all shards in this process
         shards = [FakeShard(n, bounds[r], bounds[r + 1], T, seed) for r in range(world)]
         reps = distributed.run_smc_sharded(shards, list(range(world)), distributed.VirtualComm(world),
-                                           bounds, chunk=CHUNK, block=BLOCK)
+                                           bounds, chunk=CHUNK)
         return np.concatenate([r["state"] for r in reps]), reps[0]["resample_times"]
     shard = FakeShard(n, bounds[rank], bounds[rank + 1], T, seed)
-    (rep,) = distributed.run_smc_sharded([shard], [rank], comm, bounds, chunk=CHUNK, block=BLOCK)
+    (rep,) = distributed.run_smc_sharded([shard], [rank], comm, bounds, chunk=CHUNK)
     return rep["state"], rep["resample_times"]
 
 
 def global_reference(n, T, seed):
-    """Single-array systematic resampling with the blocked CDF (no shards at all)."""
+    """Single-array systematic resampling, the reference rule (no shards at all)."""
     state = np.stack([np.arange(n, dtype=np.float64), np.zeros(n)], 1)
     lw = np.zeros(n)
     for t in range(1, T + 1):
         lw = lw + np.array([3.0 * math.sin(0.731 * x + 1.37 * t + seed) for x in state[:, 0]])
         if not (t % 2 == 0 or t == T):
             continue
-        gmax = lw.max()
-        cum, off = np.zeros(n), 0.0
-        for b in range(-(-n // BLOCK)):
-            s = 0.0
-            for j in range(b * BLOCK, min(n, (b + 1) * BLOCK)):
-                s += math.exp(lw[j] - gmax)
-                cum[j] = s
-            for j in range(b * BLOCK, min(n, (b + 1) * BLOCK)):
-                cum[j] = cum[j] + off
-            off += s
         u = (math.sin(17.0 * t + seed) + 1.0) / 2.0 * 0.999
-        anc = [min(bisect.bisect_left(list(cum), pos(m, u, n, off)), n - 1) for m in range(n)]
+        anc = ref_ancestors([float(v) for v in lw], u)
         state = state[anc].copy()
         state[:, 1] += 1
         lw = np.zeros(n)
