@@ -349,6 +349,32 @@ int check_smem(Layout L, uint64_t d, int rows, int nacc) {
   return 0;
 }
 
+// Long-T SAIS (drivers.cpp:86-146 has no T cap): the shared-memory pass keeps per-warp
+// step accumulators for the steps of ONE launch, so a round whose T would lower the
+// pass's occupancy (or overflow 227 KB) runs in t-tiles of this many steps, the particle
+// rows parked in HBM between tiles (8d + 8 bytes per particle per tile).
+int sais_tile_rows(Layout L, uint64_t d, int T) {
+  if (L.lanes == 1 || T < 2) return T;  // one-lane pass: partials in global memory, no cap
+  if (const char* e = std::getenv("ASMC_SAIS_TILE")) {  // test hook: force the tile length
+    const int f = std::atoi(e);
+    if (f >= 1) return f < T ? f : T;
+  }
+  auto occ = [&](int rows) {
+    const size_t b = smem_pass_bytes(L.lanes, d, rows - 1, 4, g_row_words) + 1024;
+    const int o = (int)((228 * 1024) / b);
+    return o < 3 ? o : 3;  // the pass's register budget allows 3 CTAs/SM
+  };
+  const int o1 = occ(1);
+  if (occ(T) >= o1) return T;
+  int lo = 1, hi = T;  // largest rows with the same occupancy as one step
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (occ(mid) >= o1) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 // Live per-launch timing of the particle pass (bench.py roofline): events on
 // the launching stream around each pass, plus its algorithmic normal draws.
 struct ProfRec {
@@ -451,7 +477,46 @@ struct RoundBufs {
 // One SAIS round over particles [0, n): fused pass + fold + report.
 struct SaisWork {
   DBuf<LogAcc> part, chunk, tot;
+  DBuf<char> xs;  // long-T tiles: particle rows between tiles
+  DBuf<void*> xbuf;
+  DBuf<int> xcur;
+  DBuf<double> lw;
 };
+
+// The SAIS pass over steps 1..T for particles [p_begin, p_begin + n_local): one launch,
+// or t-tiles (sais_tile_rows) with the particle rows in HBM between them.  Either way
+// the same per-(block, step) partials, bit for bit (tests/test_gpu_long_t.py).
+int launch_sais_pass(DevCtx* C, const asmc_exec& ex, Layout L, PassArgs A, uint64_t nblk, int T,
+                     DBuf<char>& xs, DBuf<void*>& xbuf, DBuf<int>& xcur, DBuf<double>& lw) {
+  const int tile = sais_tile_rows(L, A.tg.dim, T);
+  A.T = T;
+  A.row_base = 0;
+  if (tile >= T) {
+    A.t_begin = 1;
+    A.t_end = T;
+    A.mode = kModeSais;
+    LCH(launch_pass(ex, L, A, nblk, C->stream));
+    return 0;
+  }
+  const size_t real = ex.precision == ASMC_PREC_FP64 ? sizeof(double) : sizeof(float);
+  TRY(xs.alloc(A.n_local * A.tg.dim * real, C->stream));
+  TRY(xbuf.alloc(2, C->stream));
+  TRY(xcur.alloc(1, C->stream));
+  TRY(lw.alloc(A.n_local, C->stream));
+  void* ptrs[2] = {xs.p, xs.p};
+  CU(cudaMemcpyAsync(xbuf.p, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, C->stream));
+  CU(cudaMemsetAsync(xcur.p, 0, sizeof(int), C->stream));
+  A.xbuf = xbuf.p;
+  A.xcur = xcur.p;
+  A.lw = lw.p;
+  for (int t0 = 1; t0 <= T; t0 += tile) {
+    A.t_begin = t0;
+    A.t_end = t0 + tile - 1 < T ? t0 + tile - 1 : T;
+    A.mode = t0 == 1 ? kModeSaisFirst : kModeSaisNext;
+    LCH(launch_pass(ex, L, A, nblk, C->stream));
+  }
+  return 0;
+}
 
 int enqueue_sais_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs& base,
                        const double* d_betas, int T, uint64_t n, uint64_t seed, uint64_t round,
@@ -463,11 +528,6 @@ int enqueue_sais_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs&
   TRY(W.tot.alloc((size_t)(T + 1) * kNAcc, C->stream));
   PassArgs A = base;
   A.betas = d_betas;
-  A.T = T;
-  A.t_begin = 1;
-  A.t_end = T;
-  A.mode = kModeSais;
-  A.row_base = 0;
   A.n = n;
   A.p_begin = 0;
   A.n_local = n;
@@ -476,7 +536,7 @@ int enqueue_sais_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs&
   A.part = W.part.p;
   A.part_stride = nblk;
   A.err = d_err;
-  LCH(launch_pass(ex, L, A, nblk, C->stream));
+  TRY(launch_sais_pass(C, ex, L, A, nblk, T, W.xs, W.xbuf, W.xcur, W.lw));
   LCH(launch_fold(ex.precision == ASMC_PREC_FP64, W.part.p, nblk, nblk, 1, T, 4, W.chunk.p, W.tot.p,
                   C->stream));
   LCH(launch_sais_report(W.tot.p, T, n, d_rd, C->stream));
@@ -949,7 +1009,7 @@ int asmc_run_sais_single(const asmc_target_desc* target, const asmc_kernel_desc*
   if (target->kind == ASMC_TARGET_ISING)
     return run_is_single(target, kernel, betas, T, n, ASMC_POLICY_NEVER, 0.5, seed, round, ex, out, false);
   Layout L;
-  TRY(choose_layout(ex, kernel->kind, target->dim, &L, T, 4));
+  TRY(choose_layout(ex, kernel->kind, target->dim, &L, 1, 4));  // long T runs in t-tiles
   DevCtx* C;
   TRY(get_ctx(ex.device, &C, ex.stream));
   const double t0 = now_s();
@@ -1060,7 +1120,7 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
   for (int k = 1; k < rounds; ++k) TRY(asmc_budget(ns[k - 1], ts[k - 1], target->dim, memory_cap, mode, &ns[k], &ts[k]));
   int tmax = 0;
   for (int k = 0; k < rounds; ++k) tmax = ts[k] > tmax ? ts[k] : tmax;
-  TRY(check_smem(L, target->dim, mode == ASMC_MODE_SAIS ? tmax : 1, mode == ASMC_MODE_SAIS ? 4 : kNAcc));
+  TRY(check_smem(L, target->dim, 1, mode == ASMC_MODE_SAIS ? 4 : kNAcc));  // SAIS: long T in t-tiles
   if (tmax > out->max_steps) return fail(ASMC_ERR_INVALID_ARGUMENT, "max_steps too small (%d needed)", tmax);
   if (mode == ASMC_MODE_SSMC)
     for (int k = 0; k < rounds; ++k)
@@ -1175,7 +1235,7 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
   if (target->kind == ASMC_TARGET_LOGISTIC || target->kind == ASMC_TARGET_ISING)
     return stepouter_partials(target, kernel, betas, T, p_begin, p_end, seed, round, ex, partials);
   Layout L;
-  TRY(choose_layout(ex, kernel->kind, target->dim, &L, T, 4));
+  TRY(choose_layout(ex, kernel->kind, target->dim, &L, 1, 4));  // long T runs in t-tiles
   DevCtx* C;
   TRY(get_ctx(ex.device, &C, ex.stream));
   const uint64_t nloc = p_end - p_begin, nblk = nblocks(nloc);
@@ -1192,10 +1252,6 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
   CU(cudaMemsetAsync(err.p, 0, sizeof(int), C->stream));
   PassArgs A = base_args(target, kernel);
   A.betas = d_betas.p;
-  A.T = T;
-  A.t_begin = 1;
-  A.t_end = T;
-  A.mode = kModeSais;
   A.n = n;
   A.p_begin = p_begin;
   A.n_local = nloc;
@@ -1204,7 +1260,11 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
   A.part = part.p;
   A.part_stride = nblk;
   A.err = err.p;
-  LCH(launch_pass(ex, L, A, nblk, C->stream));
+  DBuf<char> xs;
+  DBuf<void*> xbuf;
+  DBuf<int> xcur;
+  DBuf<double> lwb;
+  TRY(launch_sais_pass(C, ex, L, A, nblk, T, xs, xbuf, xcur, lwb));
   LCH(launch_fold_chunks(part.p, nblk, nblk, 1, T, 4, nch, chunk.p, C->stream));
   std::vector<LogAcc> h((size_t)(T + 1) * kNAcc * nch);
   CU(cudaMemcpyAsync(h.data(), chunk.p, h.size() * sizeof(LogAcc), cudaMemcpyDeviceToHost, C->stream));
@@ -1344,7 +1404,23 @@ static int resample_common(const double* log_w, uint64_t n, double u, int32_t de
   CU(cudaMemcpyAsync(lw.p, log_w, sizeof(double) * n, cudaMemcpyHostToDevice, C->stream));
   RefCdfWork w;
   refcdf_work_carve(work.p, n, &w);
+  DBuf<unsigned long long> prof;  // ASMC_REFCDF_PROF=1: per-phase %globaltimer stamps to stderr
+  const bool profile = std::getenv("ASMC_REFCDF_PROF") != nullptr;
+  if (profile) {
+    TRY(prof.alloc(16, C->stream));
+    CU(cudaMemsetAsync(prof.p, 0, 16 * sizeof(unsigned long long), C->stream));
+    w.prof = prof.p;
+  }
   LCH(launch_refcdf(lw.p, n, st.p, 0, &w, cum.p, anc.p, what, C->sms, C->stream));
+  if (profile) {
+    unsigned long long ts[16];
+    CU(cudaMemcpyAsync(ts, prof.p, sizeof ts, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaStreamSynchronize(C->stream));
+    std::fprintf(stderr, "refcdf n=%llu phases(us):", (unsigned long long)n);
+    for (int i = 1; i < 13; ++i)
+      if (ts[i]) std::fprintf(stderr, " %d:%.1f", i, (ts[i] - ts[0]) * 1e-3);
+    std::fprintf(stderr, " replays lse=%llu cdf=%llu\n", ts[14], ts[15]);
+  }
   if (ancestors && what == 1)
     CU(cudaMemcpyAsync(ancestors, anc.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, C->stream));
   if (cum_out && what >= 0)

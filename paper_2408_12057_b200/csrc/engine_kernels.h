@@ -43,15 +43,12 @@ struct RefCdfWork {
   double* ba;      // approximate block composite s -> ba s + bb
   double* bb;
   double* sstart;  // approximate running value at each block start (nblk + 1)
-  unsigned long long* tot;  // exact integer total of a stable block at its binade
-  unsigned long long* pw;   // exclusive prefix of the totals inside the block's run
-  double* shead;   // exact running value at each run's first block
+  unsigned long long* tot;     // exact integer total of a stable block at its binade
+  unsigned long long* bstart;  // exact start of each stable block, in units of its binade
   int* kb;         // binade of a stable block, or unstable
-  int* hid;        // run index of each block
-  int* heads;      // first block of each run (+ sentinel)
   double* gmax;    // max log-weight
   double* l1;      // logsumexp of the log-weights (the reference's bits)
-  int* nheads;
+  unsigned long long* prof;  // optional: %globaltimer at each phase end (16 entries)
 };
 size_t refcdf_work_bytes(uint64_t n);
 void refcdf_work_carve(void* base, uint64_t n, RefCdfWork* w);

@@ -31,7 +31,7 @@ static cudaError_t go(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
 #if ASMC_PREC == 32
 template <int G, bool kHmc>
 static cudaError_t go_smem_k(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
-  const int nacc = A.mode == kModeSmcStep ? kNAcc : 4;
+  const int nacc = mode_nacc(A.mode);
   const int rows = A.t_end - A.t_begin + 1 > 0 ? A.t_end - A.t_begin + 1 : 1;
   const size_t bytes = smem_pass_bytes(G, A.tg.dim, rows - 1, nacc, RowWords<Tgt, kHmc>::value);
   static bool configured = false;

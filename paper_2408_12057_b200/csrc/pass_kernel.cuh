@@ -31,7 +31,18 @@ namespace asmcdev {
 
 constexpr double kTwoPi = 6.283185307179586476925286766559;
 
-enum PassMode : int { kModeSais = 0, kModeSmcInit = 1, kModeSmcStep = 2, kModeTraj = 3 };
+// kModeSaisFirst / kModeSaisNext: long-T SAIS in t-tiles (drivers.cpp:86-146 has no T
+// cap): the first tile draws the particle and runs steps t_begin..t_end, later tiles
+// reload it from the state rows; every tile stores it back.  Same per-(block, step)
+// partials as one kModeSais launch over all T steps.
+enum PassMode : int {
+  kModeSais = 0, kModeSmcInit = 1, kModeSmcStep = 2, kModeTraj = 3, kModeSaisFirst = 4, kModeSaisNext = 5
+};
+__host__ __device__ __forceinline__ bool mode_loads(int m) { return m == kModeSmcStep || m == kModeSaisNext; }
+__host__ __device__ __forceinline__ bool mode_stores(int m) {
+  return m == kModeSmcStep || m == kModeSaisFirst || m == kModeSaisNext;
+}
+__host__ __device__ __forceinline__ int mode_nacc(int m) { return m == kModeSmcStep ? 6 : 4; }
 
 struct KernelCfg {
   int kind;  // ASMC_KERNEL_*
@@ -573,7 +584,7 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
   const int tid = threadIdx.x, g = tid / G, lane = tid % G;
   const int d = (int)A.tg.dim;
   const uint64_t blk = blockIdx.x;
-  const int nacc = (A.mode == kModeSmcStep) ? kNAcc : 4;
+  const int nacc = mode_nacc(A.mode);
   if (A.err && *(volatile int*)A.err) return;  // an earlier step failed: skip the work
 
   __shared__ double s_lw[NG], s_lg[NG], s_post[NG];
@@ -592,7 +603,7 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
     double lw = 0.0;
 
     // ---- init / load -----------------------------------------------------
-    if (A.mode == kModeSmcStep) {
+    if (mode_loads(A.mode)) {
       const Real* xs = reinterpret_cast<const Real*>(A.xbuf[*A.xcur]) + local * (uint64_t)d;
 #pragma unroll(KMAX <= 64 ? KMAX : 1)
       for (int k = 0; k < KMAX; ++k) {
@@ -681,7 +692,7 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
       if (tid < nacc) A.part[((size_t)(t - A.row_base) * kNAcc + tid) * A.part_stride + blk] = s_dst[tid];
     }
 
-    if (A.mode == kModeSmcStep && active) {
+    if (mode_stores(A.mode) && active) {
       Real* xs = reinterpret_cast<Real*>(A.xbuf[*A.xcur]) + local * (uint64_t)d;
 #pragma unroll(KMAX <= 64 ? KMAX : 1)
       for (int k = 0; k < KMAX; ++k) {

@@ -532,7 +532,8 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
   const int d = (int)A.tg.dim;
   const int nq = (d + 3) >> 2;
   const uint64_t blk = blockIdx.x;
-  const int nacc = (A.mode == kModeSmcStep) ? kNAcc : 4;
+  const int nacc = mode_nacc(A.mode);
+  const bool loads = mode_loads(A.mode);
   if (A.err && *(volatile int*)A.err) return;
 
   extern __shared__ __align__(16) unsigned char smem[];
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
   constexpr bool kPre = G == 4 && Tgt::kCacheV && !kHmc;
   constexpr int kPQ = kPre ? 8 : 1;  // quads per lane held (d <= 128)
   float4 pre[kPQ];
-  const bool use_pre = kPre && A.mode == kModeSmcStep && (d & 3) == 0 && nq <= G * kPQ;
+  const bool use_pre = kPre && loads && (d & 3) == 0 && nq <= G * kPQ;
   auto load_pre = [&](uint64_t loc) {
     const bool act = loc < A.n_local;
     const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A.xbuf[*A.xcur]) +
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
   for (int r = 0; r < G; ++r) {
     const uint64_t local = blk * kBlock + (uint64_t)r * NG + g;
     const bool active = local < A.n_local;
-    if (A.mode == kModeSmcStep && tid == 0 && r + 1 < G) {
+    if (loads && tid == 0 && r + 1 < G) {
       // the next round's NG particle rows are one contiguous span of the state buffer:
       // one bulk L2 prefetch now, so their loads a particle-iteration later hit L2
       const uint64_t nl = blk * kBlock + (uint64_t)(r + 1) * NG;
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
     const uint64_t pid = A.mode == kModeTraj ? (active ? A.pids[local] : 0) : A.p_begin + local;
     double lw = 0.0;
     float vs = 0.f;  // this lane's sum of vpart(x) (SmemOps::vsum)
-    if (A.mode == kModeSmcStep && use_pre) {
+    if (loads && use_pre) {
 #pragma unroll
       for (int i = 0; i < kPQ; ++i) {
         const int q = lane + G * i;
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
       lw = active ? A.lw[local] : 0.0;
       __syncwarp();
       vs = Ops::refresh_v(A.tg, lane, d, xq);  // the prefetch path is cached-target only
-    } else if (A.mode == kModeSmcStep) {
+    } else if (loads) {
       const float4* src = reinterpret_cast<const float4*>(
           reinterpret_cast<const float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d);
       const bool vec = (d & 3) == 0;
@@ -661,7 +662,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
       }
       warp_fold<G>(pre, lg, lw, active, nacc, myacc + (size_t)(t - A.t_begin) * nacc);
     }
-    if (A.mode == kModeSmcStep && active) {
+    if (mode_stores(A.mode) && active) {
       float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(A.xbuf[*A.xcur]) +
                                               local * (uint64_t)d);
       if ((d & 3) == 0) {

@@ -250,33 +250,43 @@ __device__ void phase_block_affine(const Args& A, int mode, double l1, double* s
   (void)ish;
 }
 
-// P3 (CTA 0): approximate running value at every block start: sstart[b] (b = 0..nblk)
-__device__ void phase_scan_affine(const Args& A, Aff* tile) {
+// P3 (CTA 0): approximate running value at every block start: sstart[b] (b = 0..nblk).
+// Tile of 1024 blocks, thread t composes its 4 consecutive maps, warp shuffle scan of
+// the composites, warps in order.
+__device__ void phase_scan_affine(const Args& A, Aff* wsh) {
+  const int ln = threadIdx.x & 31, w = threadIdx.x >> 5;
   double carry = 0.0;  // both chains start from s = 0 (logsum.hpp:47-48, engine.cpp:69)
+  if (threadIdx.x == 0) A.w.sstart[0] = 0.0;
   for (uint64_t t0 = 0; t0 < A.nblk; t0 += kTile) {
     const int m = (int)min((uint64_t)kTile, A.nblk - t0);
-    for (int i = threadIdx.x; i < kTile; i += kT)
-      tile[i] = i < m ? Aff{A.w.ba[t0 + i], A.w.bb[t0 + i]} : Aff{1.0, 0.0};
+    Aff f[4], c{1.0, 0.0};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * threadIdx.x + e;
+      f[e] = i < m ? Aff{A.w.ba[t0 + i], A.w.bb[t0 + i]} : Aff{1.0, 0.0};
+      c = aff_then(c, f[e]);
+    }
+    Aff inc = c;  // inclusive over lanes <= ln
+    for (int o = 1; o < 32; o <<= 1) {
+      const Aff up{__shfl_up_sync(0xffffffffu, inc.a, o), __shfl_up_sync(0xffffffffu, inc.b, o)};
+      if (ln >= o) inc = aff_then(up, inc);
+    }
+    if (ln == 31) wsh[w] = inc;
     __syncthreads();
-    for (int o = 1; o < kTile; o <<= 1) {  // Hillis-Steele inclusive scan
-      Aff nv[4];
+    Aff pre{1.0, 0.0};
+    for (int v = 0; v < w; ++v) pre = aff_then(pre, wsh[v]);
+    const Aff lup{__shfl_up_sync(0xffffffffu, inc.a, 1), __shfl_up_sync(0xffffffffu, inc.b, 1)};
+    if (ln > 0) pre = aff_then(pre, lup);
+    double sv = __fma_rn(pre.a, carry, pre.b);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int i = threadIdx.x + e * kT;
-        nv[e] = i >= o ? aff_then(tile[i - o], tile[i]) : tile[i];
-      }
-      __syncthreads();
-#pragma unroll
-      for (int e = 0; e < 4; ++e) tile[threadIdx.x + e * kT] = nv[e];
-      __syncthreads();
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * threadIdx.x + e;
+      sv = __fma_rn(f[e].a, sv, f[e].b);
+      if (i < m) A.w.sstart[t0 + i + 1] = sv;
     }
-    for (int i = threadIdx.x; i < m; i += kT) {
-      const Aff f = tile[i];
-      A.w.sstart[t0 + i + 1] = __fma_rn(f.a, carry, f.b);
-    }
-    if (t0 == 0 && threadIdx.x == 0) A.w.sstart[0] = 0.0;
-    const Aff last = tile[m - 1];
-    carry = __fma_rn(last.a, carry, last.b);
+    Aff tot{1.0, 0.0};
+    for (int v = 0; v < kT / 32; ++v) tot = aff_then(tot, wsh[v]);
+    carry = __fma_rn(tot.a, carry, tot.b);
     __syncthreads();
   }
 }
@@ -311,171 +321,187 @@ __device__ void phase_classify(const Args& A, int mode, double l1, double* sh, u
   }
 }
 
-// P5 (CTA 0): runs.  A block starts a run when it is unstable, follows an unstable
-// block, or changes binade (unstable blocks are runs of one).  hid[b] = its run's index;
-// heads[h] = first block of run h (heads[H] = nblk); pw[b] = exclusive prefix of the
-// integer totals inside b's run.
-__device__ __forceinline__ int run_head(const Args& A, uint64_t b) {
-  const int k = A.w.kb[b];
-  return (b == 0) || k == kUnstable || A.w.kb[b - 1] == kUnstable || A.w.kb[b - 1] != k;
+// ---- the exact walk (CTA 0) ----------------------------------------------------
+// Scans of 4 consecutive entries per thread (tile of 1024): exclusive prefix sums.
+__device__ __forceinline__ unsigned long long scan4_u64(unsigned long long v[4], unsigned long long ex[4],
+                                                        unsigned long long* wsh) {
+  const int ln = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned long long c = v[0] + v[1] + v[2] + v[3];
+  unsigned long long inc = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (ln >= o) inc += t;
+  }
+  __syncthreads();
+  if (ln == 31) wsh[w] = inc;
+  __syncthreads();
+  unsigned long long pre = inc - c, tot = 0;
+  for (int i = 0; i < kT / 32; ++i) {
+    if (i < w) pre += wsh[i];
+    tot += wsh[i];
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    ex[e] = pre;
+    pre += v[e];
+  }
+  return tot;
 }
 
-__device__ void phase_runs(const Args& A, int* fbuf, unsigned long long* vbuf, int* sh_i,
-                           unsigned long long* sh_u) {
-  int hcarry = 0;                 // runs started before this tile
-  unsigned long long vcarry = 0;  // inclusive total of the open run at the tile's end
-  for (uint64_t t0 = 0; t0 < A.nblk; t0 += kTile) {
-    const int m = (int)min((uint64_t)kTile, A.nblk - t0);
-    // (a) segmented inclusive scan of (head, total): (fl,vl).(fr,vr) = (fl|fr, fr ? vr : vl+vr)
-    for (int i = threadIdx.x; i < kTile; i += kT) {
-      const uint64_t b = t0 + i;
-      fbuf[i] = i < m ? run_head(A, b) : 1;
-      vbuf[i] = (i < m && A.w.kb[b] != kUnstable) ? A.w.tot[b] : 0ull;
-    }
-    __syncthreads();
-    for (int o = 1; o < kTile; o <<= 1) {
-      int nf[4];
-      unsigned long long nv[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int i = threadIdx.x + e * kT;
-        nf[e] = fbuf[i];
-        nv[e] = vbuf[i];
-        if (i >= o) {
-          if (!nf[e]) nv[e] += vbuf[i - o];
-          nf[e] |= fbuf[i - o];
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        fbuf[threadIdx.x + e * kT] = nf[e];
-        vbuf[threadIdx.x + e * kT] = nv[e];
-      }
-      __syncthreads();
-    }
-    for (int i = threadIdx.x; i < m; i += kT) {
-      const uint64_t b = t0 + i;
-      const unsigned long long incl = vbuf[i] + (fbuf[i] ? 0ull : vcarry);
-      A.w.pw[b] = incl - (A.w.kb[b] != kUnstable ? A.w.tot[b] : 0ull);
-      if (i == m - 1) sh_u[0] = incl;
-    }
-    __syncthreads();
-    // (b) run index: inclusive count of heads
-    for (int i = threadIdx.x; i < kTile; i += kT) fbuf[i] = i < m ? run_head(A, t0 + i) : 0;
-    __syncthreads();
-    for (int o = 1; o < kTile; o <<= 1) {
-      int nv[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int i = threadIdx.x + e * kT;
-        nv[e] = fbuf[i] + (i >= o ? fbuf[i - o] : 0);
-      }
-      __syncthreads();
-#pragma unroll
-      for (int e = 0; e < 4; ++e) fbuf[threadIdx.x + e * kT] = nv[e];
-      __syncthreads();
-    }
-    for (int i = threadIdx.x; i < m; i += kT) {
-      const uint64_t b = t0 + i;
-      const int h = hcarry + fbuf[i] - 1;
-      A.w.hid[b] = h;
-      if (run_head(A, b)) A.w.heads[h] = (int)b;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) sh_i[0] = hcarry + fbuf[m - 1];
-    __syncthreads();
-    hcarry = sh_i[0];
-    vcarry = sh_u[0];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    A.w.heads[hcarry] = (int)A.nblk;
-    A.w.nheads[0] = hcarry;
-  }
-}
+struct WalkSmem {
+  int kb[kTile];
+  int hid[kTile];                // run (head) index of each block of the tile
+  int heads[kTile + 1];          // first block of each run in the tile (+ m)
+  unsigned long long P[kTile + 1];  // exclusive prefix of the stable totals in the tile
+  unsigned long long u0[kTile];  // exact start units of each stable run
+  unsigned long long wsh[kT / 32];
+  double vbuf[kT];
+  unsigned char fbuf[kT];
+  double s;
+  int nh, stop, stop_end, replays;
+};
 
-// Replays block b element by element from the exact value s (thread 0's), the
-// reference's own operations; CDF mode stores cum.  Returns the new s (thread 0).
-__device__ double replay_block(const Args& A, int mode, uint64_t b, double l1, double s, double* sh,
-                               double* vbuf, unsigned char* fbuf) {
+// Replays block b element by element from the exact value W.s, with the reference's own
+// fp64 operations; CDF mode stores cum.  Leaves the new value in W.s.
+__device__ void replay_block(const Args& A, int mode, uint64_t b, double l1, double* sh, WalkSmem& W) {
   const Op op = block_op(A, mode, b, l1, sh);
-  vbuf[threadIdx.x] = op.v;
-  fbuf[threadIdx.x] = op.rescale ? 1 : 0;
+  W.vbuf[threadIdx.x] = op.v;
+  W.fbuf[threadIdx.x] = op.rescale ? 1 : 0;
   __syncthreads();
   if (threadIdx.x == 0) {
     const int m = (int)min((uint64_t)kT, A.n - b * kT);
-    for (int i = 0; i < m; ++i) {
-      if (fbuf[i]) s = __dadd_rn(__dmul_rn(s, vbuf[i]), 1.0);
-      else s = __dadd_rn(s, vbuf[i]);
-      vbuf[i] = s;
+    double s = W.s;
+    for (int i0 = 0; i0 < m; i0 += 8) {  // batches of 8: the loads are off the add chain
+      double v[8];
+      unsigned char f[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        v[e] = W.vbuf[i0 + e];
+        f[e] = W.fbuf[i0 + e];
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (i0 + e < m) {
+          s = f[e] ? __dadd_rn(__dmul_rn(s, v[e]), 1.0) : __dadd_rn(s, v[e]);
+          v[e] = s;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) W.vbuf[i0 + e] = v[e];
     }
+    W.s = s;
   }
   __syncthreads();
   if (mode == kModeCdf) {
     const uint64_t j = b * kT + threadIdx.x;
-    if (j < A.n) A.cum[j] = vbuf[threadIdx.x];
+    if (j < A.n) A.cum[j] = W.vbuf[threadIdx.x];
   }
-  __syncthreads();
-  return s;
 }
 
-// P6 (CTA 0): the exact walk over runs.  Stable run: verify the EXACT start value lies in
-// the run's binade and the run's integer total keeps it there -> one integer add; else
-// (never expected) replay the run's blocks.  Unstable block: replay.  shead[b] = exact
-// value before each stable run's first block.  Returns the final exact value.
-__device__ double phase_walk(const Args& A, int mode, double l1, double* sh, double* vbuf,
-                             unsigned char* fbuf, int* hb) {
-  __shared__ double s_sh;
-  __shared__ int flag_sh;
-  double s = 0.0;
-  const int H = A.w.nheads[0];
-  for (int h0 = 0; h0 < H; h0 += kTile) {
-    const int hm = min(kTile, H - h0);
-    for (int i = threadIdx.x; i <= hm; i += kT) hb[i] = A.w.heads[h0 + i];
+// P5 (CTA 0): walk the blocks in order with the EXACT running value.  Per tile of 1024
+// blocks: runs = maximal spans of stable blocks at one binade (unstable blocks are runs of
+// one; a tile start always starts a run).  A stable run is one integer add after checking
+// that the exact start lies in the run's binade and the run's total keeps it there; an
+// unstable block (or a run failing the check -- not expected) is replayed.  CDF mode
+// leaves bstart[b] = exact start units of every stable block for P6.
+__device__ double phase_walk(const Args& A, int mode, double l1, double* sh, WalkSmem& W) {
+  if (threadIdx.x == 0) {
+    W.s = 0.0;
+    W.replays = 0;
+  }
+  for (uint64_t t0 = 0; t0 < A.nblk; t0 += kTile) {
+    const int m = (int)min((uint64_t)kTile, A.nblk - t0);
+    int k4[4], h4[4];
+    unsigned long long v4[4], p4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * threadIdx.x + e;
+      k4[e] = i < m ? A.w.kb[t0 + i] : kUnstable;
+      v4[e] = (i < m && k4[e] != kUnstable) ? A.w.tot[t0 + i] : 0ull;
+      if (i < m) W.kb[i] = k4[e];
+    }
     __syncthreads();
-    for (int i = 0; i < hm; ++i) {
-      const int b = hb[i], bend = hb[i + 1];
-      const int k = A.w.kb[b];
-      if (threadIdx.x == 0) {
-        int ok = 0;
-        if (k != kUnstable) {
-          const unsigned long long u0 = sum_units(s);
-          const unsigned long long total = A.w.pw[bend - 1] + A.w.tot[bend - 1];
-          if (binade(s) == k && (k == -1022 || u0 >= kTwo52) && u0 + total < kTwo53) {
-            A.w.shead[b] = s;
-            s = units_value(u0 + total, k);
-            ok = 1;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * threadIdx.x + e;
+      h4[e] = i < m && (i == 0 || k4[e] == kUnstable || W.kb[i - 1] == kUnstable || W.kb[i - 1] != k4[e]);
+    }
+    const unsigned long long tot = scan4_u64(v4, p4, W.wsh);
+    unsigned long long hv[4], hx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) hv[e] = (unsigned long long)h4[e];
+    const unsigned long long nh = scan4_u64(hv, hx, W.wsh);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * threadIdx.x + e;
+      if (i < m) {
+        W.P[i] = p4[e];
+        W.hid[i] = (int)(hx[e] + hv[e]) - 1;
+        if (h4[e]) W.heads[hx[e]] = i;
+      }
+    }
+    if (threadIdx.x == 0) {
+      W.P[m] = tot;
+      W.heads[nh] = m;
+      W.nh = (int)nh;
+      W.stop = 0;
+    }
+    __syncthreads();
+    int h = 0;
+    while (h < W.nh) {  // uniform
+      if (threadIdx.x == 0) {  // run ahead over the stable runs, stop at the first replay
+        double s = W.s;
+        int stop = W.nh, stop_end = 0;
+        for (; h < W.nh; ++h) {
+          const int b0 = W.heads[h], b1 = W.heads[h + 1], k = W.kb[b0];
+          if (k != kUnstable) {
+            const unsigned long long u0 = sum_units(s), total = W.P[b1] - W.P[b0];
+            if (binade(s) == k && u0 + total < kTwo53) {
+              W.u0[h] = u0;
+              s = units_value(u0 + total, k);
+              continue;
+            }
           }
+          stop = h;
+          stop_end = b1;
+          break;
         }
-        flag_sh = ok;
-        s_sh = s;
+        W.s = s;
+        W.stop = stop;
+        W.stop_end = stop_end;
       }
       __syncthreads();
-      if (!flag_sh) {
-        for (int bb = b; bb < bend; ++bb) {
-          s = replay_block(A, mode, (uint64_t)bb, l1, s_sh, sh, vbuf, fbuf);
-          if (threadIdx.x == 0) {
-            A.w.kb[bb] = kUnstable;  // cum (CDF) written by the replay
-            s_sh = s;
-          }
-          __syncthreads();
+      h = W.stop;
+      if (h >= W.nh) break;
+      for (int i = W.heads[h]; i < W.stop_end; ++i) {
+        replay_block(A, mode, t0 + i, l1, sh, W);
+        if (threadIdx.x == 0) {
+          ++W.replays;
+          W.kb[i] = kUnstable;
+          A.w.kb[t0 + i] = kUnstable;  // P6 skips it: the replay wrote its cum
         }
       }
-      s = s_sh;
+      ++h;
       __syncthreads();
     }
+    if (mode == kModeCdf) {
+      for (int i = threadIdx.x; i < m; i += kT) {
+        if (W.kb[i] == kUnstable) continue;
+        const int hh = W.hid[i];
+        A.w.bstart[t0 + i] = W.u0[hh] + (W.P[i] - W.P[W.heads[hh]]);
+      }
+    }
+    __syncthreads();
   }
-  return s;
+  return W.s;
 }
 
-// P7 (grid, CDF): cum of the stable blocks from their run's exact start value
+// P6 (grid, CDF): cum of the stable blocks from their exact start units
 __device__ void phase_materialize(const Args& A, double l1, double* sh, unsigned long long* ush) {
   for (uint64_t b = blockIdx.x; b < A.nblk; b += gridDim.x) {
     const int k = A.w.kb[b];
     if (k == kUnstable) continue;  // uniform per CTA
-    const int hb = A.w.heads[A.w.hid[b]];
-    const unsigned long long u0 = sum_units(A.w.shead[hb]) + A.w.pw[b];
+    const unsigned long long u0 = A.w.bstart[b];
     const Op op = block_op(A, kModeCdf, b, l1, sh);
     bool tie = false, sat = false;
     const unsigned long long r = add_units(op.v, k, tie, sat);
@@ -486,19 +512,50 @@ __device__ void phase_materialize(const Args& A, double l1, double* sh, unsigned
   }
 }
 
-// P8 (grid): a_m = first j with !(cum_j < pos_m), clamped (engine.cpp:68-76)
+// P7 (grid): a_m = first j with !(cum_j < pos_m), clamped (engine.cpp:68-76).  A thread
+// takes 8 consecutive slots: one binary search, then the reference's own forward walk.
 __device__ void phase_ancestors(const Args& A, double u) {
+  constexpr int kS = 8;
   const double dn = (double)A.n;
-  for (uint64_t m = (uint64_t)blockIdx.x * kT + threadIdx.x; m < A.n; m += (uint64_t)gridDim.x * kT) {
-    const double pos = __ddiv_rn(__dadd_rn((double)m, u), dn);
+  const uint64_t nthr = (A.n + kS - 1) / kS;
+  for (uint64_t t = (uint64_t)blockIdx.x * kT + threadIdx.x; t < nthr; t += (uint64_t)gridDim.x * kT) {
+    const uint64_t m0 = t * kS;
+    double pos = __ddiv_rn(__dadd_rn((double)m0, u), dn);
     uint64_t lo = 0, hi = A.n;
     while (lo < hi) {
       const uint64_t mid = (lo + hi) >> 1;
       if (A.cum[mid] < pos) lo = mid + 1;
       else hi = mid;
     }
-    A.anc[m] = (uint32_t)(lo < A.n ? lo : A.n - 1);
+    uint64_t j = lo < A.n ? lo : A.n - 1;
+    A.anc[m0] = (uint32_t)j;
+    for (int e = 1; e < kS && m0 + e < A.n; ++e) {
+      pos = __ddiv_rn(__dadd_rn((double)(m0 + e), u), dn);
+      if (A.cum[j] < pos) {  // gallop forward from j, then bisect: O(log distance)
+        uint64_t step = 1, a = j;  // invariant: cum[a] < pos
+        uint64_t b = j + 1;
+        while (b < A.n && A.cum[b] < pos) {
+          a = b;
+          step <<= 1;
+          b = a + step;
+        }
+        if (b > A.n) b = A.n;
+        while (a + 1 < b) {  // cum[a] < pos, first j >= b has cum >= pos (or b = n)
+          const uint64_t mid = (a + b) >> 1;
+          if (A.cum[mid] < pos) a = mid;
+          else b = mid;
+        }
+        j = b < A.n ? b : A.n - 1;
+      }
+      A.anc[m0 + e] = (uint32_t)j;
+    }
   }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
@@ -506,31 +563,35 @@ __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[kT / 32 + 2];
   __shared__ unsigned long long ush[kT / 32 + 2];
-  __shared__ __align__(16) unsigned char big[kTile * sizeof(Aff)];
-  __shared__ double vbuf[kT];
-  __shared__ unsigned char fbuf[kT];
-  __shared__ int sh_i[2];
-  Aff* atile = reinterpret_cast<Aff*>(big);
-  int* ibuf = reinterpret_cast<int*>(big);
-  unsigned long long* ubuf = reinterpret_cast<unsigned long long*>(big + kTile * sizeof(int));
-  // big holds kTile Aff (16 KB) = kTile ints (4 KB) + kTile + 1 u64 (8 KB) as well
+  __shared__ union U {
+    Aff wa[kT / 32];
+    WalkSmem walk;
+  } u;
   const bool lead = blockIdx.x == 0;
+  // profiling (RefCdfWork::prof != null): CTA 0 stamps %globaltimer at each phase end
+#define MARK(i) \
+  if (A.w.prof && lead && threadIdx.x == 0) A.w.prof[i] = gtimer();
+  MARK(0);
 
   // ---- l1 = logsumexp(log_w) ----
   phase_block_max(A, sh);
   grid.sync();
+  MARK(1);
   if (lead) phase_scan_max(A, sh + 8, sh);
   grid.sync();
-  phase_block_affine(A, kModeLse, 0.0, sh, atile, ibuf);
+  MARK(2);
+  phase_block_affine(A, kModeLse, 0.0, sh, u.wa, nullptr);
   grid.sync();
-  if (lead) phase_scan_affine(A, atile);
+  MARK(3);
+  if (lead) phase_scan_affine(A, u.wa);
   grid.sync();
+  MARK(4);
   phase_classify(A, kModeLse, 0.0, sh, ush);
   grid.sync();
-  if (lead) phase_runs(A, ibuf, ubuf, sh_i, ush + 8);
-  grid.sync();
+  MARK(5);
   if (lead) {
-    const double s = phase_walk(A, kModeLse, 0.0, sh, vbuf, fbuf, ibuf);
+    const double s = phase_walk(A, kModeLse, 0.0, sh, u.walk);
+    if (threadIdx.x == 0 && A.w.prof) A.w.prof[14] = u.walk.replays;
     if (threadIdx.x == 0) {
       const double M = A.w.gmax[0];
       // LogAccumulator::log_total (logsum.hpp:40-42)
@@ -540,27 +601,37 @@ __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
     }
   }
   grid.sync();
+  MARK(6);
   const double l1 = *(volatile double*)A.w.l1;
   if (l1 == kNegInfD || A.want_anc < 0) return;  // degenerate (engine.cpp:66) / l1 only
 
   // ---- cum_j, the reference's sequential CDF ----
-  phase_block_affine(A, kModeCdf, l1, sh, atile, ibuf);
+  phase_block_affine(A, kModeCdf, l1, sh, u.wa, nullptr);
   grid.sync();
-  if (lead) phase_scan_affine(A, atile);
+  MARK(7);
+  if (lead) phase_scan_affine(A, u.wa);
   grid.sync();
+  MARK(8);
   phase_classify(A, kModeCdf, l1, sh, ush);
   grid.sync();
-  if (lead) phase_runs(A, ibuf, ubuf, sh_i, ush + 8);
-  grid.sync();
+  MARK(9);
   if (lead) {
-    const double s = phase_walk(A, kModeCdf, l1, sh, vbuf, fbuf, ibuf);
+    const double s = phase_walk(A, kModeCdf, l1, sh, u.walk);
+    if (threadIdx.x == 0 && A.w.prof) A.w.prof[15] = u.walk.replays;
     if (threadIdx.x == 0) A.st->total = s;
   }
   grid.sync();
+  MARK(10);
   phase_materialize(A, l1, sh, ush);
   if (A.want_anc != 1) return;
   grid.sync();
+  MARK(11);
   phase_ancestors(A, A.st->u);
+  if (A.w.prof) {
+    grid.sync();
+    MARK(12);
+  }
+#undef MARK
 }
 
 __global__ void exact_math_kernel(int which, const double* x, uint64_t n, double* out) {
@@ -578,8 +649,8 @@ cudaError_t launch_exact_math(int which, const double* x, uint64_t n, double* ou
 
 size_t refcdf_work_bytes(uint64_t n) {
   const uint64_t nb = (n + kT - 1) / kT;
-  // 7 double/u64 arrays + 3 int arrays of nb + 2 entries, 3 scalars, 16-byte alignment each
-  return (size_t)(nb + 2) * (7 * 8 + 3 * 4) + 16 * 16 + 256;
+  // 6 double/u64 arrays + 1 int array of nb + 2 entries, 3 scalars, 16-byte alignment each
+  return (size_t)(nb + 2) * (6 * 8 + 4) + 16 * 16 + 256;
 }
 
 void refcdf_work_carve(void* base, uint64_t n, RefCdfWork* w) {
@@ -595,14 +666,11 @@ void refcdf_work_carve(void* base, uint64_t n, RefCdfWork* w) {
   w->bb = (double*)take(8 * (nb + 1));
   w->sstart = (double*)take(8 * (nb + 1));
   w->tot = (unsigned long long*)take(8 * (nb + 1));
-  w->pw = (unsigned long long*)take(8 * (nb + 1));
-  w->shead = (double*)take(8 * (nb + 1));
+  w->bstart = (unsigned long long*)take(8 * (nb + 1));
   w->kb = (int*)take(4 * (nb + 1));
-  w->hid = (int*)take(4 * (nb + 1));
-  w->heads = (int*)take(4 * (nb + 2));
   w->gmax = (double*)take(16);
   w->l1 = (double*)take(16);
-  w->nheads = (int*)take(16);
+  w->prof = nullptr;
 }
 
 cudaError_t launch_refcdf(const double* lw, uint64_t n, SmcState* st, int gated, const RefCdfWork* w,
