@@ -205,6 +205,24 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
                     double rho, uint64_t seed, uint64_t memory_cap_bytes,
                     const asmc_exec* exec, asmc_rounds_out* out);
 
+/* Batched seeds (replaces the replicate loop of experiment.cpp:96-140 for
+ * run_sais): the round loop of asmc_run_rounds(ASMC_MODE_SAIS) for nseeds seeds at once,
+ * the seed an extra launch dimension of the one-lane pass (lanes 1, dim <= 1024).  Each
+ * seed's results equal its own asmc_run_rounds call bit for bit.  Host outputs:
+ * per (seed s, round k) at [s * rounds + k]: log_z_hat, elbo_hat, lambda_total (Lambda-hat);
+ * per round k: n_particles, steps, wall_seconds (CUDA events around the round, all seeds). */
+typedef struct asmc_seeds_out {
+  uint64_t* n_particles;
+  int32_t* steps;
+  double* wall_seconds;
+  double* log_z_hat;
+  double* elbo_hat;
+  double* lambda_total;
+} asmc_seeds_out;
+int asmc_run_sais_seeds(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                        uint64_t n_particles, int32_t rounds, const uint64_t* seeds, int32_t nseeds,
+                        const asmc_exec* exec, asmc_seeds_out* out);
+
 /* Multi-GPU SAIS: partials of particles [p_begin, p_end) of an n_particles round.
  * p_begin must be a multiple of ASMC_FOLD_CHUNK.  Writes per fold chunk
  * (ASMC_FOLD_CHUNK particles) and per step t = 1..T the four accumulators

@@ -86,6 +86,12 @@ class RoundsOut(C.Structure):
                 ("kernel_applications", C.POINTER(C.c_uint64))]
 
 
+class SeedsOut(C.Structure):  # asmc_seeds_out
+    _fields_ = [("n_particles", C.POINTER(C.c_uint64)), ("steps", C.POINTER(C.c_int32)),
+                ("wall_seconds", C.POINTER(C.c_double)), ("log_z_hat", C.POINTER(C.c_double)),
+                ("elbo_hat", C.POINTER(C.c_double)), ("lambda_total", C.POINTER(C.c_double))]
+
+
 class ZjaOpts(C.Structure):
     _fields_ = [("n_particles", C.c_uint64), ("target_steps", C.c_int32), ("max_steps", C.c_int32),
                 ("delta_star", C.c_double), ("seed", C.c_uint64)]

@@ -143,6 +143,25 @@ def run_rounds(target, kernel, mode, n, rounds, policy=abi.POLICY_ADAPTIVE_ESS, 
     return bufs
 
 
+def run_sais_seeds(target, kernel, n, rounds, seeds, exec_=None):
+    """run_sais for many seeds in one batched launch per kernel (asmc_run_sais_seeds).
+    Returns dict: per round n_particles, steps, wall_seconds; per (seed, round) arrays
+    log_z_hat, elbo_hat, lambda_total of shape (nseeds, rounds)."""
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    S = len(seeds)
+    bufs = dict(n_particles=np.zeros(rounds, np.uint64), steps=np.zeros(rounds, np.int32),
+                wall_seconds=np.zeros(rounds), log_z_hat=np.zeros((S, rounds)), elbo_hat=np.zeros((S, rounds)),
+                lambda_total=np.zeros((S, rounds)))
+    out = abi.SeedsOut()
+    types = dict(n_particles=C.c_uint64, steps=C.c_int32)
+    for k, v in bufs.items():
+        setattr(out, k, _arr(v, types.get(k, C.c_double)))
+    ex = exec_ or abi.execopts()
+    _check(lib().asmc_run_sais_seeds(C.byref(target), C.byref(kernel), C.c_uint64(n), C.c_int32(rounds),
+                                     _arr(seeds, C.c_uint64), C.c_int32(S), C.byref(ex), C.byref(out)))
+    return bufs
+
+
 def fold_chunks(p_begin, p_end):
     return lib().asmc_fold_chunks(C.c_uint64(p_begin), C.c_uint64(p_end))
 
@@ -467,7 +486,7 @@ class ZjaShard(SmcShard):
 
 EXPORTED = [
     "asmc_last_error", "asmc_version", "asmc_device_count", "asmc_launch_count", "asmc_run_smc",
-    "asmc_run_sais_single", "asmc_run_rounds", "asmc_fold_chunks", "asmc_sais_partials",
+    "asmc_run_sais_single", "asmc_run_rounds", "asmc_run_sais_seeds", "asmc_fold_chunks", "asmc_sais_partials",
     "asmc_fold_partials", "asmc_rng_u64", "asmc_rng_uniform", "asmc_rng_normal",
     "asmc_trajectories", "asmc_systematic_resample", "asmc_resample_cdf", "asmc_logsumexp",
     "asmc_exact_math", "asmc_ess", "asmc_barrier_estimate",

@@ -1216,6 +1216,160 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
   return rc;
 }
 
+// Batched seeds: run_sais (drivers.cpp:186-232) for many
+// seeds with the seed as an extra launch dimension -- one pass launch, one fold, one
+// report and one schedule launch per round for ALL seeds (the one-lane pass: CTA
+// s * nblk + b is block b of seed s).  Each seed's numbers are those of its own
+// asmc_run_rounds(SAIS) call, bit for bit (same kernels, same per-seed trees).
+int asmc_run_sais_seeds(const asmc_target_desc* target, const asmc_kernel_desc* kernel, uint64_t n1,
+                        int32_t rounds, const uint64_t* seeds, int32_t nseeds, const asmc_exec* exec,
+                        asmc_seeds_out* out) {
+  if (n1 < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "n_particles must be at least 1");
+  if (rounds < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "rounds must be at least 1");
+  if (nseeds < 1 || !seeds) return fail(ASMC_ERR_INVALID_ARGUMENT, "need at least one seed");
+  TRY(check_pair(target, kernel));
+  TRY(check_pass_target(target, "asmc_run_sais_seeds"));
+  if (!out) return fail(ASMC_ERR_INVALID_ARGUMENT, "null output");
+  const asmc_exec ex = exec ? *exec : default_exec();
+  const uint64_t d = target->dim;
+  if (ex.lanes > 1) return fail(ASMC_ERR_CAPABILITY, "batched seeds run the one-lane pass (lanes = 1)");
+  if (d > 1024) return fail(ASMC_ERR_CAPABILITY, "batched seeds support dim <= 1024");
+  const Layout L{1, d <= 16 ? 16 : 1024};
+  const int S = nseeds;
+  std::vector<uint64_t> ns(rounds);
+  std::vector<int> ts(rounds);
+  ns[0] = n1;
+  ts[0] = 1;
+  for (int k = 1; k < rounds; ++k)
+    TRY(asmc_budget(ns[k - 1], ts[k - 1], d, 4096ull << 20, ASMC_MODE_SAIS, &ns[k], &ts[k]));
+  int tmax = 0;
+  for (int k = 0; k < rounds; ++k) tmax = ts[k] > tmax ? ts[k] : tmax;
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C, ex.stream));
+  cudaStream_t st = C->stream;
+  DBuf<uint64_t> d_seeds;
+  TRY(d_seeds.alloc(S, st));
+  CU(cudaMemcpyAsync(d_seeds.p, seeds, sizeof(uint64_t) * S, cudaMemcpyHostToDevice, st));
+  std::vector<DBuf<double>> betas(rounds);
+  for (int k = 0; k < rounds; ++k) TRY(betas[k].alloc((size_t)S * (ts[k] + 1), st));
+  {
+    std::vector<double> b01(2 * (size_t)S);
+    for (int s = 0; s < S; ++s) {
+      b01[2 * s] = 0.0;
+      b01[2 * s + 1] = 1.0;
+    }
+    CU(cudaMemcpyAsync(betas[0].p, b01.data(), sizeof(double) * b01.size(), cudaMemcpyHostToDevice, st));
+  }
+  // per-seed round outputs: arrays of S (T + 1) (or S) entries, S RoundDev views
+  struct Out {
+    DBuf<double> g0, g1, g2, ess, cz, lam, scal;
+    DBuf<uint8_t> rs;
+    DBuf<int32_t> rt;
+    DBuf<SmcState> stt;
+    DBuf<RoundDev> rd;
+  };
+  std::vector<Out> O(rounds);
+  DBuf<int> gerr, serr;
+  TRY(gerr.alloc(1, st));
+  TRY(serr.alloc(S, st));
+  CU(cudaMemsetAsync(gerr.p, 0, sizeof(int), st));
+  CU(cudaMemsetAsync(serr.p, 0, sizeof(int) * S, st));
+  DBuf<double> sched_scratch;
+  TRY(sched_scratch.alloc((size_t)S * 5 * (tmax + 1), st));
+  const bool exact = ex.precision == ASMC_PREC_FP64;
+  const PassArgs base = base_args(target, kernel);
+  std::vector<cudaEvent_t> ev(rounds + 1);
+  for (auto& e : ev) CU(cudaEventCreate(&e));
+  CU(cudaEventRecord(ev[0], st));
+  for (int k = 0; k < rounds; ++k) {
+    const int T = ts[k];
+    const uint64_t n = ns[k], nblk = nblocks(n), rows = (uint64_t)S * (T + 1);
+    const uint64_t nchunks = (nblk + kChunkBlocks - 1) / kChunkBlocks;
+    Out& o = O[k];
+    const size_t R1 = (size_t)S * (T + 1);
+    TRY(o.g0.alloc(R1, st));
+    TRY(o.g1.alloc(R1, st));
+    TRY(o.g2.alloc(R1, st));
+    TRY(o.ess.alloc(R1, st));
+    TRY(o.cz.alloc(R1, st));
+    TRY(o.lam.alloc(R1, st));
+    TRY(o.scal.alloc(2 * (size_t)S, st));
+    TRY(o.rs.alloc(R1, st));
+    TRY(o.rt.alloc(R1, st));
+    TRY(o.stt.alloc(S, st));
+    TRY(o.rd.alloc(S, st));
+    CU(cudaMemsetAsync(o.stt.p, 0, sizeof(SmcState) * S, st));
+    std::vector<RoundDev> hv(S);
+    for (int s = 0; s < S; ++s) {
+      const size_t r0 = (size_t)s * (T + 1);
+      hv[s] = RoundDev{o.g0.p + r0, o.g1.p + r0, o.g2.p + r0, o.ess.p + r0, o.cz.p + r0, o.rs.p + r0,
+                       o.rt.p + r0, o.lam.p + r0, o.scal.p + 2 * (size_t)s, o.stt.p + s};
+    }
+    CU(cudaMemcpyAsync(o.rd.p, hv.data(), sizeof(RoundDev) * S, cudaMemcpyHostToDevice, st));
+    DBuf<LogAcc> part, chunk, tot;  // stream-ordered frees after this round's kernels
+    TRY(part.alloc(rows * kNAcc * nblk, st));
+    TRY(chunk.alloc(rows * kNAcc * nchunks, st));
+    TRY(tot.alloc(rows * kNAcc, st));
+    CU(cudaMemsetAsync(part.p, 0, sizeof(LogAcc) * rows * kNAcc * nblk, st));  // row 0 of each seed: unused
+    PassArgs A = base;
+    A.betas = betas[k].p;
+    A.T = T;
+    A.t_begin = 1;
+    A.t_end = T;
+    A.mode = kModeSais;
+    A.row_base = 0;
+    A.n = n;
+    A.p_begin = 0;
+    A.n_local = n;
+    A.seed = 0;
+    A.round = (uint64_t)(k + 1);
+    A.part = part.p;
+    A.part_stride = nblk;
+    A.err = gerr.p;
+    A.seeds = d_seeds.p;
+    A.blocks_per_seed = nblk;
+    A.betas_stride = (uint64_t)T + 1;
+    A.part_seed_stride = (uint64_t)(T + 1) * kNAcc * nblk;
+    LCH(launch_pass(ex, L, A, (uint64_t)S * nblk, st));
+    LCH(launch_fold(exact, part.p, nblk, nblk, 0, (int)rows, 4, chunk.p, tot.p, st));
+    LCH(launch_sais_report_batch(tot.p, T, n, o.rd.p, S, st));
+    if (k + 1 < rounds)
+      LCH(launch_generate_schedule_batch(o.lam.p, (uint64_t)T + 1, betas[k].p, T + 1, ts[k + 1], betas[k + 1].p,
+                                         sched_scratch.p, serr.p, S, st));
+    CU(cudaEventRecord(ev[k + 1], st));
+  }
+  CU(cudaStreamSynchronize(st));
+  int herr = 0;
+  CU(cudaMemcpy(&herr, gerr.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (herr) return device_error(herr, 0, 0.0);
+  std::vector<int> se(S);
+  CU(cudaMemcpy(se.data(), serr.p, sizeof(int) * S, cudaMemcpyDeviceToHost));
+  for (int s = 0; s < S; ++s)
+    if (se[s]) return fail(se[s], "schedule generation for seed %llu failed validation", (unsigned long long)seeds[s]);
+  for (int k = 0; k < rounds; ++k) {
+    const int T = ts[k];
+    std::vector<SmcState> sts(S);
+    std::vector<double> scal(2 * (size_t)S), lam((size_t)S * (T + 1));
+    CU(cudaMemcpy(sts.data(), O[k].stt.p, sizeof(SmcState) * S, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(scal.data(), O[k].scal.p, sizeof(double) * 2 * S, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(lam.data(), O[k].lam.p, sizeof(double) * S * (T + 1), cudaMemcpyDeviceToHost));
+    for (int s = 0; s < S; ++s) TRY(device_error(sts[s].err, sts[s].err_step, sts[s].err_val));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+    if (out->n_particles) out->n_particles[k] = ns[k];
+    if (out->steps) out->steps[k] = T;
+    if (out->wall_seconds) out->wall_seconds[k] = ms * 1e-3;
+    for (int s = 0; s < S; ++s) {
+      const size_t i = (size_t)s * rounds + k;
+      if (out->log_z_hat) out->log_z_hat[i] = scal[2 * s];
+      if (out->elbo_hat) out->elbo_hat[i] = scal[2 * s + 1];
+      if (out->lambda_total) out->lambda_total[i] = lam[(size_t)s * (T + 1) + T];
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return 0;
+}
+
 uint64_t asmc_fold_chunks(uint64_t p_begin, uint64_t p_end) {
   if (p_end <= p_begin) return 0;
   return (p_end - p_begin + ASMC_FOLD_CHUNK - 1) / ASMC_FOLD_CHUNK;

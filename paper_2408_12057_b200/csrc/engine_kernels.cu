@@ -146,8 +146,7 @@ __device__ __forceinline__ double dhat_raw(double g0, double g1, double g2) {
 
 // --------------------------------------------------------- SAIS report --
 // drivers.cpp:148-176 + barrier_estimate (schedule.cpp:41-56).
-__global__ void sais_report_kernel(const LogAcc* tot, int T, uint64_t n, RoundDev* rd) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void sais_report_body(const LogAcc* tot, int T, uint64_t n, RoundDev* rd) {
   const double log_n = log((double)n);
   rd->log_g0[0] = rd->log_g1[0] = rd->log_g2[0] = kNegInf;
   for (int t = 1; t <= T; ++t) {
@@ -176,6 +175,15 @@ __global__ void sais_report_kernel(const LogAcc* tot, int T, uint64_t n, RoundDe
   rd->lambda[0] = 0.0;
   for (int t = 1; t <= T; ++t)
     rd->lambda[t] = rd->lambda[t - 1] + sqrt(dhat_raw(rd->log_g0[t], rd->log_g1[t], rd->log_g2[t]));
+}
+__global__ void sais_report_kernel(const LogAcc* tot, int T, uint64_t n, RoundDev* rd) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  sais_report_body(tot, T, n, rd);
+}
+// batched seeds: CTA s reports seed s (tot rows s (T + 1) .. s (T + 1) + T, rd[s])
+__global__ void sais_report_batch_kernel(const LogAcc* tot, int T, uint64_t n, RoundDev* rd) {
+  if (threadIdx.x != 0) return;
+  sais_report_body(tot + (size_t)blockIdx.x * (T + 1) * kNAcc, T, n, rd + blockIdx.x);
 }
 
 // ---------------------------------------------------------- SSMC decide --
@@ -396,9 +404,8 @@ __device__ int validate_barrier(const double* lambda, const double* beta, int n)
 }
 
 // generate_schedule (schedule.cpp:144-187), one thread.  scratch: 5 * knots doubles.
-__global__ void generate_schedule_kernel(const double* lambda, const double* beta, int knots,
-                                         int t_new, double* out, double* scratch, int* err) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void generate_schedule_body(const double* lambda, const double* beta, int knots,
+                                       int t_new, double* out, double* scratch, int* err) {
   if (*err) return;
   int rc = validate_barrier(lambda, beta, knots);
   if (!rc && t_new < 1) rc = ASMC_ERR_INVALID_ARGUMENT;
@@ -454,6 +461,22 @@ __global__ void generate_schedule_kernel(const double* lambda, const double* bet
       *err = ASMC_ERR_INVALID_ARGUMENT;
       return;
     }
+}
+
+__global__ void generate_schedule_kernel(const double* lambda, const double* beta, int knots,
+                                         int t_new, double* out, double* scratch, int* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  generate_schedule_body(lambda, beta, knots, t_new, out, scratch, err);
+}
+// batched seeds: CTA s regenerates seed s's grid (knots = T + 1 -> t_new + 1 betas), its
+// own error word err[s]
+__global__ void generate_schedule_batch_kernel(const double* lambda, uint64_t lam_stride, const double* beta,
+                                               int knots, int t_new, double* out, double* scratch,
+                                               int* err) {
+  if (threadIdx.x != 0) return;
+  const uint64_t s = blockIdx.x;
+  generate_schedule_body(lambda + s * lam_stride, beta + s * knots, knots, t_new, out + s * (uint64_t)(t_new + 1),
+                         scratch + s * 5 * (uint64_t)knots, err + s);
 }
 
 // local_barrier (schedule.cpp:189-197)
@@ -603,6 +626,19 @@ cudaError_t launch_gather(const uint32_t* anc, uint64_t n, uint64_t row_bytes, v
 cudaError_t launch_generate_schedule(const double* lambda, const double* beta, int knots, int t_new,
                                      double* out, double* scratch, int* err, cudaStream_t s) {
   generate_schedule_kernel<<<1, 1, 0, s>>>(lambda, beta, knots, t_new, out, scratch, err);
+  return LAUNCH_OK();
+}
+
+cudaError_t launch_sais_report_batch(const LogAcc* tot, int T, uint64_t n, RoundDev* rd, int nseeds,
+                                     cudaStream_t s) {
+  sais_report_batch_kernel<<<nseeds, 1, 0, s>>>(tot, T, n, rd);
+  return LAUNCH_OK();
+}
+
+cudaError_t launch_generate_schedule_batch(const double* lambda, uint64_t lam_stride, const double* beta, int knots,
+                                           int t_new, double* out, double* scratch, int* err, int nseeds,
+                                           cudaStream_t s) {
+  generate_schedule_batch_kernel<<<nseeds, 1, 0, s>>>(lambda, lam_stride, beta, knots, t_new, out, scratch, err);
   return LAUNCH_OK();
 }
 

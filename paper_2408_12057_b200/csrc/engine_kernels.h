@@ -77,6 +77,12 @@ cudaError_t launch_gather(const uint32_t* anc, uint64_t n, uint64_t row_bytes, v
                           int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s);
 cudaError_t launch_generate_schedule(const double* lambda, const double* beta, int knots, int t_new,
                                      double* out, double* scratch, int* err, cudaStream_t s);
+// batched seeds (SAIS round loop over many seeds in one launch per kernel)
+cudaError_t launch_sais_report_batch(const LogAcc* tot, int T, uint64_t n, RoundDev* rd, int nseeds,
+                                     cudaStream_t s);
+cudaError_t launch_generate_schedule_batch(const double* lambda, uint64_t lam_stride, const double* beta, int knots,
+                                           int t_new, double* out, double* scratch, int* err, int nseeds,
+                                           cudaStream_t s);
 cudaError_t launch_local_barrier(const double* lambda, const double* beta, int knots, double* out,
                                  double* scratch, int* err, cudaStream_t s);
 cudaError_t launch_barrier(const double* g0, const double* g1, const double* g2, int T,

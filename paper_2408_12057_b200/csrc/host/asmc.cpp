@@ -14,7 +14,6 @@ namespace asmc {
 namespace {
 
 constexpr double kLogSqrt2Pi = 0.91893853320467274178;
-constexpr double kNegInf = -HUGE_VAL;
 
 // Rethrow a C-ABI error as the reference's exception class.
 void check(int rc) {
@@ -123,6 +122,10 @@ double AnnealedTarget::log_gamma(double beta, std::span<const double> x) const {
   return beta == 0.0 ? lr : lr + beta * potential(x);
 }
 
+void AnnealedTarget::exact_sample(double, rng::Stream&, std::span<double>) const {
+  throw capability_error("target does not provide an exact sampler");
+}
+
 double AnnealedTarget::analytic_log_z(double) const {
   throw capability_error("target does not provide analytic_log_z");
 }
@@ -167,6 +170,16 @@ double GaussianShiftTarget::analytic_discrepancy(double beta, double beta2) cons
   const double db = beta2 - beta;
   return static_cast<double>(dim_) * z_ * z_ * db * db;
 }
+void GaussianShiftTarget::sample_reference(rng::Stream& stream, std::span<double> out) const {
+  check_point(out);
+  for (double& v : out) v = mu0_ + sigma_ * stream.normal();
+}
+void GaussianShiftTarget::exact_sample(double beta, rng::Stream& stream, std::span<double> out) const {
+  check_beta(beta);
+  check_point(out);
+  const double mu = (1.0 - beta) * mu0_ + beta * mu1_;
+  for (double& v : out) v = mu + sigma_ * stream.normal();
+}
 bool GaussianShiftTarget::device_descriptor(asmc_target_desc* o) const {
   o->kind = ASMC_TARGET_GAUSSIAN_SHIFT;
   o->dim = dim_;
@@ -201,6 +214,10 @@ double MixtureTarget::potential(std::span<const double> x) const {
     s += hi + std::log1p(std::exp(lo - hi)) - log_normal_pdf(v, 0.0, ref_sigma_);
   }
   return s;
+}
+void MixtureTarget::sample_reference(rng::Stream& stream, std::span<double> out) const {
+  check_point(out);
+  for (double& v : out) v = ref_sigma_ * stream.normal();
 }
 bool MixtureTarget::device_descriptor(asmc_target_desc* o) const {
   o->kind = ASMC_TARGET_MIXTURE;
@@ -247,6 +264,16 @@ double ScaleGaussianTarget::analytic_discrepancy(double beta, double beta2) cons
     throw std::domain_error("analytic_discrepancy undefined for 2*beta2 - beta > 1");
   return analytic_log_z(std::min(1.0, b3)) + analytic_log_z(beta) - 2.0 * analytic_log_z(beta2);
 }
+void ScaleGaussianTarget::sample_reference(rng::Stream& stream, std::span<double> out) const {
+  check_point(out);
+  for (double& v : out) v = s0_ * stream.normal();
+}
+void ScaleGaussianTarget::exact_sample(double beta, rng::Stream& stream, std::span<double> out) const {
+  check_beta(beta);
+  check_point(out);
+  const double sd = 1.0 / std::sqrt(tau(beta));  // pi_beta = N(0, I / tau_beta)
+  for (double& v : out) v = sd * stream.normal();
+}
 bool ScaleGaussianTarget::device_descriptor(asmc_target_desc* o) const {
   o->kind = ASMC_TARGET_SCALE_GAUSSIAN;
   o->dim = dim_;
@@ -276,6 +303,10 @@ double LogisticTarget::potential(std::span<const double> th) const {
     acc += y_[j] * l - (l > 0.0 ? l + std::log1p(std::exp(-l)) : std::log1p(std::exp(l)));
   }
   return acc;
+}
+void LogisticTarget::sample_reference(rng::Stream& stream, std::span<double> out) const {
+  check_point(out);
+  for (double& v : out) v = sp_ * stream.normal();
 }
 bool LogisticTarget::device_descriptor(asmc_target_desc* o) const {
   o->kind = ASMC_TARGET_LOGISTIC;
@@ -312,6 +343,10 @@ double IsingTarget::potential(std::span<const double> y) const {
       acc += -0.5 * yi * u + (au + std::log1p(std::exp(-2.0 * au))) - log_normal_pdf(yi, 0.0, sigma_);
     }
   return acc;
+}
+void IsingTarget::sample_reference(rng::Stream& stream, std::span<double> out) const {
+  check_point(out);
+  for (double& v : out) v = sigma_ * stream.normal();
 }
 bool IsingTarget::device_descriptor(asmc_target_desc* o) const {
   o->kind = ASMC_TARGET_ISING;
@@ -371,6 +406,11 @@ double ess(std::span<const double> lw) {
   double out = 0.0;
   check(asmc_ess(lw.data(), lw.size(), 0, &out));
   return out;
+}
+
+std::vector<std::uint32_t> systematic_resample(std::span<const double> lw, rng::Stream& stream) {
+  if (lw.empty()) throw std::invalid_argument("cannot resample an empty system");
+  return systematic_resample(lw, stream.uniform(), 0);  // engine.cpp:67: one uniform per call
 }
 
 std::vector<std::uint32_t> systematic_resample(std::span<const double> lw, double u, int device) {

@@ -4,11 +4,17 @@
 // header.  Every sampler entry point forwards through the C-ABI of
 // include/asmc_b200.h to the B200 kernels; nothing here samples on the CPU.
 //
+// The reference's include layout is kept: asmc/{rng,logsum,errors}.hpp hold their
+// definitions, asmc/{target,kernel,engine,schedule,drivers,pt,theory}.hpp forward here,
+// so `#include "asmc/target.hpp"` code (the reference's own test fixtures) compiles
+// unchanged against -I csrc/host.
+//
 // Differences from the reference interface (documented in INTEGRATION.md):
 //  * A target is a device plugin: AnnealedTarget subclasses provide a
 //    descriptor (device_descriptor); the per-point virtuals (log_reference,
-//    potential, log_gamma, analytic_*) remain for callers, but a target the
-//    device does not implement raises capability_error when sampled.
+//    potential, sample_reference, exact_sample, log_gamma, analytic_*) keep the
+//    reference's signatures for callers and plugins, but a target the device does
+//    not implement raises capability_error when sampled (no CPU fallback).
 //  * RunOptions / DriverOptions gain execution fields (rng, precision, device,
 //    lanes).  Defaults reproduce the reference: keyed xoshiro streams, fp64
 //    reference arithmetic.  `workers` and `chunk` are accepted and ignored
@@ -21,27 +27,12 @@
 #include <string>
 #include <vector>
 
+#include "asmc/errors.hpp"
+#include "asmc/logsum.hpp"
+#include "asmc/rng.hpp"
 #include "asmc_b200.h"
 
 namespace asmc {
-
-// ---- errors.hpp:9-37 -----------------------------------------------------
-class capability_error : public std::runtime_error {
- public:
-  explicit capability_error(const std::string& w) : std::runtime_error(w) {}
-};
-class degenerate_weights_error : public std::runtime_error {
- public:
-  explicit degenerate_weights_error(const std::string& w) : std::runtime_error(w) {}
-};
-class evaluation_error : public std::runtime_error {
- public:
-  explicit evaluation_error(const std::string& w) : std::runtime_error(w) {}
-};
-class device_error : public std::runtime_error {
- public:
-  explicit device_error(const std::string& w) : std::runtime_error(w) {}
-};
 
 // ---- target.hpp -----------------------------------------------------------
 struct Capabilities {
@@ -56,11 +47,15 @@ class AnnealedTarget {
   virtual std::size_t dim() const = 0;
   virtual double log_reference(std::span<const double> x) const = 0;
   virtual double potential(std::span<const double> x) const = 0;
+  virtual void sample_reference(rng::Stream& stream, std::span<double> out) const = 0;
   virtual Capabilities capabilities() const { return {}; }
   double log_gamma(double beta, std::span<const double> x) const;
   virtual double analytic_log_z(double beta) const;
   virtual double analytic_delta(double beta) const;
   virtual double analytic_discrepancy(double beta, double beta2) const;
+  // exact draw from pi_beta (requires exact_sampler); host code for callers: the device
+  // path draws with its own kernels
+  virtual void exact_sample(double beta, rng::Stream& stream, std::span<double> out) const;
   // B200 plugin boundary: fill the device descriptor, or return false.
   virtual bool device_descriptor(asmc_target_desc* out) const { return false; }
 
@@ -75,10 +70,12 @@ class GaussianShiftTarget final : public AnnealedTarget {
   std::size_t dim() const override { return dim_; }
   double log_reference(std::span<const double> x) const override;
   double potential(std::span<const double> x) const override;
+  void sample_reference(rng::Stream& stream, std::span<double> out) const override;
   Capabilities capabilities() const override { return {true, true, true}; }
   double analytic_log_z(double beta) const override;
   double analytic_delta(double beta) const override;
   double analytic_discrepancy(double beta, double beta2) const override;
+  void exact_sample(double beta, rng::Stream& stream, std::span<double> out) const override;
   bool device_descriptor(asmc_target_desc* out) const override;
   double z() const { return z_; }
 
@@ -94,6 +91,7 @@ class MixtureTarget final : public AnnealedTarget {
   std::size_t dim() const override { return dim_; }
   double log_reference(std::span<const double> x) const override;
   double potential(std::span<const double> x) const override;
+  void sample_reference(rng::Stream& stream, std::span<double> out) const override;
   bool device_descriptor(asmc_target_desc* out) const override;
 
  private:
@@ -108,10 +106,12 @@ class ScaleGaussianTarget final : public AnnealedTarget {
   std::size_t dim() const override { return dim_; }
   double log_reference(std::span<const double> x) const override;
   double potential(std::span<const double> x) const override;
+  void sample_reference(rng::Stream& stream, std::span<double> out) const override;
   Capabilities capabilities() const override { return {true, true, true}; }
   double analytic_log_z(double beta) const override;
   double analytic_delta(double beta) const override;
   double analytic_discrepancy(double beta, double beta2) const override;
+  void exact_sample(double beta, rng::Stream& stream, std::span<double> out) const override;
   bool device_descriptor(asmc_target_desc* out) const override;
 
  private:
@@ -128,6 +128,7 @@ class LogisticTarget final : public AnnealedTarget {
   std::size_t dim() const override { return dim_; }
   double log_reference(std::span<const double> x) const override;
   double potential(std::span<const double> x) const override;
+  void sample_reference(rng::Stream& stream, std::span<double> out) const override;
   bool device_descriptor(asmc_target_desc* out) const override;
   std::size_t n_data() const { return y_.size(); }
 
@@ -146,6 +147,7 @@ class IsingTarget final : public AnnealedTarget {
   std::size_t dim() const override { return static_cast<std::size_t>(L_) * L_; }
   double log_reference(std::span<const double> x) const override;
   double potential(std::span<const double> x) const override;
+  void sample_reference(rng::Stream& stream, std::span<double> out) const override;
   bool device_descriptor(asmc_target_desc* out) const override;
   int side() const { return L_; }
 
@@ -220,8 +222,10 @@ struct RunOptions {
 };
 
 double ess(std::span<const double> log_weights);
-// systematic ancestors for a given uniform u (engine.cpp:61-80 draws u from
-// key (seed, round, 0, t, resample)); device blocked-CDF rule, see DESIGN.md
+// engine.cpp:61-80 on the device, bit for bit (the reference's sequential CDF):
+// the reference's signature (u = stream.uniform(), as the reference draws it) and a
+// given-u overload
+std::vector<std::uint32_t> systematic_resample(std::span<const double> log_weights, rng::Stream& stream);
 std::vector<std::uint32_t> systematic_resample(std::span<const double> log_weights, double u,
                                                int device = 0);
 bool decide_resample(ResamplePolicy policy, int t, int total_steps, double ess_value,

@@ -76,6 +76,10 @@ struct PassArgs {
   double* rec_x;         // kModeTraj: [(i * (T+1) + t) * dim + k]
   double* rec_lw;        // kModeTraj: [i * (T+1) + t]
   int* err;
+  // batched seeds (one-lane pass, SAIS): launch = nseeds x blocks_per_seed CTAs; seed
+  // s uses seeds[s], betas + s * betas_stride and part + s * part_seed_stride
+  const uint64_t* seeds;
+  uint64_t blocks_per_seed, betas_stride, part_seed_stride;
   unsigned long long* drawn;  // profiling: normals actually generated (null = off)
   PhiloxRoundKeys rk[2];      // Philox round keys of (seed, round, substep 0 | 1): set at launch
 };
@@ -583,7 +587,12 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
   static_assert(!kExact || G == 1, "reference-order path is one lane per particle");
   const int tid = threadIdx.x, g = tid / G, lane = tid % G;
   const int d = (int)A.tg.dim;
-  const uint64_t blk = blockIdx.x;
+  const uint64_t bps = A.blocks_per_seed ? A.blocks_per_seed : gridDim.x;
+  const uint64_t si = blockIdx.x / bps;  // batched seeds: this CTA's seed (0 otherwise)
+  const uint64_t blk = blockIdx.x % bps;
+  const uint64_t seed = A.seeds ? A.seeds[si] : A.seed;
+  const double* betas = A.betas + si * A.betas_stride;
+  LogAcc* part = A.part + si * A.part_seed_stride;
   const int nacc = mode_nacc(A.mode);
   if (A.err && *(volatile int*)A.err) return;  // an earlier step failed: skip the work
 
@@ -614,11 +623,11 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
     } else {
       if constexpr (kExact) {
         SeqT st;
-        st.init(A.seed, A.round, pid, 0, 0);
+        st.init(seed, A.round, pid, 0, 0);
         ExactT::init(A.tg, d, x, st);
       } else {
         typename FastT::Src src;
-        src.init(A.seed, A.round, pid, 0, 0);
+        src.init(seed, A.round, pid, 0, 0);
         FastT::init(A.tg, lane, d, x, src);
       }
     }
@@ -646,18 +655,18 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
 
     // ---- annealing steps -----------------------------------------------------
     for (int t = A.t_begin; t <= A.t_end; ++t) {
-      const double b0 = A.betas[t - 1], b1 = A.betas[t];
+      const double b0 = betas[t - 1], b1 = betas[t];
       double lg;
       if constexpr (kExact) {
         Real prop[KMAX];
         lg = ExactT::weight(A.tg, d, b0, b1, x, A.err);
         SeqT st;
-        st.init(A.seed, A.round, pid, (uint64_t)t, 1);
+        st.init(seed, A.round, pid, (uint64_t)t, 1);
         ExactT::move(A.tg, A.kc, d, b1, x, prop, st);
       } else {
         lg = FastT::weight(A.tg, lane, d, b0, b1, x);
         typename FastT::Src src;
-        src.init(A.seed, A.round, pid, (uint64_t)t, 1);
+        src.init(seed, A.round, pid, (uint64_t)t, 1);
         FastT::move(A.tg, A.kc, lane, d, b1, x, src);
       }
       const double pre = lw;
@@ -684,12 +693,12 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
       __syncthreads();
       const bool first = (r == 0);
       if (!first && tid < nacc) {
-        s_dst[tid] = A.part[((size_t)(t - A.row_base) * kNAcc + tid) * A.part_stride + blk];
+        s_dst[tid] = part[((size_t)(t - A.row_base) * kNAcc + tid) * A.part_stride + blk];
       }
       __syncthreads();
       block_reduce<kExact, NG>(s_lw, s_lg, s_post, s_act, nacc, s_dst, first);
       __syncthreads();
-      if (tid < nacc) A.part[((size_t)(t - A.row_base) * kNAcc + tid) * A.part_stride + blk] = s_dst[tid];
+      if (tid < nacc) part[((size_t)(t - A.row_base) * kNAcc + tid) * A.part_stride + blk] = s_dst[tid];
     }
 
     if (mode_stores(A.mode) && active) {

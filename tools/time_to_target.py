@@ -1,16 +1,28 @@
-"""Time to a target relative variance of Z-hat (BASELINE metric, second half).
+"""Time to a target relative variance of Z-hat, wall clock on both sides (BASELINE
+metric, second half; SURVEY 8d "Time-to-target", 8f-1/8f-2).
 
-Config 1 family (SAIS, d = 10 Gaussian shift, exact log Z = 0, RWMH {0.1,1,10},
-N_1 = 2^14, doubling rounds).  For R seeds, rel-var_k = Var(Z_k)/E[Z_k]^2 of the
-round-k estimate; k* = first round with rel-var_k <= target.  Time to target =
-mean over seeds of the cumulative round times up to k*:
-  * B200: CUDA-event round times from asmc_run_rounds (reference arithmetic:
-    keyed xoshiro + fp64, so the estimates -- and hence k* -- are the
-    reference's own; the Philox/fp32 mode is reported beside it);
-  * CPU: the unmodified reference (oracle/_ref) run_sais for k* rounds with
-    workers = all host cores, on a few seeds (its time does not depend on the seed).
-As in the paper process start and JIT are excluded.
+Definitions (the paper's GPU experiment, and the reference's
+replicate loop, experiment.cpp:96-140):
+  * an effort level = one sampler run for one seed: SAIS = the doubling round loop
+    run to round k (run_sais, drivers.cpp:186-232; the schedule of round k needs rounds
+    1..k); ZJA = run_zja (drivers.cpp:234-341) with delta* = (Lambda / T)^2, the paper's
+    matching of ZJA's conditional-ESS threshold to T steps;
+  * rel-var of a level = Var(Z-hat) / E[Z-hat]^2 over R seeds (exact log Z = 0, so
+    Z-hat = exp(log Z-hat));
+  * time of a level = WALL-CLOCK seconds of one seed's run (time.perf_counter around the
+    public call, host buffers in and out), median over a few seeds; the B200 batched
+    figure (asmc_run_sais_seeds: all R seeds in one launch per kernel) is reported
+    beside it as wall seconds per seed;
+  * time to target = the time of the cheapest level whose rel-var <= target.
+CPU: the unmodified reference (oracle/_ref/libasmc_ref_release.so, -O3) on the box's
+host cores (workers = nproc), wall clock of the same level for a few seeds.
+Process start and JIT are excluded, as in the paper.
+
+  python tools/time_to_target.py [--configs 1,2,3] [--zja] [--seeds 1000]
 """
+import argparse
+import json
+import math
 import os
 import sys
 import time
@@ -21,79 +33,182 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2408_12057_b200 import abi  # noqa: E402
 
+XO, PH, F64, F32 = abi.RNG_XOSHIRO, abi.RNG_PHILOX, abi.PREC_FP64, abi.PREC_FP32
+RWMH = abi.kernel(abi.KERNEL_RWMH, (0.1, 1.0, 10.0), 1)
 
-def rel_var(log_z):
-    z = np.exp(np.asarray(log_z) - 0.0)
+
+def rel_var(log_z, c=0.0):
+    lz = np.asarray(log_z, float) - c
+    m = np.max(lz)
+    z = np.exp(lz - m)  # rel-var is scale invariant
     return float(np.var(z, ddof=1) / np.mean(z) ** 2)
 
 
-def gpu_runs(seeds, rounds, n1, rng, prec, device=0, streams=16):
-    """All seeds' round loops, `streams` at a time: each host thread drives its own
-    CUDA stream (the library keeps a per-thread context), so independent replicas
-    overlap on the device; per-seed round times are that seed's CUDA events."""
-    from concurrent.futures import ThreadPoolExecutor
-    from paper_2408_12057_b200 import capi
-    tg = abi.gaussian_shift(0.0, 1.0, 1.0, 10)
-    k = abi.kernel(abi.KERNEL_RWMH)
-    ex = abi.execopts(rng, prec, device=device)
-
-    def one(s):
-        r = capi.run_rounds(tg, k, abi.MODE_SAIS, n1, rounds, seed=int(s), exec_=ex)
-        return r["log_z_hat"].copy(), r["wall_seconds"].copy()
-
-    with ThreadPoolExecutor(max_workers=streams) as pool:
-        res = list(pool.map(one, seeds))
-    return np.array([a for a, _ in res]), np.array([b for _, b in res])
-
-
-def cpu_time(rounds, n1, workers, seeds):
-    import oracle
-    ref = oracle.load("ref", abi.RNG_XOSHIRO)
-    tg = abi.gaussian_shift(0.0, 1.0, 1.0, 10)
-    k = abi.kernel(abi.KERNEL_RWMH)
+def wall(fn, reps):
     ts = []
-    for s in seeds:
+    for i in range(reps):
         t0 = time.perf_counter()
-        ref.run_rounds(tg, k, abi.MODE_SAIS, n1, rounds, seed=int(s), workers=workers)
+        fn(i)
         ts.append(time.perf_counter() - t0)
-    return float(np.mean(ts))
+    return float(np.median(ts))
 
 
-def measure(n_seeds=1000, target=0.05, rounds=6, n1=1 << 14, cpu_seeds=3, timing_seeds=20):
-    out = {"config": "config1: SAIS d=10 Gaussian shift (log Z = 0), RWMH {0.1,1,10}, N1=2^14, doubling rounds",
-           "target_rel_var": target, "seeds": n_seeds}
-    # estimator statistics over all seeds: concurrent streams (replicas overlap on the
-    # device); the time-to-target itself: CUDA-event round times of uncontended runs
+def cpu_ref():
+    import oracle
+    return oracle.load("ref_release") if oracle.available("ref_release") else oracle.load("ref", XO)
+
+
+IDEAL = abi.kernel(abi.KERNEL_IDEALIZED)
+
+CONFIGS = {
+    # target, mode, n1, max rounds, exec, seeds batched on the device?, target rel-var, kernel
+    "1": dict(name="config1: SAIS d=10 Gaussian shift (log Z = 0), RWMH {0.1,1,10}, N1=2^14",
+            target=lambda: abi.gaussian_shift(0.0, 1.0, 1.0, 10), mode=abi.MODE_SAIS, n1=1 << 14, rounds=6,
+            ex=lambda: abi.execopts(XO, F64, lanes=1), batched=True, rv=0.05, kernel=RWMH),
+    # config 2's RWMH {0.1, 1, 10} cannot follow the annealed scale in d = 1000 within
+    # reachable T (log Z-hat ~ -250, seed-dominated: DESIGN.md 3.10); the same target with
+    # the reference's idealized kernel gives the schedule-limited time to target
+    "2": dict(name="config2: SAIS d=1000 scale-mismatch Gaussian (log Z = 0), RWMH {0.1,1,10}, N1=2^14",
+              target=lambda: abi.scale_gaussian(1.0, 2.0, 1000), mode=abi.MODE_SAIS, n1=1 << 14, rounds=8,
+              ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=RWMH),
+    "2i": dict(name="config2 target, idealized kernel (exact pi_beta draws), N1=2^12",
+               target=lambda: abi.scale_gaussian(1.0, 2.0, 1000), mode=abi.MODE_SAIS, n1=1 << 12, rounds=10,
+               ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=IDEAL),
+    "3": dict(name="config3: SSMC adaptive-ESS d=100 mixture (log Z = 0), RWMH {0.1,1,10}, N1=2^16",
+              target=lambda: abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100), mode=abi.MODE_SSMC, n1=1 << 16,
+              rounds=8, ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=RWMH),
+}
+
+
+def sais_levels(cfg, seeds, timing_reps=5):
+    """rel-var and per-seed wall time of every round-loop level on the B200."""
+    from paper_2408_12057_b200 import capi
+    tg, ex, R, K = cfg["target"](), cfg["ex"](), cfg["rounds"], cfg["kernel"]
+    out = {"seeds": len(seeds)}
     t0 = time.perf_counter()
-    lz, _ = gpu_runs(range(1, n_seeds + 1), rounds, n1, abi.RNG_XOSHIRO, abi.PREC_FP64, streams=16)
-    out["all_seeds_wall_seconds"] = time.perf_counter() - t0
-    _, wall = gpu_runs(range(1, timing_seeds + 1), rounds, n1, abi.RNG_XOSHIRO, abi.PREC_FP64, streams=1)
-    rv = [rel_var(lz[:, k]) for k in range(rounds)]
-    out["rel_var_by_round"] = rv
-    hit = [k for k in range(rounds) if rv[k] <= target]
-    if not hit:
-        out["reached"] = False
-        return out
-    ks = hit[0]
-    out.update(reached=True, rounds_needed=ks + 1,
-               b200_seconds=float(np.mean(np.sum(wall[:, : ks + 1], axis=1))))
-    lz32, _ = gpu_runs(range(1, n_seeds + 1), rounds, n1, abi.RNG_PHILOX, abi.PREC_FP32, streams=16)
-    _, wall32 = gpu_runs(range(1, timing_seeds + 1), rounds, n1, abi.RNG_PHILOX, abi.PREC_FP32, streams=1)
-    rv32 = [rel_var(lz32[:, k]) for k in range(rounds)]
-    hit32 = [k for k in range(rounds) if rv32[k] <= target]
-    out["philox_fp32"] = {"rel_var_by_round": rv32,
-                          "rounds_needed": hit32[0] + 1 if hit32 else None,
-                          "b200_seconds": float(np.mean(np.sum(wall32[:, : hit32[0] + 1], axis=1)))
-                          if hit32 else None}
-    workers = os.cpu_count() or 1
-    out["cpu_seconds"] = cpu_time(ks + 1, n1, workers, range(1, cpu_seeds + 1))
-    out["cpu_seconds_1core"] = cpu_time(ks + 1, n1, 1, range(1, 2))
-    out["cpu_cores"] = workers
-    out["cpu_kind"] = "reference (oracle/_ref, unmodified run_sais)"
-    out["speedup_vs_cpu_all_cores"] = out["cpu_seconds"] / out["b200_seconds"]
+    if cfg["batched"]:
+        b = capi.run_sais_seeds(tg, K, cfg["n1"], R, seeds, exec_=ex)
+        lz = b["log_z_hat"]
+        out["batched_wall_s"] = time.perf_counter() - t0
+        out["batched_device_s_by_round"] = [float(v) for v in b["wall_seconds"]]
+    else:
+        lz = np.array([capi.run_rounds(tg, K, cfg["mode"], cfg["n1"], R, seed=int(s), exec_=ex)["log_z_hat"]
+                       for s in seeds])
+        out["sequential_wall_s"] = time.perf_counter() - t0
+    out["rel_var_by_round"] = [rel_var(lz[:, k]) for k in range(R)]
+    out["log_z_mean_by_round"] = [float(np.mean(lz[:, k])) for k in range(R)]
+    capi.run_rounds(tg, K, cfg["mode"], cfg["n1"], 1, seed=99, exec_=ex)  # warm-up
+    out["b200_wall_s_by_round"] = [
+        wall(lambda i, k=k: capi.run_rounds(tg, K, cfg["mode"], cfg["n1"], k + 1, seed=int(seeds[i]), exec_=ex),
+             timing_reps) for k in range(R)]
+    if cfg["batched"]:
+        out["b200_batched_wall_s_per_seed_by_round"] = []
+        for k in range(R):
+            t0 = time.perf_counter()
+            capi.run_sais_seeds(tg, K, cfg["n1"], k + 1, seeds, exec_=ex)
+            out["b200_batched_wall_s_per_seed_by_round"].append((time.perf_counter() - t0) / len(seeds))
     return out
 
 
+def first_hit(rv, target):
+    for k, v in enumerate(rv):
+        if v <= target:
+            return k
+    return None
+
+
+def measure_config(c, n_seeds, cpu_reps=3):
+    cfg = CONFIGS[c]
+    seeds = np.arange(1, n_seeds + 1, dtype=np.uint64)
+    res = {"config": cfg["name"], "target_rel_var": cfg["rv"]}
+    res.update(sais_levels(cfg, seeds))
+    k = first_hit(res["rel_var_by_round"], cfg["rv"])
+    res["reached"] = k is not None
+    if k is None:
+        return res
+    workers = os.cpu_count() or 1
+    ref, tg = cpu_ref(), cfg["target"]()
+    cpu = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], cfg["n1"], k + 1, seed=int(seeds[i]),
+                                        workers=workers), cpu_reps)
+    res["time_to_target"] = {
+        "rounds_needed": k + 1, "b200_wall_s": res["b200_wall_s_by_round"][k], "cpu_wall_s": cpu,
+        "cpu_cores": workers, "cpu_kind": "reference (unmodified run_sais/run_ssmc, -O3)",
+        "speedup_wall": cpu / res["b200_wall_s_by_round"][k]}
+    if cfg["batched"]:
+        res["time_to_target"]["b200_batched_wall_s_per_seed"] = res["b200_batched_wall_s_per_seed_by_round"][k]
+    return res
+
+
+def zja_vs_sais(n_seeds_sais=1000, n_seeds_zja=200, target=0.05, Ts=(2, 4, 8, 16, 32), timing_reps=5):
+    """The paper's GPU experiment on the config-1 family: 2^14
+    particles, SAIS effort = rounds, ZJA effort = T via delta* = (Lambda / T)^2."""
+    from paper_2408_12057_b200 import capi
+    cfg = CONFIGS[1]
+    tg, n = cfg["target"](), 1 << 14
+    ex = abi.execopts(PH, F32, lanes=1)  # both samplers in the throughput mode
+    out = {"config": "config1 family (d=10 Gaussian shift), 2^14 particles, philox/fp32", "target_rel_var": target}
+    seeds = np.arange(1, n_seeds_sais + 1, dtype=np.uint64)
+    b = capi.run_sais_seeds(tg, RWMH, n, 6, seeds, exec_=ex)
+    lam = float(np.mean(b["lambda_total"][:, -1]))
+    out["lambda_hat"] = lam
+    rv_s = [rel_var(b["log_z_hat"][:, k]) for k in range(6)]
+    capi.run_rounds(tg, RWMH, abi.MODE_SAIS, n, 1, seed=99, exec_=ex)
+    t_s = [wall(lambda i, k=k: capi.run_rounds(tg, RWMH, abi.MODE_SAIS, n, k + 1, seed=int(seeds[i]), exec_=ex),
+                timing_reps) for k in range(6)]
+    out["sais"] = {"rel_var_by_round": rv_s, "wall_s_by_round": t_s}
+    zs = {"T": list(Ts), "delta_star": [], "rel_var": [], "wall_s": [], "steps_mean": []}
+    capi.run_zja(tg, RWMH, n, delta_star=(lam / 4) ** 2, seed=99, exec_=ex)
+    for T in Ts:
+        ds = (lam / T) ** 2
+        lz, steps = [], []
+        for s in range(1, n_seeds_zja + 1):
+            z = capi.run_zja(tg, RWMH, n, delta_star=ds, seed=s, exec_=ex)
+            lz.append(z["rounds"][-1]["log_z_hat"])
+            steps.append(z["steps"])
+        zs["delta_star"].append(ds)
+        zs["rel_var"].append(rel_var(lz))
+        zs["steps_mean"].append(float(np.mean(steps)))
+        zs["wall_s"].append(wall(lambda i, ds=ds: capi.run_zja(tg, RWMH, n, delta_star=ds, seed=int(i + 1), exec_=ex),
+                                 timing_reps))
+    out["zja"] = zs
+    ks, kz = first_hit(rv_s, target), first_hit(zs["rel_var"], target)
+    out["sais_time_to_target_s"] = t_s[ks] if ks is not None else None
+    out["zja_time_to_target_s"] = zs["wall_s"][kz] if kz is not None else None
+    if ks is not None and kz is not None:
+        out["zja_over_sais"] = out["zja_time_to_target_s"] / out["sais_time_to_target_s"]
+        # the same two effort levels on the host CPU (reference Philox build: same streams)
+        import oracle
+        ref = oracle.load("ref", PH) if oracle.available("ref", PH) else None
+        if ref is not None:
+            workers = os.cpu_count() or 1
+            cs = wall(lambda i: ref.run_rounds(tg, RWMH, abi.MODE_SAIS, n, ks + 1, seed=i + 1, workers=workers), 3)
+            cz = wall(lambda i: ref.run_zja(tg, RWMH, n, delta_star=zs["delta_star"][kz], seed=i + 1,
+                                            workers=workers), 3)
+            out["cpu"] = {"cores": workers, "sais_wall_s": cs, "zja_wall_s": cz, "zja_over_sais": cz / cs,
+                          "kind": "reference Philox build (oracle/_ref/libasmc_ref_philox.so, -O2)"}
+    return out
+
+
+def measure(n_seeds=1000):
+    """bench.py's time_to_target field: config 1 (batched seeds, wall clock both sides)."""
+    return measure_config("1", n_seeds)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,2i,3")
+    ap.add_argument("--seeds", type=int, default=1000)
+    ap.add_argument("--seeds-slow", type=int, default=32, help="seeds for the configs run one seed at a time")
+    ap.add_argument("--zja", action="store_true")
+    a = ap.parse_args()
+    res = {}
+    for c in [v for v in a.configs.split(",") if v]:
+        res[f"config{c}"] = measure_config(c, a.seeds if CONFIGS[c]["batched"] else a.seeds_slow)
+        print(json.dumps({f"config{c}": res[f"config{c}"]}), flush=True)
+    if a.zja:
+        res["zja_vs_sais"] = zja_vs_sais()
+        print(json.dumps({"zja_vs_sais": res["zja_vs_sais"]}), flush=True)
+
+
 if __name__ == "__main__":
-    import json
-    print(json.dumps(measure(), indent=1))
+    main()
