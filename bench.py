@@ -267,31 +267,82 @@ def other_cpu_baselines():
     return out
 
 
-def other_configs(stream, ex):
+def reference_arithmetic(stream, n1=1 << 16):
+    """Config 2 in the device's reference mode (keyed xoshiro streams, fp64, one lane per
+    particle, the reference's operation order): the cost of the reference's own
+    arithmetic on the B200, beside the fp32/Philox headline (bounded N1)."""
+    import torch
+    from paper_2408_12057_b200 import capi
+    tg = abi.scale_gaussian(SIGMA0, SIGMA1, D)
+    k = abi.kernel(abi.KERNEL_RWMH, STEPS, 1)
+    ex64 = abi.execopts(abi.RNG_XOSHIRO, abi.PREC_FP64, stream=stream.cuda_stream)
+    capi.run_rounds(tg, k, abi.MODE_SAIS, 1 << 10, 2, seed=SEED, exec_=ex64)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    r = capi.run_rounds(tg, k, abi.MODE_SAIS, n1, ROUNDS, seed=SEED, exec_=ex64)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dt = e0.elapsed_time(e1) * 1e-3
+    ps = float(np.sum(r["kernel_applications"]))
+    return {"workload": f"config2 shape (d={D}, 4 rounds) with N1={n1}", "rng": "keyed xoshiro256++",
+            "precision": "fp64, reference operation order", "value": ps / dt, "unit": "particle-steps/s",
+            "device_s": dt, "psteps": ps}
+
+
+ISSUE_PEAK = 148 * 4 * 32 * 1.965e9  # thread-instructions/s at the max SM clock (SURVEY 8d)
+
+
+def other_configs(stream, ex, peak_normals, peaks):
     """BASELINE.json configs 3-5 on this GPU (single-GPU shapes), device time by CUDA
-    events on the library's stream; inputs resident, one warm-up each."""
+    events on the library's stream; inputs resident, one warm-up each.  Each carries the
+    roofline of its dominant kernel and an e2e wall-clock figure through the
+    public call (host buffers in and out)."""
     import torch
     from paper_2408_12057_b200 import capi, exact
     out = {}
 
-    def timed(fn):
+    def timed(fn, prof=False):
         fn()  # warm-up (JIT-free, but first-touch of pools / data upload)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if prof:
+            capi.profile_enable(True)
+        t0 = time.perf_counter()
         e0.record(stream)
         r = fn()
         e1.record(stream)
         torch.cuda.synchronize()
-        return r, e0.elapsed_time(e1) * 1e-3
+        wall = time.perf_counter() - t0
+        pr = None
+        if prof:
+            pr = capi.profile_collect()
+            capi.profile_enable(False)
+        return r, e0.elapsed_time(e1) * 1e-3, wall, pr
 
     # config 3: SSMC, adaptive ESS, d=100 bimodal mixture, N=2^22, 6 rounds
     tg = abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100)
     k = abi.kernel(abi.KERNEL_RWMH, STEPS, 1)
-    r, dt = timed(lambda: capi.run_rounds(tg, k, abi.MODE_SSMC, 1 << 22, 6, policy=abi.POLICY_ADAPTIVE_ESS,
-                                          seed=SEED, exec_=ex))
+    r, dt, wall, (pms, pnorm) = timed(lambda: capi.run_rounds(tg, k, abi.MODE_SSMC, 1 << 22, 6,
+                                                             policy=abi.POLICY_ADAPTIVE_ESS, seed=SEED, exec_=ex),
+                                      prof=True)
     ps = float(np.sum(r["kernel_applications"]))
+    pass_s = float(np.sum(pms)) * 1e-3
+    ach = float(np.sum(pnorm)) / pass_s
     out["config3"] = {"workload": "SSMC adaptive-ESS (rho 0.5) d=100 mixture, N1=2^22, 6 rounds, RWMH [0.1,1,10]",
                       "psteps": ps, "device_s": dt, "value": ps / dt, "unit": "particle-steps/s",
+                      "e2e": {"value": ps / wall, "unit": "particle-steps/s", "wall_s": wall,
+                              "path": "C-ABI asmc_run_rounds (run_ssmc), host outputs"},
+                      "roofline": {"bound": "issue", "kernel": "pass_smem_kernel<TgtMixture, 4> (SMC step mode)",
+                                   "achieved": ach / 1e9, "peak": peak_normals / 1e9, "unit": "Gnormal/s",
+                                   "frac": ach / peak_normals, "pass_share_of_device_time": pass_s / dt,
+                                   "algorithmic_units": "normals = N*d per init + N*S*d per step (no early "
+                                                        "rejection on the mixture: drawn = algorithmic)",
+                                   "hbm": {"bytes_per_pstep": 8 * 100 + 16,
+                                           "achieved_gbs": ps * (8 * 100 + 16) / pass_s / 1e9,
+                                           "peak": peaks.get("hbm_gbs"),
+                                           "frac": ps * (8 * 100 + 16) / pass_s / 1e9 / peaks.get("hbm_gbs", 6543.1),
+                                           "note": "step mode loads and stores each fp32 row (8d) and log-w (16 B)"}},
                       "resampling_events": int(np.sum(r["resampled"])),
                       "last_log_z_hat": float(r["log_z_hat"][-1]), "exact_log_z": 0.0}
     # config 4: SAIS Bayesian logistic regression, X 1e5 x 256, N=2^20 (tensor cores)
@@ -299,27 +350,45 @@ def other_configs(stream, ex):
     tg = abi.logistic(X, y, 1.0)
     k = abi.kernel(abi.KERNEL_RWMH, (0.002, 0.005, 0.01), 1)
     betas = np.linspace(0.0, 1.0, 5)
-    capi.profile_enable(True)
-    r, dt = timed(lambda: capi.run_sais_single(tg, k, betas, 1 << 20, seed=SEED, round=1, exec_=ex))
-    ms, flops = capi.profile_collect()
-    capi.profile_enable(False)
-    n_ev = len(ms) // 2
-    ev_ms, ev_flops = float(np.sum(ms[n_ev:])), float(np.sum(flops[n_ev:]))
-    out["config4"] = {"workload": "SAIS logistic regression n=1e5 d=256, N=2^20, T=4, RWMH x3 (split-bf16 tcgen05)",
+    r, dt, wall, (ms, flops) = timed(lambda: capi.run_sais_single(tg, k, betas, 1 << 20, seed=SEED, round=1,
+                                                                   exec_=ex), prof=True)
+    ev_ms, ev_flops = float(np.sum(ms)), float(np.sum(flops))
+    alg_tf = ev_flops / (ev_ms * 1e-3) / 1e12
+    sus = peaks.get("bf16_tflops_sustained", 1398.3)
+    out["config4"] = {"workload": "SAIS logistic regression n=1e5 d=256 (general fp32 X), N=2^20, T=4, RWMH x3 "
+                                  "(split-bf16 tcgen05)",
                       "psteps": float((1 << 20) * 4), "device_s": dt, "value": (1 << 20) * 4 / dt,
-                      "unit": "particle-steps/s", "likelihood_tflops_algorithmic": ev_flops / (ev_ms * 1e-3) / 1e12,
-                      "tensor_tflops_issued": 3 * ev_flops / (ev_ms * 1e-3) / 1e12}
+                      "unit": "particle-steps/s",
+                      "e2e": {"value": (1 << 20) * 4 / wall, "unit": "particle-steps/s", "wall_s": wall,
+                              "path": "C-ABI asmc_run_sais_single, host X/y in, host report out"},
+                      "roofline": {"bound": "tensor", "kernel": "lg_eval_kernel (tcgen05.mma cta_group::2)",
+                                   "achieved": alg_tf, "peak": sus, "unit": "TFLOP/s", "frac": alg_tf / sus,
+                                   "issued_tflops": 3 * alg_tf, "issued_frac": 3 * alg_tf / sus,
+                                   "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside "
+                                                  "a long step)",
+                                   "algorithmic_units": "2 n d flop per particle-proposal (X theta'); the 3-MMA "
+                                                        "split-bf16 scheme issues 3x",
+                                   "likelihood_share_of_device_time": ev_ms * 1e-3 / dt}}
     # config 5: SAIS relaxed Ising 64x64 at K_c, HMC, schedule adaptation over 12 doubling
     # rounds ending at N = 2^18 (N1 = 5793: the budget rule's sqrt(2) growth)
     tg = abi.ising(64, exact.K_CRITICAL, 1.0, 1.0)
     k = abi.kernel(abi.KERNEL_HMC, (0.25,), 1, leapfrog=10)
-    r, dt = timed(lambda: capi.run_rounds(tg, k, abi.MODE_SAIS, 5793, 12, seed=SEED, exec_=ex))
+    r, dt, wall, _ = timed(lambda: capi.run_rounds(tg, k, abi.MODE_SAIS, 5793, 12, seed=SEED, exec_=ex))
     ps = float(np.sum(r["kernel_applications"]))
     steps = [int(v) for v in r["steps"]]
+    sg = ps * 11 * 4096 / dt
     out["config5"] = {"workload": "SAIS relaxed Ising 64x64 K=K_c, HMC eps 0.25 x 10 leapfrog, 12 adaptive rounds, "
                                   "N 5793 -> 2^18, T 1 -> 104",
                       "psteps": ps, "device_s": dt, "value": ps / dt, "unit": "particle-steps/s",
-                      "site_gradients_per_s": ps * 11 * 4096 / dt,
+                      "site_gradients_per_s": sg,
+                      "e2e": {"value": ps / wall, "unit": "particle-steps/s", "wall_s": wall,
+                              "path": "C-ABI asmc_run_rounds (run_sais), host outputs"},
+                      "roofline": {"bound": "issue", "kernel": "is_tile_kernel<64> (HMC leapfrog, 4x4 tiles)",
+                                   "achieved": sg / 1e12, "peak": ISSUE_PEAK / 20 / 1e12,
+                                   "unit": "Tsite-gradient/s", "frac": sg / (ISSUE_PEAK / 20),
+                                   "peak_source": "derived: 148 SMs x 4 schedulers x 32 lanes x 1.965 GHz over "
+                                                  "the 20 thread-instructions of one site-gradient (leapfrog loop "
+                                                  "SASS, DESIGN.md 3.7); achieved over the whole device time"},
                       "n_final": int(r["n_particles"][-1]), "T": steps,
                       "lambda_hat": [float(r["lambda_"][i][steps[i]]) for i in range(len(steps))],
                       "log_z_hat": [float(v) for v in r["log_z_hat"]],
@@ -359,6 +428,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # the NCCL INIT lines show the ranks and transports
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -498,7 +568,8 @@ def main():
             line["cpu_baseline"] = cpu
         if world == 1 and not args.no_configs:
             try:
-                line["other_configs"] = other_configs(stream, ex)
+                line["other_configs"] = other_configs(stream, ex, peak_normals, peaks)
+                line["reference_arithmetic"] = reference_arithmetic(stream)
                 if not args.no_cpu_baseline:
                     for key, v in other_cpu_baselines().items():
                         line["other_configs"][key]["cpu_baseline"] = v

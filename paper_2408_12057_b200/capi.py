@@ -179,6 +179,26 @@ def sais_partials(target, kernel, betas, n, p_begin, p_end, seed=0, round=0, exe
     return out[:nch]
 
 
+def sais_partials_dev(target, kernel, betas, n, p_begin, p_end, out_ptr, seed=0, round=0, exec_=None):
+    """asmc_sais_partials_dev: this rank's chunk partials written to a DEVICE buffer
+    (out_ptr, e.g. a float64 tensor of shape (chunks, T+1, 4, 2)) on exec_.stream."""
+    betas = np.ascontiguousarray(betas, dtype=np.float64)
+    T = len(betas) - 1
+    ex = exec_ or abi.execopts(abi.RNG_PHILOX, abi.PREC_FP32)
+    _check(lib().asmc_sais_partials_dev(C.byref(target), C.byref(kernel), _arr(betas, C.c_double),
+                                        C.c_int32(T), C.c_uint64(n), C.c_uint64(p_begin), C.c_uint64(p_end),
+                                        C.c_uint64(seed), C.c_uint64(round), C.byref(ex), C.c_void_p(out_ptr)))
+
+
+def fold_partials_dev(partials_ptr, chunks, T, n, exec_=None):
+    """asmc_fold_partials_dev: fold all-gathered DEVICE partials on the GPU."""
+    rep, bufs = _report(T)
+    ex = exec_ or abi.execopts(abi.RNG_PHILOX, abi.PREC_FP32)
+    _check(lib().asmc_fold_partials_dev(C.c_void_p(partials_ptr), C.c_uint64(chunks), C.c_int32(T),
+                                        C.c_uint64(n), C.byref(ex), C.byref(rep)))
+    return _finish(rep, bufs, False)
+
+
 def fold_partials(partials, n):
     partials = np.ascontiguousarray(partials, dtype=np.float64)
     chunks, T1 = partials.shape[0], partials.shape[1]
@@ -487,7 +507,7 @@ class ZjaShard(SmcShard):
 EXPORTED = [
     "asmc_last_error", "asmc_version", "asmc_device_count", "asmc_launch_count", "asmc_run_smc",
     "asmc_run_sais_single", "asmc_run_rounds", "asmc_run_sais_seeds", "asmc_fold_chunks", "asmc_sais_partials",
-    "asmc_fold_partials", "asmc_rng_u64", "asmc_rng_uniform", "asmc_rng_normal",
+    "asmc_fold_partials", "asmc_sais_partials_dev", "asmc_fold_partials_dev", "asmc_rng_u64", "asmc_rng_uniform", "asmc_rng_normal",
     "asmc_trajectories", "asmc_systematic_resample", "asmc_resample_cdf", "asmc_logsumexp",
     "asmc_exact_math", "asmc_ess", "asmc_barrier_estimate",
     "asmc_generate_schedule", "asmc_local_barrier", "asmc_budget", "asmc_profile_enable",

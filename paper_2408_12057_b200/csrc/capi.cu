@@ -1375,9 +1375,10 @@ uint64_t asmc_fold_chunks(uint64_t p_begin, uint64_t p_end) {
   return (p_end - p_begin + ASMC_FOLD_CHUNK - 1) / ASMC_FOLD_CHUNK;
 }
 
-int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
-                       const double* betas, int32_t T, uint64_t n, uint64_t p_begin, uint64_t p_end,
-                       uint64_t seed, uint64_t round, const asmc_exec* exec, asmc_logacc* partials) {
+static int sais_partials_impl(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                              const double* betas, int32_t T, uint64_t n, uint64_t p_begin, uint64_t p_end,
+                              uint64_t seed, uint64_t round, const asmc_exec* exec, asmc_logacc* partials,
+                              bool device_out) {
   TRY(check_schedule(betas, T));
   TRY(check_pair(target, kernel));
   if (p_begin % ASMC_FOLD_CHUNK != 0)
@@ -1386,8 +1387,18 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
   const asmc_exec ex = exec ? *exec : default_exec();
   if (ex.precision == ASMC_PREC_FP64)
     return fail(ASMC_ERR_CAPABILITY, "sharded partials use the fp32 tree fold; fp64 reference order is single-GPU");
-  if (target->kind == ASMC_TARGET_LOGISTIC || target->kind == ASMC_TARGET_ISING)
-    return stepouter_partials(target, kernel, betas, T, p_begin, p_end, seed, round, ex, partials);
+  if (target->kind == ASMC_TARGET_LOGISTIC || target->kind == ASMC_TARGET_ISING) {
+    if (!device_out) return stepouter_partials(target, kernel, betas, T, p_begin, p_end, seed, round, ex, partials);
+    // step-outer engines produce host partials; stage them into the caller's device buffer
+    const uint64_t nch = asmc_fold_chunks(p_begin, p_end);
+    std::vector<asmc_logacc> h(nch * (uint64_t)(T + 1) * 4);
+    TRY(stepouter_partials(target, kernel, betas, T, p_begin, p_end, seed, round, ex, h.data()));
+    DevCtx* C;
+    TRY(get_ctx(ex.device, &C, ex.stream));
+    CU(cudaMemcpyAsync(partials, h.data(), h.size() * sizeof(asmc_logacc), cudaMemcpyHostToDevice, C->stream));
+    CU(cudaStreamSynchronize(C->stream));
+    return 0;
+  }
   Layout L;
   TRY(choose_layout(ex, kernel->kind, target->dim, &L, 1, 4));  // long T runs in t-tiles
   DevCtx* C;
@@ -1420,6 +1431,13 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
   DBuf<double> lwb;
   TRY(launch_sais_pass(C, ex, L, A, nblk, T, xs, xbuf, xcur, lwb));
   LCH(launch_fold_chunks(part.p, nblk, nblk, 1, T, 4, nch, chunk.p, C->stream));
+  if (device_out) {  // partials stay on the device: the caller all-gathers them there
+    LCH(launch_chunks_to_exchange(chunk.p, nch, T, reinterpret_cast<LogAcc*>(partials), C->stream));
+    int herr = 0;
+    CU(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaStreamSynchronize(C->stream));
+    return device_error(herr, 0, 0.0);
+  }
   std::vector<LogAcc> h((size_t)(T + 1) * kNAcc * nch);
   CU(cudaMemcpyAsync(h.data(), chunk.p, h.size() * sizeof(LogAcc), cudaMemcpyDeviceToHost, C->stream));
   int herr = 0;
@@ -1432,6 +1450,42 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
         const LogAcc v = t == 0 ? LogAcc{-HUGE_VAL, 0.0} : h[((size_t)t * kNAcc + a) * nch + c];
         partials[(c * (T + 1) + t) * 4 + a] = asmc_logacc{v.max, v.sum};
       }
+  return 0;
+}
+
+int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                       const double* betas, int32_t T, uint64_t n, uint64_t p_begin, uint64_t p_end,
+                       uint64_t seed, uint64_t round, const asmc_exec* exec, asmc_logacc* partials) {
+  return sais_partials_impl(target, kernel, betas, T, n, p_begin, p_end, seed, round, exec, partials, false);
+}
+
+int asmc_sais_partials_dev(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                           const double* betas, int32_t T, uint64_t n, uint64_t p_begin, uint64_t p_end,
+                           uint64_t seed, uint64_t round, const asmc_exec* exec, asmc_logacc* partials_dev) {
+  if (!partials_dev) return fail(ASMC_ERR_INVALID_ARGUMENT, "null partials buffer");
+  return sais_partials_impl(target, kernel, betas, T, n, p_begin, p_end, seed, round, exec, partials_dev, true);
+}
+
+// the device fold of all-gathered partials (device buffer, exchange layout): the same
+// fold_chunks_final order as asmc_fold_partials, no host copy of the partials
+int asmc_fold_partials_dev(const asmc_logacc* partials_dev, uint64_t chunks, int32_t T, uint64_t n,
+                           const asmc_exec* exec, asmc_report* out) {
+  if (T < 1 || chunks == 0 || !partials_dev) return fail(ASMC_ERR_INVALID_ARGUMENT, "nothing to fold");
+  const asmc_exec ex = exec ? *exec : default_exec();
+  DevCtx* C;
+  TRY(get_ctx(ex.device, &C, ex.stream));
+  DBuf<LogAcc> chunk, tot;
+  TRY(chunk.alloc((size_t)(T + 1) * kNAcc * chunks, C->stream));
+  TRY(tot.alloc((size_t)(T + 1) * kNAcc, C->stream));
+  LCH(launch_exchange_to_chunks(reinterpret_cast<const LogAcc*>(partials_dev), chunks, T, chunk.p, C->stream));
+  RoundBufs R;
+  TRY(R.alloc(T, C->stream));
+  LCH(launch_fold_chunks_final(chunk.p, chunks, 1, T, 4, tot.p, C->stream));
+  LCH(launch_sais_report(tot.p, T, n, R.rd.p, C->stream));
+  SmcState st;
+  TRY(copy_round(C->stream, R, T, false, out, &st));
+  TRY(device_error(st.err, st.err_step, st.err_val));
+  out->kernel_applications = n * (uint64_t)T;
   return 0;
 }
 

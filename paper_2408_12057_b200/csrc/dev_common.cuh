@@ -91,6 +91,15 @@ __device__ __forceinline__ LogAcc shfl_xor_acc(const LogAcc& v, int m, unsigned 
   return LogAcc{__shfl_xor_sync(mask, v.max, m), __shfl_xor_sync(mask, v.sum, m)};
 }
 
+// Block-uniform read of the error word at kernel entry: thread 0 reads it and the CTA
+// agrees.  A per-thread read could split a block when another CTA of the same launch
+// raises the error meanwhile (e.g. a zero density in ExactT::weight), leaving the
+// threads that stayed waiting at a barrier the others never reach.
+__device__ __forceinline__ bool block_err_set(const int* err) {
+  if (!err) return false;
+  return __syncthreads_or(threadIdx.x == 0 ? *(volatile const int*)err : 0) != 0;
+}
+
 // Error word: the first failing particle records its code (ASMC_ERR_*).
 __device__ __forceinline__ void raise_error(int* err, int code) {
   if (err) atomicCAS(err, 0, code);

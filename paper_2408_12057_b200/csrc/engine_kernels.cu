@@ -722,6 +722,34 @@ __global__ void pack_rows_kernel(const uint32_t* anc, uint64_t count, uint64_t p
   }
 }
 
+// SAIS chunk partials between the fold layout chunk[(t * kNAcc + a) * nch + c] and the
+// exchange layout x[(c * (T + 1) + t) * 4 + a] (include/asmc_b200.h, asmc_sais_partials),
+// on the device (multi-GPU SAIS keeps its partials out of host memory)
+__global__ void chunks_to_exchange_kernel(const LogAcc* chunk, uint64_t nch, int T, LogAcc* x) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nch * (uint64_t)(T + 1) * 4) return;
+  const int a = (int)(i % 4), t = (int)((i / 4) % (T + 1));
+  const uint64_t c = i / (4 * (uint64_t)(T + 1));
+  x[i] = t == 0 ? LogAcc{kNegInf, 0.0} : chunk[((size_t)t * kNAcc + a) * nch + c];
+}
+__global__ void exchange_to_chunks_kernel(const LogAcc* x, uint64_t nch, int T, LogAcc* chunk) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nch * (uint64_t)(T + 1) * kNAcc) return;
+  const uint64_t c = i % nch;
+  const int a = (int)((i / nch) % kNAcc), t = (int)(i / (nch * kNAcc));
+  chunk[i] = (t == 0 || a >= 4) ? LogAcc{kNegInf, 0.0} : x[(c * (uint64_t)(T + 1) + t) * 4 + a];
+}
+cudaError_t launch_chunks_to_exchange(const LogAcc* chunk, uint64_t nch, int T, LogAcc* x, cudaStream_t s) {
+  const uint64_t n = nch * (uint64_t)(T + 1) * 4;
+  chunks_to_exchange_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(chunk, nch, T, x);
+  return LAUNCH_OK();
+}
+cudaError_t launch_exchange_to_chunks(const LogAcc* x, uint64_t nch, int T, LogAcc* chunk, cudaStream_t s) {
+  const uint64_t n = nch * (uint64_t)(T + 1) * kNAcc;
+  exchange_to_chunks_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, nch, T, chunk);
+  return LAUNCH_OK();
+}
+
 cudaError_t launch_chunk_major(const LogAcc* in, uint64_t nch, LogAcc* out, cudaStream_t s) {
   const uint64_t n = nch * kNAcc;
   chunk_major_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(in, nch, out);

@@ -92,6 +92,10 @@ cudaError_t launch_rng(int rng, int what, int precision, const uint64_t key[5], 
 cudaError_t launch_peak_normals(int blocks, uint64_t quads_per_thread, float* sink, cudaStream_t s);
 cudaError_t launch_ess(const double* lw, uint64_t n, double* out, int* err, cudaStream_t s);
 
+// ---- multi-GPU SAIS: chunk partials <-> exchange layout, on the device ----
+cudaError_t launch_chunks_to_exchange(const LogAcc* chunk, uint64_t nch, int T, LogAcc* x, cudaStream_t s);
+cudaError_t launch_exchange_to_chunks(const LogAcc* x, uint64_t nch, int T, LogAcc* chunk, cudaStream_t s);
+
 // ---- sharded SSMC (one particle shard per GPU) ----
 // per-shard chunk partials [a][c] -> exchange layout [c][a]
 cudaError_t launch_chunk_major(const LogAcc* in, uint64_t nch, LogAcc* out, cudaStream_t s);

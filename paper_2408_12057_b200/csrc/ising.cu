@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(4 * L, L == 64 ? 3 : 4) is_move_kernel(const I
   using Cta = IsCta<L>;
   constexpr int R = Cta::R, N = Cta::N;
   extern __shared__ float is_smem[];
-  if (A.err && *(volatile int*)A.err) return;
+  if (block_err_set(A.err)) return;
   Cta C;
   C.Sy = is_smem;
   C.Sv = is_smem + N;
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(L * L / 16, L == 64 ? 3 : 8) is_tile_kernel(co
   using Cta = IsTile<L>;
   constexpr int N = Cta::N;
   extern __shared__ float4 is_tsmem[];
-  if (A.err && *(volatile int*)A.err) return;
+  if (block_err_set(A.err)) return;
   Cta C;
   C.E = is_tsmem;
   C.Y0 = is_tsmem + 4 * Cta::TA * Cta::TPR;

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kBlock) lg_weight_kernel(LgArgs A, const doubl
   __shared__ double s_lw[kBlock], s_lg[kBlock], s_post[kBlock];
   __shared__ int s_act[kBlock];
   __shared__ LogAcc s_dst[kNAcc];
-  if (A.err && *(volatile int*)A.err) return;
+  if (block_err_set(A.err)) return;
   const double b0 = betas[t - 1], b1 = betas[t];
   const uint64_t local = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
   const bool active = local < A.n_local;
@@ -229,6 +229,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LG_THREADS, 1)
   const uint32_t crank = cluster_rank();  // 0 = pair leader (issues the MMAs)
   const uint64_t p0 = (uint64_t)blockIdx.x * LG_M;  // pair (blockIdx.x / 2) holds 256 particles
   const int d = A.d;
+  // per-thread read, cluster-safe: nothing in this launch raises the word before this
+  // point except the alignment check below, which every CTA takes alike
   if (A.err && *(volatile int*)A.err) return;
   if (smem_u32(smem_raw) & 1023u) {  // uniform across the CTA: fail loudly, never mis-swizzle
     if (tid == 0) raise_error(A.err, ASMC_ERR_CUDA);

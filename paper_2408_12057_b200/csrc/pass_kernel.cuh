@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
   const double* betas = A.betas + si * A.betas_stride;
   LogAcc* part = A.part + si * A.part_seed_stride;
   const int nacc = mode_nacc(A.mode);
-  if (A.err && *(volatile int*)A.err) return;  // an earlier step failed: skip the work
+  if (block_err_set(A.err)) return;  // an earlier step failed: skip the work
 
   __shared__ double s_lw[NG], s_lg[NG], s_post[NG];
   __shared__ int s_act[NG];

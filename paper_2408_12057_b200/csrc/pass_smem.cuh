@@ -369,6 +369,7 @@ struct SmemOps {
                                      float bnd, float vs, int mfirst, bool& rejected, float& vs_new,
                                      uint32_t& drawn) {
     float dl = 0.f, bp = 0.f, vn = 0.f;
+    float sA = 0.f, sB = 0.f;  // Tgt::kQuadMH: sum z x, sum z^2 (dl = Tgt::dl_from(s, A, B))
     const float lu = log_u;
     const int mmax = (nq + G - 1) / G;
     int q = lane;
@@ -406,7 +407,12 @@ struct SmemOps {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
             if (kAligned || 4 * q + e < d) {
-              dl += Tgt::dlg(kf, xv[e], s * z[e]);
+              if constexpr (Tgt::kQuadMH) {
+                sA = fmaf(z[e], xv[e], sA);
+                sB = fmaf(z[e], z[e], sB);
+              } else {
+                dl += Tgt::dlg(kf, xv[e], s * z[e]);
+              }
               if (Tgt::kEarly) bp += Tgt::kBoundFromV ? Tgt::vpart(kf, xv[e]) : Tgt::dmax(kf, xv[e], 0.f);
               vn += Tgt::vpart(kf, xp[e]);
             }
@@ -417,6 +423,7 @@ struct SmemOps {
         // warp-uniform: every lane runs mmax iterations
         if (m < 7 && m + 1 < mmax && (m >= mfirst || (m == 0 && mfirst != kNoChecks))) {
           const float rem = Tgt::kBoundFromV ? Tgt::bound_of_v(kf, vs - bp) : bnd - bp;
+          if constexpr (Tgt::kQuadMH) dl = Tgt::dl_from(kf, s, sA, sB);
           if (certainly_rejected(dl, rem, lu)) {
             rejected = true;
             return dl;
@@ -425,6 +432,7 @@ struct SmemOps {
       }
     }
     vs_new = vn;
+    if constexpr (Tgt::kQuadMH) dl = Tgt::dl_from(kf, s, sA, sB);
     return dl;
   }
 
@@ -534,7 +542,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
   const uint64_t blk = blockIdx.x;
   const int nacc = mode_nacc(A.mode);
   const bool loads = mode_loads(A.mode);
-  if (A.err && *(volatile int*)A.err) return;
+  if (block_err_set(A.err)) return;
 
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int kWords = RowWords<Tgt, kHmc>::value;

@@ -78,6 +78,7 @@ struct TgtGaussShift {
   // early rejection: max over h of dlg(x, h) (a concave quadratic in h)
   static constexpr bool kEarly = true;
   static constexpr bool kBoundFromV = false;
+  static constexpr bool kQuadMH = false;
   __device__ static float bound_of_v(const F32&, float) { return 0.f; }
   __device__ static float dmax(const F32& k, float x, float) {
     const float g = k.ba - (x - k.mu0) * k.inv_s2;
@@ -135,6 +136,7 @@ struct TgtMixture {
   // max_h dlg(x, h) <= beta (lmix - vterm(x)) + sr(x)^2 / 2  (v = the cached vterm(x))
   static constexpr bool kEarly = false;  // bound too loose at d = 100 to pay for its bookkeeping
   static constexpr bool kBoundFromV = false;
+  static constexpr bool kQuadMH = false;
   __device__ static float bound_of_v(const F32&, float) { return 0.f; }
   __device__ static float dmax(const F32& k, float x, float v) {
     const float sr = x * k.inv_r;
@@ -243,6 +245,13 @@ struct TgtScale {
   // the unprocessed coordinates from the carried vpart sum, no separate bound pass
   static constexpr bool kBoundFromV = true;
   __device__ static float bound_of_v(const F32& k, float v) { return 0.5f * k.tau * v; }
+  // the MH log-ratio of a proposal x + s z as two running sums (2 FFMA per coordinate
+  // instead of the 4 of sum dlg):  sum_i dlg(x_i, s z_i) = -tau (s A + s^2 B / 2),
+  // A = sum z_i x_i, B = sum z_i^2 -- no cancellation between the terms
+  static constexpr bool kQuadMH = true;
+  __device__ static float dl_from(const F32& k, float s, float A, float B) {
+    return -k.tau * s * fmaf(0.5f * s, B, A);
+  }
   __device__ static double v_from(const TgtParams& T, double s) {
     return T.c[4] * s - (double)T.dim * T.c[5];
   }

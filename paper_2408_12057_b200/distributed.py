@@ -6,7 +6,10 @@ contiguous chunk range [r C / G, (r+1) C / G).  Each rank runs the fused pass
 for its range (asmc_sais_partials), all ranks allgather the per-chunk
 accumulator partials (4 log-moments x (T+1) steps x 16 B per chunk -- about
 40 KB per GPU per round), and every rank folds all chunks in chunk order
-(asmc_fold_partials) -- so the estimates are bit-identical for any GPU count.
+(asmc_fold_partials_dev) -- so the estimates are bit-identical for any GPU count.
+The partials never visit the host: the pass writes them into a device tensor
+(asmc_sais_partials_dev), the all-gather runs device to device (NCCL), and the fold
+runs on the GPU, all on one CUDA stream shared by torch and the library.
 The barrier estimate and the next schedule are then computed redundantly on
 every rank (device kernels), and the next round starts.  There is no other
 data-path collective: SAIS particles never leave the GPU that drew them.
@@ -64,21 +67,23 @@ def run_sais(target, kernel, n1, rounds, seed, exec_, rank, world, partials_fn=N
              fold_fn=None, barrier_fn=None, schedule_fn=None, budget_fn=None, device=None):
     """run_sais (drivers.cpp:186-232) sharded over `world` ranks.
 
-    The *_fn hooks default to the C-ABI (capi) and exist so the host logic can
-    be exercised on CPU-only gloo tests with a stand-in for the device pass."""
-    if partials_fn is None or fold_fn is None:
+    Default (no hooks): the device path -- partials in device tensors, NCCL all-gather,
+    device fold.  The *_fn hooks replace the C-ABI calls with host-array stand-ins so the
+    host logic runs on CPU-only gloo tests."""
+    device_path = partials_fn is None and fold_fn is None
+    if device_path:
+        import torch
+        import torch.distributed as dist
         from . import capi
-        partials_fn = partials_fn or (lambda b, n, p0, p1, k: capi.sais_partials(
-            target, kernel, b, n, p0, p1, seed=seed, round=k, exec_=exec_))
-        fold_fn = fold_fn or capi.fold_partials
+        dev = torch.device("cuda", exec_.device)
+        stream = torch.cuda.current_stream(dev)
+        ex = abi.execopts(exec_.rng, exec_.precision, exec_.device, exec_.lanes, stream.cuda_stream)
         barrier_fn = barrier_fn or (lambda r, b: capi.barrier_estimate(
             r["log_g0"], r["log_g1"], r["log_g2"], b, device=exec_.device))
         schedule_fn = schedule_fn or (lambda lam, b, tn: capi.generate_schedule(
             lam, b, tn, device=exec_.device))
-        budget_fn = budget_fn or (lambda n, t: capi.budget(n, t, target.dim, 4096 << 20,
-                                                            abi.MODE_SAIS))
-        if device is None:
-            device = f"cuda:{exec_.device}"
+    budget_fn = budget_fn or (lambda n, t: __import__(__package__ + ".capi", fromlist=["budget"]).budget(
+        n, t, target.dim, 4096 << 20, abi.MODE_SAIS))
     betas = np.array([0.0, 1.0])
     n, T = n1, 1
     res = {k: [] for k in ("n_particles", "steps", "betas", "log_g0", "log_g1", "log_g2",
@@ -88,9 +93,28 @@ def run_sais(target, kernel, n1, rounds, seed, exec_, rank, world, partials_fn=N
         ranges = chunk_partition(n, world)
         counts = [chunks_of(r) for r in ranges]
         p0, p1 = ranges[rank]
-        local = partials_fn(betas, n, p0, p1, k) if p1 > p0 else np.zeros((0, T + 1, 4, 2))
-        allp = allgather_partials(local, counts, T, device) if world > 1 else local
-        rep = fold_fn(allp, n)
+        if device_path:
+            cmax = max(max(counts), 1)
+            local = torch.zeros((cmax, T + 1, 4, 2), dtype=torch.float64, device=dev)
+            if p1 > p0:
+                capi.sais_partials_dev(target, kernel, betas, n, p0, p1, local.data_ptr(), seed=seed, round=k,
+                                       exec_=ex)
+            if world > 1 and dist.get_backend() == "nccl":  # device to device
+                outs = [torch.empty_like(local) for _ in counts]
+                dist.all_gather(outs, local)
+            elif world > 1:  # gloo (the 2-ranks-on-one-GPU check): staged through the host
+                host = local.cpu()
+                outs = [torch.empty_like(host) for _ in counts]
+                dist.all_gather(outs, host)
+                outs = [o.to(dev) for o in outs]
+            else:
+                outs = [local]
+            allp = torch.cat([o[:c] for o, c in zip(outs, counts)]).contiguous()
+            rep = capi.fold_partials_dev(allp.data_ptr(), allp.shape[0], T, n, exec_=ex)
+        else:
+            local = partials_fn(betas, n, p0, p1, k) if p1 > p0 else np.zeros((0, T + 1, 4, 2))
+            allp = allgather_partials(local, counts, T, device) if world > 1 else local
+            rep = fold_fn(allp, n)
         lam = barrier_fn(rep, betas)
         for key, val in (("n_particles", n), ("steps", T), ("betas", betas.copy()),
                          ("log_g0", rep["log_g0"]), ("log_g1", rep["log_g1"]),

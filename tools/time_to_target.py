@@ -72,11 +72,11 @@ CONFIGS = {
               target=lambda: abi.scale_gaussian(1.0, 2.0, 1000), mode=abi.MODE_SAIS, n1=1 << 14, rounds=8,
               ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=RWMH),
     "2i": dict(name="config2 target, idealized kernel (exact pi_beta draws), N1=2^12",
-               target=lambda: abi.scale_gaussian(1.0, 2.0, 1000), mode=abi.MODE_SAIS, n1=1 << 12, rounds=10,
+               target=lambda: abi.scale_gaussian(1.0, 2.0, 1000), mode=abi.MODE_SAIS, n1=1 << 12, rounds=14,
                ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=IDEAL),
     "3": dict(name="config3: SSMC adaptive-ESS d=100 mixture (log Z = 0), RWMH {0.1,1,10}, N1=2^16",
               target=lambda: abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100), mode=abi.MODE_SSMC, n1=1 << 16,
-              rounds=8, ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=RWMH),
+              rounds=12, ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=RWMH),
 }
 
 
@@ -128,11 +128,22 @@ def measure_config(c, n_seeds, cpu_reps=3):
         return res
     workers = os.cpu_count() or 1
     ref, tg = cpu_ref(), cfg["target"]()
-    cpu = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], cfg["n1"], k + 1, seed=int(seeds[i]),
-                                        workers=workers), cpu_reps)
+    # p-steps of the level; beyond ~2e7 the CPU run is a scaled-down N1 (same rounds, same
+    # T plan) and its time is scaled by the p-step ratio (reported as extrapolated)
+    from paper_2408_12057_b200 import capi
+    plan_n, plan_t = capi.plan_steps(k + 1, cfg["n1"], tg.dim, 4096 << 20, cfg["mode"])
+    ps_full = sum(a * b for a, b in zip(plan_n, plan_t))
+    n1c, reps = cfg["n1"], cpu_reps
+    if ps_full > 2e7:
+        n1c, reps = max(256, int(cfg["n1"] * 2e7 / ps_full)), 1
+    pn, pt = capi.plan_steps(k + 1, n1c, tg.dim, 4096 << 20, cfg["mode"])
+    ps_cpu = sum(a * b for a, b in zip(pn, pt))
+    cpu = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], n1c, k + 1, seed=int(seeds[i]),
+                                        workers=workers), reps) * ps_full / ps_cpu
     res["time_to_target"] = {
         "rounds_needed": k + 1, "b200_wall_s": res["b200_wall_s_by_round"][k], "cpu_wall_s": cpu,
         "cpu_cores": workers, "cpu_kind": "reference (unmodified run_sais/run_ssmc, -O3)",
+        "cpu_extrapolated": n1c != cfg["n1"], "cpu_sample_n1": n1c,
         "speedup_wall": cpu / res["b200_wall_s_by_round"][k]}
     if cfg["batched"]:
         res["time_to_target"]["b200_batched_wall_s_per_seed"] = res["b200_batched_wall_s_per_seed_by_round"][k]
@@ -143,7 +154,7 @@ def zja_vs_sais(n_seeds_sais=1000, n_seeds_zja=200, target=0.05, Ts=(2, 4, 8, 16
     """The paper's GPU experiment on the config-1 family: 2^14
     particles, SAIS effort = rounds, ZJA effort = T via delta* = (Lambda / T)^2."""
     from paper_2408_12057_b200 import capi
-    cfg = CONFIGS[1]
+    cfg = CONFIGS["1"]
     tg, n = cfg["target"](), 1 << 14
     ex = abi.execopts(PH, F32, lanes=1)  # both samplers in the throughput mode
     out = {"config": "config1 family (d=10 Gaussian shift), 2^14 particles, philox/fp32", "target_rel_var": target}
