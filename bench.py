@@ -213,9 +213,10 @@ def load_profile_issue():
     """Issue-slot utilisation of the bench's own pass launch from its ncu capture
     (profiles/r1_bench_pass_ncu_full.json): the pass is ALU/SFU-issue bound, so this
     is its hardware roofline fraction beside the generator-peak one."""
-    path = os.path.join(ROOT, "profiles", "r1_bench_pass_ncu_full.json")
+    path = os.path.join(ROOT, "profiles", "r2_bench_pass_ncu_full.json")
     try:
         d = json.load(open(path))[0]
+        pk = json.load(open(os.path.join(ROOT, "profiles", "r2_peak_ncu_full.json")))[0]
     except (OSError, ValueError, IndexError, KeyError):
         return None
     def pct(key):
@@ -225,7 +226,12 @@ def load_profile_issue():
             "fma_pipe": pct("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
             "alu_pipe": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
             "xu_pipe": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
-            "source": "profiles/r1_bench_pass_ncu_full.json (ncu --set full of bench.py's round-1 pass launch)"}
+            "peak_kernel_issue_active": round(float(pk["smsp__issue_active.avg.pct_of_peak_sustained_active"].split()[0])
+                                              / 100.0, 4),
+            "note": "the generator microbenchmark itself issues on 66 % of cycles (math-pipe throttle: Philox's "
+                    "IMAD.WIDE on the heavy FMA pipe), so the pass's issue share already exceeds its peak's",
+            "source": "profiles/r2_bench_pass_ncu_full.json, r2_peak_ncu_full.json (ncu --set full of bench.py's "
+                      "round-1 pass launch and of its generator-peak launch)"}
 
 
 def other_cpu_baselines():
@@ -540,7 +546,9 @@ def main():
                 "bound": "issue", "kernel": "pass_smem_kernel<TgtScale, 32> (fused init+weight+RWMH pass)",
                 "achieved": achieved / 1e9, "peak": peak_normals / 1e9, "unit": "Gnormal/s",
                 "frac": achieved / peak_normals,
-                "peak_source": "asmc_peak_normals: same Philox4x32-10 + fp32 Box-Muller, registers only, measured live",
+                "issue_frac": (load_profile_issue() or {}).get("issue_active"),
+                "peak_source": "asmc_peak_normals: the pass's own generator (PhiloxKeyC, parameter-bank round keys, "
+                               "normals4<float> SFU Box-Muller, 4x unrolled), registers only, measured live",
                 "algorithmic_units": "normals = N*(d + T*S*d) per pass launch (the RWMH algorithm's draws)",
                 "drawn": {"achieved": drawn_rate / 1e9, "frac": drawn_rate / peak_normals,
                           "fraction_of_algorithmic": pass_drawn / pass_normals,
