@@ -439,7 +439,10 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
-    stream = torch.cuda.current_stream()
+    # a non-default stream, current for torch and passed to the library: the library
+    # enqueues on it (asmc_exec.stream), so the CUDA events below bracket its kernels
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     ex = abi.execopts(abi.RNG_PHILOX, abi.PREC_FP32, device=local, stream=stream.cuda_stream)
     tg = abi.scale_gaussian(SIGMA0, SIGMA1, args.dim)
     kern = abi.kernel(abi.KERNEL_RWMH, STEPS, 1)

@@ -76,7 +76,12 @@ def run_sais(target, kernel, n1, rounds, seed, exec_, rank, world, partials_fn=N
         import torch.distributed as dist
         from . import capi
         dev = torch.device("cuda", exec_.device)
-        stream = torch.cuda.current_stream(dev)
+        # one non-default stream shared by torch (buffers, collectives) and the library:
+        # with torch's legacy default stream (handle 0) the library would run on its own
+        # non-blocking stream, unordered with torch's zero-fill of the partials buffer
+        stream = torch.cuda.Stream(device=dev) if exec_.stream == 0 else \
+            torch.cuda.ExternalStream(exec_.stream, device=dev)
+        torch.cuda.current_stream(dev).synchronize()
         ex = abi.execopts(exec_.rng, exec_.precision, exec_.device, exec_.lanes, stream.cuda_stream)
         barrier_fn = barrier_fn or (lambda r, b: capi.barrier_estimate(
             r["log_g0"], r["log_g1"], r["log_g2"], b, device=exec_.device))
@@ -95,21 +100,23 @@ def run_sais(target, kernel, n1, rounds, seed, exec_, rank, world, partials_fn=N
         p0, p1 = ranges[rank]
         if device_path:
             cmax = max(max(counts), 1)
-            local = torch.zeros((cmax, T + 1, 4, 2), dtype=torch.float64, device=dev)
+            with torch.cuda.stream(stream):
+                local = torch.zeros((cmax, T + 1, 4, 2), dtype=torch.float64, device=dev)
             if p1 > p0:
                 capi.sais_partials_dev(target, kernel, betas, n, p0, p1, local.data_ptr(), seed=seed, round=k,
                                        exec_=ex)
-            if world > 1 and dist.get_backend() == "nccl":  # device to device
-                outs = [torch.empty_like(local) for _ in counts]
-                dist.all_gather(outs, local)
-            elif world > 1:  # gloo (the 2-ranks-on-one-GPU check): staged through the host
-                host = local.cpu()
-                outs = [torch.empty_like(host) for _ in counts]
-                dist.all_gather(outs, host)
-                outs = [o.to(dev) for o in outs]
-            else:
-                outs = [local]
-            allp = torch.cat([o[:c] for o, c in zip(outs, counts)]).contiguous()
+            with torch.cuda.stream(stream):
+                if world > 1 and dist.get_backend() == "nccl":  # device to device
+                    outs = [torch.empty_like(local) for _ in counts]
+                    dist.all_gather(outs, local)
+                elif world > 1:  # gloo (the 2-ranks-on-one-GPU check): staged through the host
+                    host = local.cpu()
+                    outs = [torch.empty_like(host) for _ in counts]
+                    dist.all_gather(outs, host)
+                    outs = [o.to(dev) for o in outs]
+                else:
+                    outs = [local]
+                allp = torch.cat([o[:c] for o, c in zip(outs, counts)]).contiguous()
             rep = capi.fold_partials_dev(allp.data_ptr(), allp.shape[0], T, n, exec_=ex)
         else:
             local = partials_fn(betas, n, p0, p1, k) if p1 > p0 else np.zeros((0, T + 1, 4, 2))
