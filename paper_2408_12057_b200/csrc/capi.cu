@@ -257,6 +257,16 @@ TgtParams make_params(const asmc_target_desc* t) {
       P.c[2] = std::log1p(-p[1]);
       P.c[3] = std::log(p[3]);
       P.c[4] = std::log(p[5]);
+      {  // TgtMixture::F32 (targets.cuh): log-normal constants folded, base-2 vterm terms
+        const double l1 = P.c[1] - P.c[3] + P.c[0], l2 = P.c[2] - P.c[4] + P.c[0];
+        const double lm = (l1 > l2 ? l1 : l2) + std::log1p(std::exp(-std::fabs(l1 - l2)));
+        const double log2e = 1.4426950408889634, h = std::sqrt(0.5 * log2e);
+        const double c1 = h / p[3], c2 = h / p[5];
+        const double v[16] = {1.0 / p[0], l1, p[2], 1.0 / p[3], l2, p[4], 1.0 / p[5], lm,
+                              c1, -p[2] * c1, c2, -p[4] * c2, l1 * log2e, l2 * log2e,
+                              0.5 * log2e / (p[0] * p[0]), 0.5 / (p[0] * p[0])};
+        for (int i = 0; i < 16; ++i) P.f[i] = static_cast<float>(v[i]);
+      }
       break;
     case ASMC_TARGET_SCALE_GAUSSIAN:
       P.c[0] = std::log(p[0]);

@@ -31,6 +31,7 @@ struct TgtParams {
   uint64_t dim;
   double p[8];
   double c[8];  // host-precomputed constants (see host make_params)
+  float f[16];  // host-precomputed beta-independent fp32 constants (TgtMixture::F32)
 };
 
 // target.cpp:16-19 with log(sigma) supplied
@@ -120,17 +121,12 @@ struct TgtMixture {
     float c1, d1, c2, d2, L1, L2, kr;
     float hr;  // 1 / (2 r^2)
   };
+  // every field but beta is beta-independent: the host folds them once per call
+  // (capi.cu make_params -> TgtParams::f, in this order); per (particle, step) only beta
+  // is set -- no fp64 log1p / exp / sqrt / divisions on the device
   __device__ static F32 f32(const TgtParams& T, double beta) {
-    // log-normal constants folded: log N(x; mu, s) = -0.5((x-mu)/s)^2 - log s - c
-    const double l1 = T.c[1] - T.c[3] + T.c[0], l2 = T.c[2] - T.c[4] + T.c[0];
-    const double lm = (l1 > l2 ? l1 : l2) + log1p(exp(-fabs(l1 - l2)));
-    const double log2e = 1.4426950408889634, h = sqrt(0.5 * log2e);
-    const double c1 = h / T.p[3], c2 = h / T.p[5];
-    return F32{(float)beta, (float)(1.0 / T.p[0]), (float)l1, (float)T.p[2], (float)(1.0 / T.p[3]),
-               (float)l2, (float)T.p[4], (float)(1.0 / T.p[5]), (float)lm,
-               (float)c1, (float)(-T.p[2] * c1), (float)c2, (float)(-T.p[4] * c2),
-               (float)(l1 * log2e), (float)(l2 * log2e), (float)(0.5 * log2e / (T.p[0] * T.p[0])),
-               (float)(0.5 / (T.p[0] * T.p[0]))};
+    return F32{(float)beta, T.f[0], T.f[1], T.f[2], T.f[3], T.f[4], T.f[5], T.f[6], T.f[7],
+               T.f[8], T.f[9], T.f[10], T.f[11], T.f[12], T.f[13], T.f[14], T.f[15]};
   }
   // early rejection: f_beta(y) = beta (hi + log1p) - (1 - beta) sr^2 / 2 <= beta lmix, so
   // max_h dlg(x, h) <= beta (lmix - vterm(x)) + sr(x)^2 / 2  (v = the cached vterm(x))
