@@ -336,11 +336,6 @@ int choose_layout_impl(const asmc_exec& ex, int kind, uint64_t d, Layout* L) {
     return 0;
   }
   int lanes = ex.lanes;
-  if (kind == ASMC_KERNEL_SLICE) {  // elliptical slice: one lane per particle (pass_kernel)
-    if (lanes > 1) return fail(ASMC_ERR_CAPABILITY, "the slice kernel runs one lane per particle (lanes = 1)");
-    if (d > 1024) return fail(ASMC_ERR_CAPABILITY, "the slice kernel supports dim <= 1024");
-    lanes = 1;
-  }
   if (lanes == 0) lanes = d <= 16 ? 1 : (d <= 128 ? 4 : 32);
   if (lanes == 1 && d <= 1024) *L = Layout{1, d <= 16 ? 16 : 1024};
   else if (lanes == 4 || lanes == 32) *L = Layout{lanes, 0};  // shared-memory particle store

@@ -29,14 +29,14 @@ static cudaError_t go(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
 }
 
 #if ASMC_PREC == 32
-template <int G, bool kHmc>
+template <int G, int kMove>
 static cudaError_t go_smem_k(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
   const int nacc = mode_nacc(A.mode);
   const int rows = A.t_end - A.t_begin + 1 > 0 ? A.t_end - A.t_begin + 1 : 1;
-  const size_t bytes = smem_pass_bytes(G, A.tg.dim, rows - 1, nacc, RowWords<Tgt, kHmc>::value);
+  const size_t bytes = smem_pass_bytes(G, A.tg.dim, rows - 1, nacc, RowWords<Tgt, kMove == kMoveHmc>::value);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(pass_smem_kernel<Tgt, G, kHmc>,
+    cudaError_t e = cudaFuncSetAttribute(pass_smem_kernel<Tgt, G, kMove>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -44,13 +44,15 @@ static cudaError_t go_smem_k(const PassArgs& A, uint64_t blocks, cudaStream_t s)
   PassArgs Ak = A;
   philox_round_keys(A.seed, A.round, 0, Ak.rk[0]);
   philox_round_keys(A.seed, A.round, 1, Ak.rk[1]);
-  pass_smem_kernel<Tgt, G, kHmc><<<(unsigned)blocks, kBlock, bytes, s>>>(Ak);
+  pass_smem_kernel<Tgt, G, kMove><<<(unsigned)blocks, kBlock, bytes, s>>>(Ak);
   return cudaGetLastError();
 }
 // HMC gets its own instantiation so the RWMH pass keeps its lean register allocation
 template <int G>
 static cudaError_t go_smem(const PassArgs& A, uint64_t blocks, cudaStream_t s) {
-  return A.kc.kind == ASMC_KERNEL_HMC ? go_smem_k<G, true>(A, blocks, s) : go_smem_k<G, false>(A, blocks, s);
+  if (A.kc.kind == ASMC_KERNEL_HMC) return go_smem_k<G, kMoveHmc>(A, blocks, s);
+  if (A.kc.kind == ASMC_KERNEL_SLICE) return go_smem_k<G, kMoveSlice>(A, blocks, s);
+  return go_smem_k<G, kMoveRwmh>(A, blocks, s);
 }
 #endif
 

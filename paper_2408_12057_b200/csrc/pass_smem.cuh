@@ -44,8 +44,13 @@ struct RowWords {
   static constexpr int value = CacheWords<Tgt>::value * (kDual ? 2 : 1);
 };
 
-template <class Tgt, int G, bool kHmc = false>
+// kMove: 0 = RWMH (also idealized), 1 = HMC, 2 = elliptical slice -- separate
+// instantiations, so each hot loop keeps its own registers and code layout
+constexpr int kMoveRwmh = 0, kMoveHmc = 1, kMoveSlice = 2;
+
+template <class Tgt, int G, int kMove = kMoveRwmh>
 struct SmemOps {
+  static constexpr bool kHmc = kMove == kMoveHmc;
   static constexpr bool kCache = Tgt::kCacheV;
   static constexpr bool kDual = RowWords<Tgt, kHmc>::kDual;
 
@@ -171,6 +176,10 @@ struct SmemOps {
       vs = vsum(T, lane, d, xq);
       return;
     }
+    if constexpr (kMove == kMoveSlice) {
+      if (kc.kind == ASMC_KERNEL_SLICE) slice(T, kc, lane, d, beta, xq, xalt, k, drawn, vs);
+      return;
+    } else {
     if (kc.kind != (kHmc ? ASMC_KERNEL_HMC : ASMC_KERNEL_RWMH)) return;
     const typename Tgt::F32 kf = Tgt::f32(T, beta);
     const int nprop = kc.sweeps * kc.n_steps;
@@ -251,6 +260,76 @@ struct SmemOps {
         }
       }
     }
+  }  // kMove != kMoveSlice
+  }
+
+  // Elliptical slice w.r.t. eta (oracle/restate.c:slice_move; the one-lane fp32 form in
+  // pass_kernel.cuh), G lanes per particle.  Sweep s draws nu ~ eta from normals
+  // s d .. s d + d - 1 of the (particle, step) stream, then uniforms u (log y), theta and
+  // one per bracket shrink, in that order -- the one-lane pass's stream order.  Each
+  // candidate regenerates nu from the counter-based stream, writes x' (and its cached
+  // vterm) to the spare row, and an accepted candidate flips the rows.  The shrink loop
+  // runs warp-uniformly (G < 32 holds several particles per warp): a group that has
+  // accepted idles until every group of the warp is done.
+  __device__ static void slice(const TgtParams& T, const KernelCfg& kc, int lane, int d, double beta,
+                               float4*& xq, float4*& xalt, const PhiloxKeyC& k, uint32_t& drawn, float& vs) {
+    const int nq = (d + 3) >> 2;
+    const typename Tgt::F32 kb = Tgt::f32(T, beta), k0 = Tgt::f32(T, 0.0);
+    const float mu = (float)Tgt::ref_draw(T, 0.0);
+    constexpr double kTwoPiS = 6.283185307179586476925286766559;
+    uint32_t ku = 0;  // uniforms drawn from this (particle, step) stream
+    for (int sw = 0; sw < kc.sweeps; ++sw) {
+      const uint64_t base = (uint64_t)sw * (uint64_t)d;
+      const double log_u = log(k.uniform(ku++));
+      double theta = k.uniform(ku++) * kTwoPiS;
+      double lo = theta - kTwoPiS, hi = theta;
+      bool done = false;
+      for (int it = 0; it < ASMC_SLICE_MAX_SHRINK; ++it) {
+        if (__all_sync(0xffffffffu, done)) break;
+        const float c = (float)cos(theta), sn = (float)sin(theta);
+        float dl = 0.f;  // beta (V(x') - V(x)) as a difference of log-density differences
+        for (int q = lane; q < nq; q += G) {
+          if (done) break;
+          ++drawn;
+          float z[4];
+          quad(k, base, q, z);
+          const float4 x4 = xq[q];
+          const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+          float xp[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (4 * q + e < d) {
+              const float nu = (float)Tgt::ref_draw(T, (double)z[e]);
+              xp[e] = mu + (xv[e] - mu) * c + (nu - mu) * sn;
+              const float h = xp[e] - xv[e];
+              dl += Tgt::dlg(kb, xv[e], h) - Tgt::dlg(k0, xv[e], h);
+            } else {
+              xp[e] = 0.f;
+            }
+          }
+          const float4 xn = make_float4(xp[0], xp[1], xp[2], xp[3]);
+          xalt[q] = xn;
+          if constexpr (kCache) xalt[nq + q] = vquad(k0, xn);
+        }
+        const double delta = group_sum<G>((double)dl);
+        const bool accept = !done && delta > log_u;
+        __syncwarp();
+        if (accept) {  // the candidate is the spare row: flip
+          float4* t = xq;
+          xq = xalt;
+          xalt = t;
+        }
+        if (!done && !accept) {
+          if (theta < 0.0) lo = theta;
+          else hi = theta;
+          theta = lo + (hi - lo) * k.uniform(ku++);
+        }
+        done = done || accept;
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+    vs = vsum(T, lane, d, xq);
   }
 
   // sum of the early-rejection bound over this lane's coordinates (same order as delta_pass)
@@ -529,11 +608,11 @@ __device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_po
   }
 }
 
-template <class Tgt, int G, bool kHmc = false>
+template <class Tgt, int G, int kMove = kMoveRwmh>
 // RWMH passes: <= 85 registers (3 CTAs/SM; the dual-row footprint allows no more at d = 1000)
 // G = 4 RWMH on cached-potential targets: 4 rows per particle, so shared memory holds
 // 2 CTAs/SM anyway and the registers may grow to 128 (the row prefetch below)
-__global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ? 2 : 3))
+__global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tgt::kCacheV) ? 2 : 3))
     pass_smem_kernel(const __grid_constant__ PassArgs A) {
   constexpr int NG = kBlock / G;
   const int tid = threadIdx.x, g = tid / G, lane = tid % G, warp = tid >> 5;
@@ -545,6 +624,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
   if (block_err_set(A.err)) return;
 
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr bool kHmc = kMove == kMoveHmc;
   constexpr int kWords = RowWords<Tgt, kHmc>::value;
   float4* xq = reinterpret_cast<float4*>(smem) + (size_t)g * nq * kWords;
   float4* xalt = xq + (size_t)nq * CacheWords<Tgt>::value;  // spare row (kDual only)
@@ -555,7 +635,7 @@ __global__ void __launch_bounds__(kBlock, kHmc ? 4 : ((G == 4 && Tgt::kCacheV) ?
     for (int i = 0; i < rows * nacc; ++i)
       myacc[i] = (i % nacc == kAccTop2) ? LogAcc{-__builtin_huge_val(), -__builtin_huge_val()}
                                          : lacc_empty();
-  using Ops = SmemOps<Tgt, G, kHmc>;
+  using Ops = SmemOps<Tgt, G, kMove>;
   uint32_t drawn = 0;  // quads of normals this lane generated (profiling)
 
   // SMC step, G = 4: the next round's particle row is loaded into registers while this

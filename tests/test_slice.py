@@ -59,12 +59,16 @@ def test_slice_trajectories_fp64_match_oracle(name, tg):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("lanes", [0, 1, 4, 32])
 @pytest.mark.parametrize("name,tg", TARGETS)
-def test_slice_trajectories_fp32_close_to_oracle(name, tg):
+def test_slice_trajectories_fp32_close_to_oracle(name, tg, lanes):
+    """fp32 one-lane pass and the lane-cooperative shared-memory pass (G = 4, 32: nu
+    regenerated from the counter-based stream per candidate, the spare row flipped on
+    acceptance, the shrink loop warp-uniform) against the fp64 restatement."""
     betas = np.linspace(0.0, 1.0, 5)
     rs = oracle.load("restate", PH)
     pids = np.arange(48)
-    x, lw = capi.trajectories(tg, SLICE, betas, 4, 1, pids, abi.execopts(PH, F32))
+    x, lw = capi.trajectories(tg, SLICE, betas, 4, 1, pids, abi.execopts(PH, F32, lanes=lanes))
     ok = sum(np.max(np.abs(x[i] - rs.trajectory(tg, SLICE, betas, 4, 1, int(p))[0]))
              < 5e-4 * max(1.0, np.max(np.abs(x[i]))) for i, p in enumerate(pids))
     assert ok >= len(pids) - 1, (name, ok)
@@ -83,6 +87,19 @@ def test_slice_sais_and_ssmc_on_device():
     b = capi.run_smc(tg, SLICE, np.linspace(0, 1, 9), 512, policy=abi.POLICY_ALWAYS, seed=2,
                      exec_=abi.execopts(XO, F64))
     assert abs(a["log_z_hat"] - b["log_z_hat"]) < 1e-9
-    with pytest.raises(capi.AsmcError) as e:
-        capi.run_sais_single(tg, SLICE, [0.0, 1.0], 16, exec_=abi.execopts(PH, F32, lanes=32))
-    assert e.value.code == abi.ERR_CAPABILITY
+    # the shared-memory pass (G = 32 / 4) and the one-lane pass agree within fp32 noise
+    tg = abi.gaussian_shift(0.0, 0.5, 1.0, 50)
+    one = capi.run_sais_single(tg, SLICE, np.linspace(0, 1, 17), 1 << 14, seed=4, round=1,
+                               exec_=abi.execopts(PH, F32, lanes=1))
+    for lanes in (4, 32):
+        many = capi.run_sais_single(tg, SLICE, np.linspace(0, 1, 17), 1 << 14, seed=4, round=1,
+                                    exec_=abi.execopts(PH, F32, lanes=lanes))
+        assert abs(one["log_z_hat"] - many["log_z_hat"]) < 2e-3, (lanes, one["log_z_hat"], many["log_z_hat"])
+
+
+@pytest.mark.gpu
+def test_slice_beyond_the_one_lane_limit():
+    """d = 2000 (> the one-lane pass's 1024): the shared-memory pass runs the slice move."""
+    tg = abi.gaussian_shift(0.0, 0.05, 1.0, 2000)
+    r = capi.run_sais_single(tg, SLICE, np.linspace(0, 1, 33), 4096, seed=5, round=1, exec_=abi.execopts(PH, F32))
+    assert abs(r["log_z_hat"]) < 0.2, r["log_z_hat"]
