@@ -608,6 +608,45 @@ __device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_po
   }
 }
 
+// SMC step mode with several particles per warp (G < 32): each lane keeps ONE running
+// accumulator in registers across the CTA's particle rounds -- lane l of a group owns
+// accumulator l (g0, g1, g2, elbo), lane 0 also the sq and top-2 rows -- one exp per
+// (particle, step) and no shuffles; the groups of a warp are combined once at the end
+// (warp_regfold_finish).  Same sums as warp_fold, another fixed association.
+struct RegFold {
+  LogAcc acc, sq, top;
+};
+template <int G>
+__device__ __forceinline__ void warp_regfold_add(double lw_pre, double lg, double lw_post, bool active,
+                                                 RegFold& f) {
+  const int l = (threadIdx.x & 31) % G;
+  if (!active) return;
+  if (l == kAccElbo) {
+    if (lg != 0.0) sacc_add(f.acc, lw_pre + log(fabs(lg)), lg > 0.0 ? 1.0 : -1.0);
+  } else {
+    lacc_add(f.acc, l == kAccG0 ? lw_pre : (l == kAccG1 ? lw_pre + lg : lw_pre + 2.0 * lg));
+  }
+  if (l == 0) {
+    lacc_add(f.sq, 2.0 * lw_post);
+    top2_add(f.top, lw_post);
+  }
+}
+template <int G>
+__device__ __forceinline__ void warp_regfold_finish(RegFold& f, int nacc, LogAcc* acc) {
+  const int ln = threadIdx.x & 31, l = ln % G;
+#pragma unroll
+  for (int m = G; m < 32; m <<= 1) {
+    lacc_combine(f.acc, shfl_xor_acc(f.acc, m));
+    lacc_combine(f.sq, shfl_xor_acc(f.sq, m));
+    top2_merge(f.top, shfl_xor_acc(f.top, m));
+  }
+  if (ln < G && l < 4) acc[l] = f.acc;
+  if (ln == 0 && nacc > kAccSq) {
+    acc[kAccSq] = f.sq;
+    acc[kAccTop2] = f.top;
+  }
+}
+
 template <class Tgt, int G, int kMove = kMoveRwmh>
 // RWMH passes: <= 85 registers (3 CTAs/SM; the dual-row footprint allows no more at d = 1000)
 // G = 4 RWMH on cached-potential targets: 4 rows per particle, so shared memory holds
@@ -636,6 +675,9 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
       myacc[i] = (i % nacc == kAccTop2) ? LogAcc{-__builtin_huge_val(), -__builtin_huge_val()}
                                          : lacc_empty();
   using Ops = SmemOps<Tgt, G, kMove>;
+  // G < 32 SMC step: per-lane register accumulators (one step per launch)
+  const bool regfold = G < 32 && A.mode == kModeSmcStep && rows == 1;
+  RegFold rf{lacc_empty(), lacc_empty(), LogAcc{-__builtin_huge_val(), -__builtin_huge_val()}};
   uint32_t drawn = 0;  // quads of normals this lane generated (profiling)
 
   // SMC step, G = 4: the next round's particle row is loaded into registers while this
@@ -748,7 +790,8 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
         }
         continue;
       }
-      warp_fold<G>(pre, lg, lw, active, nacc, myacc + (size_t)(t - A.t_begin) * nacc);
+      if (G < 32 && regfold) warp_regfold_add<G>(pre, lg, lw, active, rf);
+      else warp_fold<G>(pre, lg, lw, active, nacc, myacc + (size_t)(t - A.t_begin) * nacc);
     }
     if (mode_stores(A.mode) && active) {
       float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(A.xbuf[*A.xcur]) +
@@ -770,6 +813,7 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
     if ((tid & 31) == 0) atomicAdd(A.drawn, 4ull * c);
   }
   if (A.mode == kModeTraj || A.mode == kModeSmcInit) return;
+  if (G < 32 && regfold) warp_regfold_finish<G>(rf, nacc, myacc);
   __syncthreads();
   // block partial = warps folded in order (fixed tree)
   for (int i = tid; i < rows * nacc; i += blockDim.x) {
