@@ -1631,8 +1631,9 @@ static int resample_common(const double* log_w, uint64_t n, double u, int32_t de
     CU(cudaStreamSynchronize(C->stream));
     std::fprintf(stderr, "refcdf n=%llu phases(us):", (unsigned long long)n);
     for (int i = 1; i < 13; ++i)
-      if (ts[i]) std::fprintf(stderr, " %d:%.1f", i, (ts[i] - ts[0]) * 1e-3);
-    std::fprintf(stderr, " replays lse=%llu cdf=%llu\n", ts[14], ts[15]);
+      if (ts[i] > ts[0]) std::fprintf(stderr, " %d:%.1f", i, (ts[i] - ts[0]) * 1e-3);
+    std::fprintf(stderr, " replays lse=%llu (%.1f us) cdf=%llu (%.1f us)\n", ts[14], ts[13] * 1e-3,
+                 ts[15] & 0xfffff, (ts[15] >> 20) * 1e-3);
   }
   if (ancestors && what == 1)
     CU(cudaMemcpyAsync(ancestors, anc.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, C->stream));

@@ -46,6 +46,8 @@ struct RefCdfWork {
   unsigned long long* tot;     // exact integer total of a stable block at its binade
   unsigned long long* bstart;  // exact start of each stable block, in units of its binade
   int* kb;         // binade of a stable block, or unstable
+  unsigned long long* ovf;  // slot runs of heavy ancestors (lo, hi, j), at most n / 1024
+  unsigned int* novf;
   double* gmax;    // max log-weight
   double* l1;      // logsumexp of the log-weights (the reference's bits)
   unsigned long long* prof;  // optional: %globaltimer at each phase end (16 entries)

@@ -321,6 +321,12 @@ __device__ void phase_classify(const Args& A, int mode, double l1, double* sh, u
   }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---- the exact walk (CTA 0) ----------------------------------------------------
 // Scans of 4 consecutive entries per thread (tile of 1024): exclusive prefix sums.
 __device__ __forceinline__ unsigned long long scan4_u64(unsigned long long v[4], unsigned long long ex[4],
@@ -358,36 +364,86 @@ struct WalkSmem {
   double vbuf[kT];
   unsigned char fbuf[kT];
   double s;
-  int nh, stop, stop_end, replays;
+  int nh, stop, stop_end, replays, ev_first;
+  unsigned long long t_replay;  // profiling: %globaltimer ns spent replaying (thread 0)
 };
 
 // Replays block b element by element from the exact value W.s, with the reference's own
 // fp64 operations; CDF mode stores cum.  Leaves the new value in W.s.
+// Replays block b from the exact value W.s with the reference's own fp64 operations and
+// leaves the new value in W.s (CDF mode also stores cum).  Events -- the elements that
+// change the binade of the running value, exact ties and the LogAccumulator's rescales --
+// are few in a replayed block (typically 1-3), so the block is replayed as segments:
+// between two events every add is the integer r_k of the current binade (one CTA prefix
+// scan per segment, all elements at once), and each event is applied directly in fp64.
+// A block with many events (e.g. log-weights increasing with the index) is replayed by
+// one thread, element by element.
 __device__ void replay_block(const Args& A, int mode, uint64_t b, double l1, double* sh, WalkSmem& W) {
   const Op op = block_op(A, mode, b, l1, sh);
-  W.vbuf[threadIdx.x] = op.v;
-  W.fbuf[threadIdx.x] = op.rescale ? 1 : 0;
-  __syncthreads();
+  const int i = threadIdx.x;
+  const int m = (int)min((uint64_t)kT, A.n - b * kT);
+  const double v = i < m ? op.v : 0.0;
+  const bool resc = i < m && op.rescale;
+  W.vbuf[i] = v;
+  W.fbuf[i] = resc ? 1 : 0;
+  const int nresc = __syncthreads_count(resc ? 1 : 0);
+  if (nresc <= 16) {
+    double cum = 0.0;  // this element's value after its op (CDF store)
+    int start = 0;
+    while (start < m) {  // uniform
+      const double s = W.s;
+      const int k = binade(s);
+      const unsigned long long u0 = sum_units(s);
+      bool tie = false, sat = false;
+      const unsigned long long r = (i >= start && i < m) ? add_units(v, k, tie, sat) : 0ull;
+      const unsigned long long inc = cta_incl_u64(r, W.wsh);
+      const bool ev = i >= start && i < m && (resc || tie || sat || u0 + inc >= kTwo53 || k >= 0x40000000);
+      // first event at or after `start` (m if none)
+      if (i == 0) W.ev_first = m;
+      __syncthreads();
+      if (ev) atomicMin(&W.ev_first, i);
+      __syncthreads();
+      const int p = W.ev_first;
+      if (i >= start && i < p) cum = units_value(u0 + inc, k);
+      __syncthreads();
+      if (i == p - 1 && p > start) W.s = cum;  // the value before the event / at the end
+      __syncthreads();
+      if (p < m) {
+        if (i == p) {  // the event, in the reference's fp64 operations
+          const double sp = W.s;
+          cum = resc ? __dadd_rn(__dmul_rn(sp, v), 1.0) : __dadd_rn(sp, v);
+          W.s = cum;
+        }
+        __syncthreads();
+      }
+      start = p + 1;
+    }
+    if (mode == kModeCdf) {
+      const uint64_t j = b * kT + i;
+      if (j < A.n) A.cum[j] = cum;
+    }
+    __syncthreads();
+    return;
+  }
   if (threadIdx.x == 0) {
-    const int m = (int)min((uint64_t)kT, A.n - b * kT);
     double s = W.s;
     for (int i0 = 0; i0 < m; i0 += 8) {  // batches of 8: the loads are off the add chain
-      double v[8];
+      double vv[8];
       unsigned char f[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        v[e] = W.vbuf[i0 + e];
+        vv[e] = W.vbuf[i0 + e];
         f[e] = W.fbuf[i0 + e];
       }
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         if (i0 + e < m) {
-          s = f[e] ? __dadd_rn(__dmul_rn(s, v[e]), 1.0) : __dadd_rn(s, v[e]);
-          v[e] = s;
+          s = f[e] ? __dadd_rn(__dmul_rn(s, vv[e]), 1.0) : __dadd_rn(s, vv[e]);
+          vv[e] = s;
         }
       }
 #pragma unroll
-      for (int e = 0; e < 8; ++e) W.vbuf[i0 + e] = v[e];
+      for (int e = 0; e < 8; ++e) W.vbuf[i0 + e] = vv[e];
     }
     W.s = s;
   }
@@ -396,6 +452,7 @@ __device__ void replay_block(const Args& A, int mode, uint64_t b, double l1, dou
     const uint64_t j = b * kT + threadIdx.x;
     if (j < A.n) A.cum[j] = W.vbuf[threadIdx.x];
   }
+  __syncthreads();
 }
 
 // P5 (CTA 0): walk the blocks in order with the EXACT running value.  Per tile of 1024
@@ -408,6 +465,7 @@ __device__ double phase_walk(const Args& A, int mode, double l1, double* sh, Wal
   if (threadIdx.x == 0) {
     W.s = 0.0;
     W.replays = 0;
+    W.t_replay = 0;
   }
   for (uint64_t t0 = 0; t0 < A.nblk; t0 += kTile) {
     const int m = (int)min((uint64_t)kTile, A.nblk - t0);
@@ -473,6 +531,8 @@ __device__ double phase_walk(const Args& A, int mode, double l1, double* sh, Wal
       __syncthreads();
       h = W.stop;
       if (h >= W.nh) break;
+      unsigned long long tr0 = 0;
+      if (A.w.prof && threadIdx.x == 0) tr0 = gtimer();
       for (int i = W.heads[h]; i < W.stop_end; ++i) {
         replay_block(A, mode, t0 + i, l1, sh, W);
         if (threadIdx.x == 0) {
@@ -481,6 +541,7 @@ __device__ double phase_walk(const Args& A, int mode, double l1, double* sh, Wal
           A.w.kb[t0 + i] = kUnstable;  // P6 skips it: the replay wrote its cum
         }
       }
+      if (A.w.prof && threadIdx.x == 0) W.t_replay += gtimer() - tr0;
       ++h;
       __syncthreads();
     }
@@ -512,50 +573,67 @@ __device__ void phase_materialize(const Args& A, double l1, double* sh, unsigned
   }
 }
 
-// P7 (grid): a_m = first j with !(cum_j < pos_m), clamped (engine.cpp:68-76).  A thread
-// takes 8 consecutive slots: one binary search, then the reference's own forward walk.
+// P7 (grid): a_m = first j with !(cum_j < pos_m), clamped to n - 1 (engine.cpp:68-76),
+// inverted: particle j owns the output slots m with cum_{j-1} < pos_m <= cum_j (the last
+// particle also every slot beyond cum_{n-1}), i.e. [M(cum_{j-1}), M(cum_j)) with
+// M(c) = first m with pos_m > c.  pos_m = (m + u) / n is evaluated exactly as the
+// reference does, M(c) from the estimate c n - u corrected by exact comparisons, so a
+// thread reads two neighbouring CDF values (coalesced) and writes its slots: no search.
+__device__ __forceinline__ double slot_pos(uint64_t m, double u, double dn) {
+  return __ddiv_rn(__dadd_rn((double)m, u), dn);
+}
+__device__ __forceinline__ uint64_t first_slot_above(double c, double u, uint64_t n, double dn) {
+  double est = floor(__fma_rn(c, dn, -u));
+  if (!(est >= 0.0)) est = 0.0;  // also NaN
+  uint64_t m = est > (double)n ? n : (uint64_t)est;
+  while (m > 0 && slot_pos(m - 1, u, dn) > c) --m;
+  while (m < n && !(slot_pos(m, u, dn) > c)) ++m;
+  return m;
+}
+constexpr uint64_t kSlotRun = 8192;  // longer runs of one ancestor go to the whole grid (P8)
 __device__ void phase_ancestors(const Args& A, double u) {
-  constexpr int kS = 8;
   const double dn = (double)A.n;
-  const uint64_t nthr = (A.n + kS - 1) / kS;
-  for (uint64_t t = (uint64_t)blockIdx.x * kT + threadIdx.x; t < nthr; t += (uint64_t)gridDim.x * kT) {
-    const uint64_t m0 = t * kS;
-    double pos = __ddiv_rn(__dadd_rn((double)m0, u), dn);
-    uint64_t lo = 0, hi = A.n;
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (A.cum[mid] < pos) lo = mid + 1;
-      else hi = mid;
-    }
-    uint64_t j = lo < A.n ? lo : A.n - 1;
-    A.anc[m0] = (uint32_t)j;
-    for (int e = 1; e < kS && m0 + e < A.n; ++e) {
-      pos = __ddiv_rn(__dadd_rn((double)(m0 + e), u), dn);
-      if (A.cum[j] < pos) {  // gallop forward from j, then bisect: O(log distance)
-        uint64_t step = 1, a = j;  // invariant: cum[a] < pos
-        uint64_t b = j + 1;
-        while (b < A.n && A.cum[b] < pos) {
-          a = b;
-          step <<= 1;
-          b = a + step;
-        }
-        if (b > A.n) b = A.n;
-        while (a + 1 < b) {  // cum[a] < pos, first j >= b has cum >= pos (or b = n)
-          const uint64_t mid = (a + b) >> 1;
-          if (A.cum[mid] < pos) a = mid;
-          else b = mid;
-        }
-        j = b < A.n ? b : A.n - 1;
+  const int ln = threadIdx.x & 31;
+  // warp-uniform trip count: every lane of a warp iterates while any lane has particles
+  const uint64_t stride = (uint64_t)gridDim.x * kT;
+  for (uint64_t j0 = (uint64_t)blockIdx.x * kT + (threadIdx.x & ~31u); j0 < A.n; j0 += stride) {
+    const uint64_t j = j0 + ln;
+    uint64_t lo = 0, hi = 0;
+    if (j < A.n) {
+      lo = j == 0 ? 0 : first_slot_above(A.cum[j - 1], u, A.n, dn);
+      hi = j + 1 == A.n ? A.n : first_slot_above(A.cum[j], u, A.n, dn);
+      if (hi - lo > kSlotRun) {  // a heavy ancestor: the rest of its slots go to the grid
+        const unsigned int e = atomicAdd(A.w.novf, 1u);
+        A.w.ovf[3 * e] = lo + kSlotRun;
+        A.w.ovf[3 * e + 1] = hi;
+        A.w.ovf[3 * e + 2] = j;
+        hi = lo + kSlotRun;
       }
-      A.anc[m0 + e] = (uint32_t)j;
+    }
+    // short runs (the common case: ~1 slot per particle) by their own lane; the warp
+    // writes the longer ones together, 32 slots at a time
+    const bool big = hi - lo > 32;
+    if (!big)
+      for (uint64_t m = lo; m < hi; ++m) A.anc[m] = (uint32_t)j;
+    unsigned int bal = __ballot_sync(0xffffffffu, big);
+    while (bal) {
+      const int src = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const uint64_t a = __shfl_sync(0xffffffffu, lo, src), e = __shfl_sync(0xffffffffu, hi, src);
+      for (uint64_t m = a + ln; m < e; m += 32) A.anc[m] = (uint32_t)(j0 + src);
     }
   }
 }
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+// P8 (grid): the slot runs of heavy ancestors, every CTA striding over each run
+__device__ void phase_heavy_slots(const Args& A) {
+  const unsigned int ne = *(volatile unsigned int*)A.w.novf;
+  for (unsigned int e = 0; e < ne; ++e) {
+    const uint64_t lo = A.w.ovf[3 * e], hi = A.w.ovf[3 * e + 1];
+    const uint32_t j = (uint32_t)A.w.ovf[3 * e + 2];
+    for (uint64_t m = lo + (uint64_t)blockIdx.x * kT + threadIdx.x; m < hi; m += (uint64_t)gridDim.x * kT)
+      A.anc[m] = j;
+  }
 }
 
 __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
@@ -572,6 +650,7 @@ __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
 #define MARK(i) \
   if (A.w.prof && lead && threadIdx.x == 0) A.w.prof[i] = gtimer();
   MARK(0);
+  if (lead && threadIdx.x == 0) *A.w.novf = 0u;
 
   // ---- l1 = logsumexp(log_w) ----
   phase_block_max(A, sh);
@@ -591,7 +670,10 @@ __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
   MARK(5);
   if (lead) {
     const double s = phase_walk(A, kModeLse, 0.0, sh, u.walk);
-    if (threadIdx.x == 0 && A.w.prof) A.w.prof[14] = u.walk.replays;
+    if (threadIdx.x == 0 && A.w.prof) {
+      A.w.prof[14] = u.walk.replays;
+      A.w.prof[12 + 1] = u.walk.t_replay;
+    }
     if (threadIdx.x == 0) {
       const double M = A.w.gmax[0];
       // LogAccumulator::log_total (logsum.hpp:40-42)
@@ -617,7 +699,7 @@ __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
   MARK(9);
   if (lead) {
     const double s = phase_walk(A, kModeCdf, l1, sh, u.walk);
-    if (threadIdx.x == 0 && A.w.prof) A.w.prof[15] = u.walk.replays;
+    if (threadIdx.x == 0 && A.w.prof) A.w.prof[15] = u.walk.replays + (u.walk.t_replay << 20);
     if (threadIdx.x == 0) A.st->total = s;
   }
   grid.sync();
@@ -627,6 +709,8 @@ __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
   grid.sync();
   MARK(11);
   phase_ancestors(A, A.st->u);
+  grid.sync();
+  phase_heavy_slots(A);
   if (A.w.prof) {
     grid.sync();
     MARK(12);
@@ -650,7 +734,7 @@ cudaError_t launch_exact_math(int which, const double* x, uint64_t n, double* ou
 size_t refcdf_work_bytes(uint64_t n) {
   const uint64_t nb = (n + kT - 1) / kT;
   // 6 double/u64 arrays + 1 int array of nb + 2 entries, 3 scalars, 16-byte alignment each
-  return (size_t)(nb + 2) * (6 * 8 + 4) + 16 * 16 + 256;
+  return (size_t)(nb + 2) * (6 * 8 + 4) + 24 * (nb / 4 + 2) + 18 * 16 + 256;
 }
 
 void refcdf_work_carve(void* base, uint64_t n, RefCdfWork* w) {
@@ -668,6 +752,8 @@ void refcdf_work_carve(void* base, uint64_t n, RefCdfWork* w) {
   w->tot = (unsigned long long*)take(8 * (nb + 1));
   w->bstart = (unsigned long long*)take(8 * (nb + 1));
   w->kb = (int*)take(4 * (nb + 1));
+  w->ovf = (unsigned long long*)take(24 * (nb / 4 + 2));
+  w->novf = (unsigned int*)take(16);
   w->gmax = (double*)take(16);
   w->l1 = (double*)take(16);
   w->prof = nullptr;

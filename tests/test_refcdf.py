@@ -50,6 +50,12 @@ def weight_sets(g):
     for n in (1, 2, 3, 255, 256, 257, 511, 1025):
         yield f"n{n}", g.normal(0, 3, n)
     yield "laplace", g.laplace(0, 4, 200_000)
+    lw = np.full(300_000, -800.0)
+    lw[123_457] = 0.0  # one particle carries all the mass: every slot is its (heavy-run path)
+    yield "one_heavy", lw
+    lw = g.normal(0, 1, 250_000)
+    lw[[17, 99_999, 200_003]] = 40.0  # three heavy ancestors
+    yield "three_heavy", lw
 
 
 def test_gexp_bit_exact_vs_host_libm():
