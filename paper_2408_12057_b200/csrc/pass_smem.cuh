@@ -235,7 +235,21 @@ struct SmemOps {
       bool rejected = false;
       float vs_new = 0.f;
       // checks after every quad-iteration up to the 7th (the test hook turns them off)
-      const int mfirst = kc.no_early ? kNoChecks : 1;
+      // the first quad-iteration whose check can plausibly reject (checks are warp-uniform
+      // and exact whichever ones run -- skipping one only draws more normals): for the
+      // scale family the partial sum after c coordinates is ~ -tau s^2 c / 2 and the bound
+      // of the rest tau X (1 - c / d) / 2 (X = sum x^2, from lane 0's carried sum): a check
+      // is useless before c ~ X / (s^2 + X / d), 2 quad-iterations of slack
+      // (G = 32 only: with several particles per warp the check -- a warp vote -- must
+      // start at the same iteration for every group)
+      int mfirst = kc.no_early ? kNoChecks : 0;
+      if constexpr (Tgt::kBoundFromV && G == 32) {
+        if (!kc.no_early) {
+          const float X = __shfl_sync(0xffffffffu, vs, gbase) * (float)G;
+          const float need = X / (4.f * (float)G * fmaf(s, s, X / (float)d));
+          mfirst = max(0, (int)ceilf(need) - 2);
+        }
+      }
       const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst,
                                                   rejected, vs_new, drawn)
                                : delta_pass<false>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst,
@@ -438,7 +452,7 @@ struct SmemOps {
 
   // sum over this lane's quads of f_beta(x + s z) - f_beta(x), writing x + s z to the
   // spare row and its vpart sum to vs_new.  Early rejection (exact): after quad-iteration
-  // m (m < 7; m = 0 and every m >= mfirst, kNoChecks = none) the warp checks
+  // m (m < 7, m >= mfirst; kNoChecks = none) the warp checks
   //   partial + sum over unprocessed coordinates of max_h dlg  <  log u
   // (certainly_rejected); then the proposal is rejected whatever the remaining normals
   // are, so they are not drawn.  Accepted proposals see the identical sum.
@@ -500,7 +514,7 @@ struct SmemOps {
       }
       if constexpr (Tgt::kEarly) {
         // warp-uniform: every lane runs mmax iterations
-        if (m < 7 && m + 1 < mmax && (m >= mfirst || (m == 0 && mfirst != kNoChecks))) {
+        if (m < 7 && m + 1 < mmax && m >= mfirst) {
           const float rem = Tgt::kBoundFromV ? Tgt::bound_of_v(kf, vs - bp) : bnd - bp;
           if constexpr (Tgt::kQuadMH) dl = Tgt::dl_from(kf, s, sA, sB);
           if (certainly_rejected(dl, rem, lu)) {
