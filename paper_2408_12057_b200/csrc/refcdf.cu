@@ -583,6 +583,7 @@ __device__ __forceinline__ double slot_pos(uint64_t m, double u, double dn) {
   return __ddiv_rn(__dadd_rn((double)m, u), dn);
 }
 __device__ __forceinline__ uint64_t first_slot_above(double c, double u, uint64_t n, double dn) {
+  if (c != c) return n;  // a NaN CDF (NaN log-weights): no walk over all slots
   double est = floor(__fma_rn(c, dn, -u));
   if (!(est >= 0.0)) est = 0.0;  // also NaN
   uint64_t m = est > (double)n ? n : (uint64_t)est;

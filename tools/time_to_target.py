@@ -74,9 +74,15 @@ CONFIGS = {
     "2i": dict(name="config2 target, idealized kernel (exact pi_beta draws), N1=2^12",
                target=lambda: abi.scale_gaussian(1.0, 2.0, 1000), mode=abi.MODE_SAIS, n1=1 << 12, rounds=14,
                ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=IDEAL),
+    # the same target with HMC (eps 0.3, 5 leapfrog steps): the reference has no HMC, so
+    # the CPU side is the oracle's plain-C port (one core), marked kind "port"
+    "2h": dict(name="config2 target, HMC eps=0.3 x 5 leapfrog, N1=2^12",
+               target=lambda: abi.scale_gaussian(1.0, 2.0, 1000), mode=abi.MODE_SAIS, n1=1 << 12, rounds=15,
+               ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05,
+               kernel=abi.kernel(abi.KERNEL_HMC, (0.3,), 1, 5), cpu="port"),
     "3": dict(name="config3: SSMC adaptive-ESS d=100 mixture (log Z = 0), RWMH {0.1,1,10}, N1=2^16",
               target=lambda: abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100), mode=abi.MODE_SSMC, n1=1 << 16,
-              rounds=12, ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=RWMH),
+              rounds=15, ex=lambda: abi.execopts(PH, F32), batched=False, rv=0.05, kernel=RWMH),
 }
 
 
@@ -127,7 +133,13 @@ def measure_config(c, n_seeds, cpu_reps=3):
     if k is None:
         return res
     workers = os.cpu_count() or 1
-    ref, tg = cpu_ref(), cfg["target"]()
+    port = cfg.get("cpu") == "port"
+    if port:
+        import oracle
+        ref, workers = oracle.load("restate", PH), 1
+    else:
+        ref = cpu_ref()
+    tg = cfg["target"]()
     # p-steps of the level; beyond ~2e7 the CPU run is a scaled-down N1 (same rounds, same
     # T plan) and its time is scaled by the p-step ratio (reported as extrapolated)
     from paper_2408_12057_b200 import capi
@@ -142,7 +154,9 @@ def measure_config(c, n_seeds, cpu_reps=3):
                                         workers=workers), reps) * ps_full / ps_cpu
     res["time_to_target"] = {
         "rounds_needed": k + 1, "b200_wall_s": res["b200_wall_s_by_round"][k], "cpu_wall_s": cpu,
-        "cpu_cores": workers, "cpu_kind": "reference (unmodified run_sais/run_ssmc, -O3)",
+        "cpu_cores": workers,
+        "cpu_kind": "port (oracle/restate.c, one core: the reference has no HMC)" if port else
+                    "reference (unmodified run_sais/run_ssmc, -O3)",
         "cpu_extrapolated": n1c != cfg["n1"], "cpu_sample_n1": n1c,
         "speedup_wall": cpu / res["b200_wall_s_by_round"][k]}
     if cfg["batched"]:
@@ -207,7 +221,7 @@ def measure(n_seeds=1000):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="1,2,2i,3")
+    ap.add_argument("--configs", default="1,2,2i,2h,3")
     ap.add_argument("--seeds", type=int, default=1000)
     ap.add_argument("--seeds-slow", type=int, default=32, help="seeds for the configs run one seed at a time")
     ap.add_argument("--zja", action="store_true")
