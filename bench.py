@@ -591,6 +591,8 @@ def main():
                 sys.path.insert(0, os.path.join(ROOT, "tools"))
                 import time_to_target
                 line["time_to_target"] = time_to_target.measure(n_seeds=args.ttt_seeds)
+                # the paper's GPU claim: SAIS vs ZJA at equal relative variance
+                line["time_to_target"]["zja_vs_sais"] = time_to_target.zja_vs_sais()
             except Exception as exc:  # reported, never required
                 line["time_to_target"] = {"unavailable": str(exc)}
         print(json.dumps(line), flush=True)
