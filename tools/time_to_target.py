@@ -140,14 +140,20 @@ def measure_config(c, n_seeds, cpu_reps=3):
     else:
         ref = cpu_ref()
     tg = cfg["target"]()
-    # p-steps of the level; beyond ~2e7 the CPU run is a scaled-down N1 (same rounds, same
-    # T plan) and its time is scaled by the p-step ratio (reported as extrapolated)
+    # p-steps of the level; a level the CPU cannot run in ~20 s is timed on a scaled-down N1
+    # (same rounds, same T plan) and scaled by the p-step ratio (reported as extrapolated):
+    # the sample size comes from the CPU rate of a small probe run
     from paper_2408_12057_b200 import capi
     plan_n, plan_t = capi.plan_steps(k + 1, cfg["n1"], tg.dim, 4096 << 20, cfg["mode"])
     ps_full = sum(a * b for a, b in zip(plan_n, plan_t))
+    n1p = max(64, cfg["n1"] // 64)
+    pn, pt = capi.plan_steps(k + 1, n1p, tg.dim, 4096 << 20, cfg["mode"])
+    t_probe = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], n1p, k + 1, seed=int(seeds[0]),
+                                            workers=workers), 1)
+    rate = sum(a * b for a, b in zip(pn, pt)) / max(t_probe, 1e-6)
     n1c, reps = cfg["n1"], cpu_reps
-    if ps_full > 2e7:
-        n1c, reps = max(256, int(cfg["n1"] * 2e7 / ps_full)), 1
+    if ps_full / rate > 20.0:
+        n1c, reps = max(64, int(cfg["n1"] * 20.0 * rate / ps_full)), 1
     pn, pt = capi.plan_steps(k + 1, n1c, tg.dim, 4096 << 20, cfg["mode"])
     ps_cpu = sum(a * b for a, b in zip(pn, pt))
     cpu = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], n1c, k + 1, seed=int(seeds[i]),
