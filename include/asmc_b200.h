@@ -240,6 +240,15 @@ int asmc_sais_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
  * tail of run_sais_single (drivers.cpp:148-176). Host-side scalar code. */
 int asmc_fold_partials(const asmc_logacc* partials, uint64_t chunks, int32_t steps,
                        uint64_t n_particles, asmc_report* out);
+/* Device-buffer variants (multi-GPU SAIS, distributed.run_sais): the partials are
+ * written to / read from DEVICE memory in the same exchange layout, on exec->stream,
+ * so the all-gather runs device to device and the fold runs on the GPU. */
+int asmc_sais_partials_dev(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
+                           const double* betas, int32_t steps, uint64_t n_particles,
+                           uint64_t p_begin, uint64_t p_end, uint64_t seed, uint64_t round,
+                           const asmc_exec* exec, asmc_logacc* partials_dev);
+int asmc_fold_partials_dev(const asmc_logacc* partials_dev, uint64_t chunks, int32_t steps,
+                           uint64_t n_particles, const asmc_exec* exec, asmc_report* out);
 
 /* Multi-GPU SSMC: run_smc (src/engine.cpp:97-188) with the particles of one round
  * split into contiguous shards, one per GPU, each shard starting at a multiple of
@@ -296,6 +305,18 @@ int asmc_zja_shard_create(const asmc_target_desc* target, const asmc_kernel_desc
 int asmc_zja_shard_eval(asmc_smc_shard* shard);
 int asmc_zja_shard_probe(asmc_smc_shard* shard, double beta, double b2, asmc_logacc* chunk_partials);
 int asmc_zja_shard_set_beta(asmc_smc_shard* shard, int32_t t, double beta);
+/* The same search kept on the device (no host round trip per probe): search_begin arms
+ * it for step t; probe_dev writes this shard's (chunks, 2) partials at the search's
+ * current point to DEVICE memory (stream-ordered, no sync); the caller all-gathers them
+ * (e.g. ncclAllGather, chunk order over ranks) and search_step folds them in chunk order
+ * and advances the bisection identically on every rank, writing betas[t] when done;
+ * probes after that are no-ops.  search_poll (the one synchronising call) reports
+ * done / the chosen beta / the non-monotone warning / probes taken. */
+int asmc_zja_shard_search_begin(asmc_smc_shard* shard, int32_t t, double delta_star);
+int asmc_zja_shard_probe_dev(asmc_smc_shard* shard, asmc_logacc* chunk_partials_dev);
+int asmc_zja_shard_search_step(asmc_smc_shard* shard, const asmc_logacc* all_partials_dev, uint64_t all_chunks);
+int asmc_zja_shard_search_poll(asmc_smc_shard* shard, int32_t* done, double* beta, int32_t* warn,
+                               int32_t* probes);
 /* parity hook: copy this shard's particles (row-major, row_bytes each) and log-weights */
 int asmc_smc_shard_state(asmc_smc_shard* shard, void* rows_host, double* log_w_host);
 

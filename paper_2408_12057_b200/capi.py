@@ -498,6 +498,24 @@ class ZjaShard(SmcShard):
     def set_beta(self, t, beta):
         _check(self._lib.asmc_zja_shard_set_beta(self._h, C.c_int32(t), C.c_double(beta)))
 
+    # device-resident search: no host round trip per probe (asmc_zja_shard_search_*)
+    def search_begin(self, t, delta_star):
+        _check(self._lib.asmc_zja_shard_search_begin(self._h, C.c_int32(t), C.c_double(delta_star)))
+
+    def probe_dev(self, out_ptr):
+        """this shard's (chunks, 2) partials at the search's current point -> device out_ptr"""
+        _check(self._lib.asmc_zja_shard_probe_dev(self._h, C.c_void_p(out_ptr)))
+
+    def search_step(self, all_ptr, all_chunks):
+        _check(self._lib.asmc_zja_shard_search_step(self._h, C.c_void_p(all_ptr), C.c_uint64(all_chunks)))
+
+    def search_poll(self):
+        """(done, chosen beta, warning, probes taken); synchronises the shard's stream"""
+        done, warn, probes, beta = C.c_int32(), C.c_int32(), C.c_int32(), C.c_double()
+        _check(self._lib.asmc_zja_shard_search_poll(self._h, C.byref(done), C.byref(beta), C.byref(warn),
+                                                    C.byref(probes)))
+        return bool(done.value), beta.value, bool(warn.value), probes.value
+
     def report(self, T=None):
         rep, bufs = _report(self.T if T is None else T)
         _check(self._lib.asmc_smc_shard_report(self._h, C.byref(rep)))
@@ -516,5 +534,6 @@ EXPORTED = [
     "asmc_smc_shard_step", "asmc_smc_shard_decide", "asmc_smc_shard_plan", "asmc_smc_shard_pack",
     "asmc_smc_shard_accept", "asmc_smc_shard_report", "asmc_smc_shard_state", "asmc_run_zja",
     "asmc_zja_next_beta", "asmc_run_pt", "asmc_profile_collect_drawn", "asmc_zja_shard_create",
-    "asmc_zja_shard_eval", "asmc_zja_shard_probe", "asmc_zja_shard_set_beta",
+    "asmc_zja_shard_eval", "asmc_zja_shard_probe", "asmc_zja_shard_set_beta", "asmc_zja_shard_search_begin",
+    "asmc_zja_shard_probe_dev", "asmc_zja_shard_search_step", "asmc_zja_shard_search_poll",
 ]

@@ -2173,9 +2173,10 @@ struct asmc_smc_shard {
   RoundBufs R;
   std::vector<uint64_t> slots;
   // multi-GPU ZJA mode: open-ended schedule (betas[t] set per step), potential cache, probes
-  int zja = 0;
+  int zja = 0, zt = 0;
   DBuf<double> lr, V;
   DBuf<LogAcc> zpart, zchunk;
+  DBuf<ZjaSearch> zs;  // device-resident search state (asmc_zja_shard_search_*)
 };
 
 extern "C" {
@@ -2420,6 +2421,7 @@ int asmc_zja_shard_create(const asmc_target_desc* target, const asmc_kernel_desc
     TRY(h->V.alloc(h->n_local, s));
     TRY(h->zpart.alloc(2 * h->nblk, s));
     TRY(h->zchunk.alloc((size_t)kNAcc * h->nch, s));
+    TRY(h->zs.alloc(1, s));
     return 0;
   }();
   if (rc) {
@@ -2451,6 +2453,55 @@ int asmc_zja_shard_probe(asmc_smc_shard* h, double beta, double b2, asmc_logacc*
     out[2 * i] = asmc_logacc{c[i].max, c[i].sum};
     out[2 * i + 1] = asmc_logacc{c[h->nch + i].max, c[h->nch + i].sum};
   }
+  return 0;
+}
+
+// Device-resident search (no host round trip per probe): begin(t) arms the state machine
+// at beta_{t-1}; each probe_dev writes this shard's (chunks, 2) partials at the search's
+// current point to device memory; the caller all-gathers them (chunk order over ranks)
+// and search_step folds them and advances the search -- identically on every rank --,
+// writing betas[t] once it is done.  poll() is the only synchronising call.
+int asmc_zja_shard_search_begin(asmc_smc_shard* h, int32_t t, double delta_star) {
+  if (!h || !h->zja) return fail(ASMC_ERR_INVALID_ARGUMENT, "not a ZJA shard");
+  if (!(delta_star > 0.0)) return fail(ASMC_ERR_INVALID_ARGUMENT, "delta_star must be positive");
+  if (t < 1 || t > h->T) return fail(ASMC_ERR_EVALUATION, "online adaptation failed to reach beta = 1 within %d steps", h->T);
+  h->zt = t;
+  LCH(launch_zja_search_init(h->zs.p, h->betas.p, t, delta_star, 1e-10, h->C.stream));
+  return 0;
+}
+
+int asmc_zja_shard_probe_dev(asmc_smc_shard* h, asmc_logacc* partials_dev) {
+  if (!h || !h->zja || !partials_dev || h->zt < 1)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "not a ZJA shard with an open search, or null output");
+  cudaStream_t s = h->C.stream;
+  LCH(launch_zja_probe_dev(h->lw.p, h->V.p, h->n_local, h->zs.p, h->zpart.p, h->nblk, s));
+  LCH(launch_fold_chunks(h->zpart.p, h->nblk, h->nblk, 0, 1, 2, h->nch, h->zchunk.p, s));
+  LCH(launch_zja_interleave(h->zchunk.p, h->nch, h->zs.p, reinterpret_cast<LogAcc*>(partials_dev), s));
+  return 0;
+}
+
+int asmc_zja_shard_search_step(asmc_smc_shard* h, const asmc_logacc* all_partials_dev, uint64_t all_chunks) {
+  if (!h || !h->zja || !all_partials_dev || h->zt < 1)
+    return fail(ASMC_ERR_INVALID_ARGUMENT, "not a ZJA shard with an open search, or null partials");
+  LCH(launch_zja_search_step(h->zs.p, reinterpret_cast<const LogAcc*>(all_partials_dev), all_chunks, h->betas.p,
+                             h->zt, nullptr, &h->R.st.p->err, h->C.stream));
+  return 0;
+}
+
+int asmc_zja_shard_search_poll(asmc_smc_shard* h, int32_t* done, double* beta, int32_t* warn, int32_t* probes) {
+  if (!h || !h->zja || h->zt < 1) return fail(ASMC_ERR_INVALID_ARGUMENT, "not a ZJA shard with an open search");
+  ZjaSearch z;
+  int err = 0;
+  cudaStream_t s = h->C.stream;
+  CU(cudaMemcpyAsync(&z, h->zs.p, sizeof z, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(&err, &h->R.st.p->err, sizeof err, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  if (err == ASMC_ERR_DEGENERATE) return fail(ASMC_ERR_DEGENERATE, "all log-weights are -inf");
+  TRY(device_error(err, h->zt, 0.0));
+  if (done) *done = z.phase == kZjaSearchDone;
+  if (beta) *beta = z.chosen;
+  if (warn) *warn = z.warn;
+  if (probes) *probes = z.probes;
   return 0;
 }
 

@@ -261,8 +261,8 @@ cudaError_t launch_zja_eval(const TgtParams& T, bool fp64_state, const void* con
 // dhat(b2) -- or, with b2 < 0, the log-sum-exp of the log-weights in m1 -- as a fixed
 // tree (thread = particle, warp xor butterfly, warps in order), written to
 // part[a * stride + blk] (a = 0: m1, a = 1: m2); the caller folds blocks into chunks.
-__global__ void zja_probe_blocks_kernel(const double* lw, const double* V, uint64_t n, double beta, double b2,
-                                        LogAcc* part, uint64_t stride) {
+__device__ __forceinline__ void zja_probe_body(const double* lw, const double* V, uint64_t n, double beta,
+                                               double b2, LogAcc* part, uint64_t stride) {
   const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   LogAcc m1 = lacc_empty(), m2 = lacc_empty();
   if (p < n) {
@@ -293,9 +293,166 @@ __global__ void zja_probe_blocks_kernel(const double* lw, const double* V, uint6
   }
 }
 
+__global__ void zja_probe_blocks_kernel(const double* lw, const double* V, uint64_t n, double beta, double b2,
+                                        LogAcc* part, uint64_t stride) {
+  zja_probe_body(lw, V, n, beta, b2, part, stride);
+}
+
 cudaError_t launch_zja_probe_blocks(const double* lw, const double* V, uint64_t n, double beta, double b2,
                                     LogAcc* part, uint64_t stride, cudaStream_t s) {
   zja_probe_blocks_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lw, V, n, beta, b2, part, stride);
+  return cudaGetLastError();
+}
+
+// ---- device-resident multi-GPU search: zja_search above as a resumable state machine
+// whose probe point lives in HBM.  Every rank holds an identical ZjaSearch and advances
+// it from the same all-gathered chunk partials, so the ranks stay in lock step with no
+// host round trip per probe: probe (reads S->b2) -> all-gather -> step (folds in chunk
+// order, takes the branch, writes the next S->b2).  Once done, further probes are no-ops.
+enum : int { kZsM0 = 0, kZsTest1 = 1, kZsBisect = 2, kZsScan = 3, kZsFallback = 4, kZsDone = kZjaSearchDone };
+constexpr int kZjaGridPoints = 16;  // schedule.cpp:254-261
+
+__global__ void zja_search_init_kernel(ZjaSearch* S, const double* betas, int t, double delta, double tol) {
+  ZjaSearch z{};
+  z.beta = betas[t - 1];
+  z.delta = delta;
+  z.tol = tol;
+  z.b2 = -1.0;
+  z.chosen = z.beta;
+  z.phase = kZsM0;
+  *S = z;
+}
+
+__global__ void zja_probe_dev_kernel(const double* lw, const double* V, uint64_t n, const ZjaSearch* S,
+                                     LogAcc* part, uint64_t stride) {
+  const int phase = S->phase;  // block-uniform
+  if (phase == kZsDone) return;
+  zja_probe_body(lw, V, n, S->beta, phase == kZsM0 ? -1.0 : S->b2, part, stride);
+}
+
+// chunk-major (m1, m2) pairs: the exchange layout (all-gathered = chunk order over ranks)
+__global__ void zja_interleave_kernel(const LogAcc* zchunk, uint64_t nch, const ZjaSearch* S, LogAcc* out) {
+  if (S->phase == kZsDone) return;
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += (uint64_t)gridDim.x * blockDim.x) {
+    out[2 * c] = zchunk[c];
+    out[2 * c + 1] = zchunk[nch + c];
+  }
+}
+
+__device__ __forceinline__ bool zs_bisect_next(ZjaSearch& z) {
+  if (z.hi - z.lo > z.tol) {
+    z.b2 = 0.5 * (z.lo + z.hi);
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void zs_scan_point(ZjaSearch& z) {
+  z.b2 = z.beta + (z.root - z.beta) * (double)z.scan_i / kZjaGridPoints;
+}
+
+__device__ __forceinline__ void zs_start_scan(ZjaSearch& z) {
+  z.root = z.lo;
+  z.phase = kZsScan;
+  z.scan_i = 1;
+  zs_scan_point(z);
+}
+
+__device__ __forceinline__ void zs_finish(ZjaSearch& z, double v) {
+  z.chosen = v;
+  z.phase = kZsDone;
+}
+
+__global__ void zja_search_step_kernel(ZjaSearch* S, const LogAcc* all, uint64_t nch, double* betas, int t,
+                                       int* warn, int* err) {
+  ZjaSearch z = *S;
+  if (z.phase == kZsDone) return;
+  LogAcc a = lacc_empty(), b = lacc_empty();
+  for (uint64_t c = 0; c < nch; ++c) {  // chunk order: the same bits on every rank
+    lacc_combine(a, all[2 * c]);
+    lacc_combine(b, all[2 * c + 1]);
+  }
+  ++z.probes;
+  if (z.phase == kZsM0) {  // logsumexp of the log-weights (drivers.cpp's log_m0)
+    z.log_m0 = lacc_log_total(a);
+    if (z.log_m0 == -__builtin_huge_val()) {
+      *err = ASMC_ERR_DEGENERATE;
+      z.phase = kZsDone;
+    } else {
+      z.phase = kZsTest1;
+      z.b2 = 1.0;
+    }
+    *S = z;
+    return;
+  }
+  const double raw = lacc_log_total(b) - 2.0 * lacc_log_total(a) + z.log_m0;  // schedule.cpp:201-215
+  const double d = raw > 0.0 ? raw : 0.0;
+  const double x = z.b2;  // the point just probed
+  switch (z.phase) {
+    case kZsTest1:
+      if (d <= z.delta) {
+        zs_finish(z, 1.0);
+        break;
+      }
+      z.lo = z.beta;
+      z.hi = 1.0;
+      z.phase = kZsBisect;
+      if (!zs_bisect_next(z)) zs_start_scan(z);
+      break;
+    case kZsBisect:
+      if (d <= z.delta) z.lo = x;
+      else z.hi = x;
+      if (!zs_bisect_next(z)) zs_start_scan(z);
+      break;
+    case kZsScan:
+      if (d > z.delta * (1.0 + 1e-12)) {  // non-monotone: bisect (beta, probe]
+        z.warn = 1;
+        z.lo = z.beta;
+        z.hi = x;
+        z.phase = kZsFallback;
+        if (!zs_bisect_next(z)) zs_finish(z, z.lo);
+      } else if (++z.scan_i < kZjaGridPoints) {
+        zs_scan_point(z);
+      } else {
+        zs_finish(z, z.root);
+      }
+      break;
+    case kZsFallback:
+      if (d <= z.delta) z.lo = x;
+      else z.hi = x;
+      if (!zs_bisect_next(z)) zs_finish(z, z.lo);
+      break;
+    default:
+      break;
+  }
+  if (z.phase == kZsDone) {
+    betas[t] = z.chosen;
+    if (z.warn && warn) *warn = 1;
+  }
+  *S = z;
+}
+
+cudaError_t launch_zja_search_init(ZjaSearch* S, const double* betas, int t, double delta, double tol,
+                                   cudaStream_t s) {
+  zja_search_init_kernel<<<1, 1, 0, s>>>(S, betas, t, delta, tol);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zja_probe_dev(const double* lw, const double* V, uint64_t n, const ZjaSearch* S, LogAcc* part,
+                                 uint64_t stride, cudaStream_t s) {
+  zja_probe_dev_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lw, V, n, S, part, stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zja_interleave(const LogAcc* zchunk, uint64_t nch, const ZjaSearch* S, LogAcc* out,
+                                  cudaStream_t s) {
+  zja_interleave_kernel<<<(unsigned)((nch + 127) / 128), 128, 0, s>>>(zchunk, nch, S, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zja_search_step(ZjaSearch* S, const LogAcc* all, uint64_t nch, double* betas, int t, int* warn,
+                                   int* err, cudaStream_t s) {
+  zja_search_step_kernel<<<1, 1, 0, s>>>(S, all, nch, betas, t, warn, err);
   return cudaGetLastError();
 }
 

@@ -35,4 +35,22 @@ int zja_grid_blocks(int device);
 cudaError_t launch_zja_probe_blocks(const double* lw, const double* V, uint64_t n, double beta, double b2,
                                     LogAcc* part, uint64_t stride, cudaStream_t s);
 
+// multi-GPU device-resident search (zja_search as a state machine; see zja.cu)
+constexpr int kZjaSearchDone = 5;  // ZjaSearch::phase once beta_t is chosen
+struct ZjaSearch {
+  double beta, delta, tol, log_m0;
+  double b2;            // the next probe point (phase 0: the log-weights' lse)
+  double lo, hi, root;  // bisection interval / first root
+  double chosen;        // beta_t once phase == done
+  int phase, scan_i, warn, probes;
+};
+cudaError_t launch_zja_search_init(ZjaSearch* S, const double* betas, int t, double delta, double tol,
+                                   cudaStream_t s);
+cudaError_t launch_zja_probe_dev(const double* lw, const double* V, uint64_t n, const ZjaSearch* S, LogAcc* part,
+                                 uint64_t stride, cudaStream_t s);
+cudaError_t launch_zja_interleave(const LogAcc* zchunk, uint64_t nch, const ZjaSearch* S, LogAcc* out,
+                                  cudaStream_t s);
+cudaError_t launch_zja_search_step(ZjaSearch* S, const LogAcc* all, uint64_t nch, double* betas, int t, int* warn,
+                                   int* err, cudaStream_t s);
+
 }  // namespace asmcdev

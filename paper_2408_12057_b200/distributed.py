@@ -366,10 +366,26 @@ def zja_search(dhat, beta, delta, tol=1e-10):
     return root, False
 
 
+def _bisect_probes(beta, tol=1e-10):
+    """probes bisect(beta, 1) takes when the interval halves exactly (a lower bound)"""
+    k, w = 0, 1.0 - beta
+    while w > tol:
+        w *= 0.5
+        k += 1
+    return k
+
+
 def run_zja_multi(target, kernel, n, delta_star, seed=0, exec_=None, comm=None, rank=0, world=1, max_steps=100000,
-                  round=1, stats=None):
+                  round=1, stats=None, device_search=True):
     """run_zja's adaptive round (delta_star > 0) sharded over `world` GPUs; returns the
-    run report with the chosen schedule (`betas`) on every rank."""
+    run report with the chosen schedule (`betas`) on every rank.
+
+    device_search=True keeps the bisection on the device (asmc_zja_shard_search_*):
+    probe -> all-gather -> step are stream-ordered with no host round trip; the host
+    enqueues a batch of probes sized to the search's expected length (test + bisection
+    + 15-point scan) and polls once, adding small batches only for the non-monotone
+    fallback.  device_search=False is the host-driven search (one synchronising
+    all-gather per probe), kept for A/B."""
     import torch
     from . import capi
     if not delta_star > 0:
@@ -401,6 +417,7 @@ def run_zja_multi(target, kernel, n, delta_star, seed=0, exec_=None, comm=None, 
         betas = [0.0]
         warning = False
         t = 0
+        launched = polls = 0
         while betas[-1] < 1.0:
             t += 1
             if t > max_steps:
@@ -409,9 +426,7 @@ def run_zja_multi(target, kernel, n, delta_star, seed=0, exec_=None, comm=None, 
             beta = betas[-1]
             for s in shards:
                 s.eval()
-            log_m0 = _lacc_total(fold(gathered([s.probe(beta, -1.0) for s in shards]), 0))
-            if log_m0 == -math.inf:
-                raise capi.AsmcError(abi.ERR_DEGENERATE, "all log-weights are -inf")
+            log_m0 = None
 
             def dhat(b2):
                 nonlocal probes
@@ -420,11 +435,35 @@ def run_zja_multi(target, kernel, n, delta_star, seed=0, exec_=None, comm=None, 
                 raw = _lacc_total(fold(allp, 1)) - 2.0 * _lacc_total(fold(allp, 0)) + log_m0
                 return raw if raw > 0.0 else 0.0
 
-            b, w = zja_search(dhat, beta, delta_star)
+            if device_search:
+                for s in shards:
+                    s.search_begin(t, delta_star)
+                zp = [torch.empty((s.chunks, 2, 2), dtype=torch.float64, device=dev) for s in shards]
+                batch = 2 + _bisect_probes(beta) + 15
+                while True:
+                    for _ in range(batch):
+                        for s, z in zip(shards, zp):
+                            s.probe_dev(z.data_ptr())
+                        allz = comm.allgather(zp, n_chunks)
+                        for s, a in zip(shards, allz):
+                            s.search_step(a.data_ptr(), a.shape[0])
+                        launched += 1
+                    polls += 1
+                    done, b, w, taken = shards[0].search_poll()
+                    if done:
+                        break
+                    batch = 8
+                probes += taken
+            else:
+                log_m0 = _lacc_total(fold(gathered([s.probe(beta, -1.0) for s in shards]), 0))
+                if log_m0 == -math.inf:
+                    raise capi.AsmcError(abi.ERR_DEGENERATE, "all log-weights are -inf")
+                b, w = zja_search(dhat, beta, delta_star)
+                for s in shards:
+                    s.set_beta(t, b)
             warning = warning or w
             betas.append(b)
             for s, p in zip(shards, parts):
-                s.set_beta(t, b)
                 s.step(t, p.data_ptr())
             allp = comm.allgather(parts, n_chunks)
             for s, a, bt in zip(shards, allp, lws):  # policy never: no exchange
@@ -436,6 +475,12 @@ def run_zja_multi(target, kernel, n, delta_star, seed=0, exec_=None, comm=None, 
     for r in reps:
         r.update(betas=np.array(betas), steps=t, warning=warning, delta_star=delta_star)
     if stats is not None:
-        stats["probes"] = probes
-        stats["collectives"] = probes + 2 * t  # probes + log_m0 + step partials per step
+        stats["probes"] = probes  # incl. the log_m0 probe on the device path
+        if device_search:
+            stats["probes_launched"] = launched  # incl. no-op probes after the search ended
+            stats["host_syncs"] = polls
+            stats["collectives"] = launched + t
+        else:
+            stats["host_syncs"] = probes + t
+            stats["collectives"] = probes + 2 * t  # probes + log_m0 + step partials per step
     return reps

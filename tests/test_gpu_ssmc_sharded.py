@@ -115,3 +115,24 @@ def test_multi_gpu_zja_identical_for_any_shard_count():
     assert np.max(np.abs(single["rounds"][-1]["betas"] - one[0]["betas"])) < 1e-6
     assert abs(single["rounds"][-1]["log_z_hat"] - one[0]["log_z_hat"]) < 1e-6
     assert stats["probes"] > 20 * one[0]["steps"]  # the communication the paper's SAIS avoids
+    # the device-resident search syncs with the host about once per annealing step
+    assert stats["host_syncs"] <= 2 * one[0]["steps"]
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_multi_gpu_zja_device_search_matches_host_search(world):
+    """asmc_zja_shard_search_* (state machine in HBM, no host round trip per probe) against
+    the host-driven search over the same all-gathered partials: the same schedule up to the
+    fold's last-ulp libm differences, the same warnings, far fewer host synchronisations."""
+    k = abi.kernel(abi.KERNEL_RWMH, (0.1, 0.5, 1.0), 1)
+    ex = abi.execopts(PH, F32)
+    for tg, delta in ((abi.gaussian_shift(0.0, 2.0, 1.0, 4), 0.05),
+                      (abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 2), 0.02)):
+        sd, sh = {}, {}
+        dev = distributed.run_zja_multi(tg, k, N, delta, seed=5, exec_=ex, world=world, stats=sd)
+        host = distributed.run_zja_multi(tg, k, N, delta, seed=5, exec_=ex, world=world, stats=sh,
+                                         device_search=False)
+        assert dev[0]["steps"] == host[0]["steps"] and dev[0]["warning"] == host[0]["warning"]
+        assert np.max(np.abs(dev[0]["betas"] - host[0]["betas"])) < 1e-9
+        assert abs(dev[0]["log_z_hat"] - host[0]["log_z_hat"]) < 1e-8
+        assert sd["host_syncs"] * 10 < sh["host_syncs"]
