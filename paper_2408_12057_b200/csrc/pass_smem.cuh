@@ -514,7 +514,7 @@ struct SmemOps {
       }
       if constexpr (Tgt::kEarly) {
         // warp-uniform: every lane runs mmax iterations
-        if (m < 7 && m + 1 < mmax && m >= mfirst) {
+        if (((Tgt::kCheckMask >> m) & 1u) && m + 1 < mmax && m >= mfirst) {
           const float rem = Tgt::kBoundFromV ? Tgt::bound_of_v(kf, vs - bp) : bnd - bp;
           if constexpr (Tgt::kQuadMH) dl = Tgt::dl_from(kf, s, sA, sB);
           if (certainly_rejected(dl, rem, lu)) {

@@ -78,6 +78,7 @@ struct TgtGaussShift {
   __device__ static float vpart(const F32&, float x) { return x; }
   // early rejection: max over h of dlg(x, h) (a concave quadratic in h)
   static constexpr bool kEarly = true;
+  static constexpr unsigned kCheckMask = 0x7Fu;  // early-rejection checks after quad-iterations 0..6
   static constexpr bool kBoundFromV = false;
   static constexpr bool kQuadMH = false;
   __device__ static float bound_of_v(const F32&, float) { return 0.f; }
@@ -130,7 +131,11 @@ struct TgtMixture {
   }
   // early rejection: f_beta(y) = beta (hi + log1p) - (1 - beta) sr^2 / 2 <= beta lmix, so
   // max_h dlg(x, h) <= beta (lmix - vterm(x)) + sr(x)^2 / 2  (v = the cached vterm(x))
-  static constexpr bool kEarly = false;  // bound too loose at d = 100 to pay for its bookkeeping
+#ifndef ASMC_MIX_EARLY
+#define ASMC_MIX_EARLY 0
+#endif
+  static constexpr bool kEarly = ASMC_MIX_EARLY != 0;
+  static constexpr unsigned kCheckMask = ASMC_MIX_EARLY == 2 ? 0x0Au : 0x7Fu;
   static constexpr bool kBoundFromV = false;
   static constexpr bool kQuadMH = false;
   __device__ static float bound_of_v(const F32&, float) { return 0.f; }
@@ -236,6 +241,7 @@ struct TgtScale {
   __device__ static float vpart(const F32&, float x) { return x * x; }
   // early rejection: max over h of -tau h (x + h/2) = tau x^2 / 2
   static constexpr bool kEarly = true;
+  static constexpr unsigned kCheckMask = 0x7Fu;  // early-rejection checks after quad-iterations 0..6
   __device__ static float dmax(const F32& k, float x, float) { return 0.5f * k.tau * x * x; }
   // dmax summed over coordinates = (tau / 2) * sum vpart(x): the pass derives the bound of
   // the unprocessed coordinates from the carried vpart sum, no separate bound pass

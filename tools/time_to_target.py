@@ -147,23 +147,30 @@ def measure_config(c, n_seeds, cpu_reps=3):
     plan_n, plan_t = capi.plan_steps(k + 1, cfg["n1"], tg.dim, 4096 << 20, cfg["mode"])
     ps_full = sum(a * b for a, b in zip(plan_n, plan_t))
     n1p = max(64, cfg["n1"] // 64)
-    pn, pt = capi.plan_steps(k + 1, n1p, tg.dim, 4096 << 20, cfg["mode"])
-    t_probe = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], n1p, k + 1, seed=int(seeds[0]),
+    pn, pt = capi.plan_steps(1, n1p, tg.dim, 4096 << 20, cfg["mode"])
+    t_probe = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], n1p, 1, seed=int(seeds[0]),
                                             workers=workers), 1)
     rate = sum(a * b for a, b in zip(pn, pt)) / max(t_probe, 1e-6)
-    n1c, reps = cfg["n1"], cpu_reps
-    if ps_full / rate > 20.0:
+    n1c, rc, reps = cfg["n1"], k + 1, cpu_reps
+
+    def ps_of(n1_, r_):
+        a, b = capi.plan_steps(r_, n1_, tg.dim, 4096 << 20, cfg["mode"])
+        return sum(x * y for x, y in zip(a, b))
+
+    if ps_full / rate > 20.0:  # scale N1 down, then drop the last rounds if still too long
         n1c, reps = max(64, int(cfg["n1"] * 20.0 * rate / ps_full)), 1
-    pn, pt = capi.plan_steps(k + 1, n1c, tg.dim, 4096 << 20, cfg["mode"])
-    ps_cpu = sum(a * b for a, b in zip(pn, pt))
-    cpu = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], n1c, k + 1, seed=int(seeds[i]),
+        while rc > 1 and ps_of(n1c, rc) / rate > 30.0:
+            rc -= 1
+    ps_cpu = ps_of(n1c, rc)
+    cpu = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], n1c, rc, seed=int(seeds[i]),
                                         workers=workers), reps) * ps_full / ps_cpu
     res["time_to_target"] = {
         "rounds_needed": k + 1, "b200_wall_s": res["b200_wall_s_by_round"][k], "cpu_wall_s": cpu,
         "cpu_cores": workers,
         "cpu_kind": "port (oracle/restate.c, one core: the reference has no HMC)" if port else
                     "reference (unmodified run_sais/run_ssmc, -O3)",
-        "cpu_extrapolated": n1c != cfg["n1"], "cpu_sample_n1": n1c,
+        "cpu_extrapolated": n1c != cfg["n1"] or rc != k + 1, "cpu_sample_n1": n1c, "cpu_sample_rounds": rc,
+        "cpu_sample_psteps": ps_cpu, "psteps_full": ps_full,
         "speedup_wall": cpu / res["b200_wall_s_by_round"][k]}
     if cfg["batched"]:
         res["time_to_target"]["b200_batched_wall_s_per_seed"] = res["b200_batched_wall_s_per_seed_by_round"][k]
