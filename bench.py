@@ -322,16 +322,16 @@ def other_configs(stream, ex, peak_normals, peaks):
         wall = time.perf_counter() - t0
         pr = None
         if prof:
-            pr = capi.profile_collect()
+            pr = capi.profile_collect(drawn=True)  # (ms, algorithmic units, drawn normals) per launch
             capi.profile_enable(False)
         return r, e0.elapsed_time(e1) * 1e-3, wall, pr
 
     # config 3: SSMC, adaptive ESS, d=100 bimodal mixture, N=2^22, 6 rounds
     tg = abi.mixture(2.0, 0.5, -1.0, 0.5, 1.0, 0.5, 100)
     k = abi.kernel(abi.KERNEL_RWMH, STEPS, 1)
-    r, dt, wall, (pms, pnorm) = timed(lambda: capi.run_rounds(tg, k, abi.MODE_SSMC, 1 << 22, 6,
-                                                             policy=abi.POLICY_ADAPTIVE_ESS, seed=SEED, exec_=ex),
-                                      prof=True)
+    r, dt, wall, (pms, pnorm, pdrawn) = timed(lambda: capi.run_rounds(tg, k, abi.MODE_SSMC, 1 << 22, 6,
+                                                                     policy=abi.POLICY_ADAPTIVE_ESS, seed=SEED,
+                                                                     exec_=ex), prof=True)
     ps = float(np.sum(r["kernel_applications"]))
     pass_s = float(np.sum(pms)) * 1e-3
     ach = float(np.sum(pnorm)) / pass_s
@@ -342,8 +342,12 @@ def other_configs(stream, ex, peak_normals, peaks):
                       "roofline": {"bound": "issue", "kernel": "pass_smem_kernel<TgtMixture, 4> (SMC step mode)",
                                    "achieved": ach / 1e9, "peak": peak_normals / 1e9, "unit": "Gnormal/s",
                                    "frac": ach / peak_normals, "pass_share_of_device_time": pass_s / dt,
-                                   "algorithmic_units": "normals = N*d per init + N*S*d per step (no early "
-                                                        "rejection on the mixture: drawn = algorithmic)",
+                                   "algorithmic_units": "normals = N*d per init + N*S*d per step (the RWMH "
+                                                        "algorithm's draws)",
+                                   "drawn": {"fraction_of_algorithmic": float(np.sum(pdrawn)) / float(np.sum(pnorm)),
+                                             "frac": float(np.sum(pdrawn)) / pass_s / peak_normals,
+                                             "note": "normals generated: the s = 10 proposals are early-rejected "
+                                                     "after their first quad-iteration (TgtMixture::early_worth)"},
                                    "hbm": {"bytes_per_pstep": 8 * 100 + 16,
                                            "achieved_gbs": ps * (8 * 100 + 16) / pass_s / 1e9,
                                            "peak": peaks.get("hbm_gbs"),
@@ -356,7 +360,7 @@ def other_configs(stream, ex, peak_normals, peaks):
     tg = abi.logistic(X, y, 1.0)
     k = abi.kernel(abi.KERNEL_RWMH, (0.002, 0.005, 0.01), 1)
     betas = np.linspace(0.0, 1.0, 5)
-    r, dt, wall, (ms, flops) = timed(lambda: capi.run_sais_single(tg, k, betas, 1 << 20, seed=SEED, round=1,
+    r, dt, wall, (ms, flops, _) = timed(lambda: capi.run_sais_single(tg, k, betas, 1 << 20, seed=SEED, round=1,
                                                                    exec_=ex), prof=True)
     ev_ms, ev_flops = float(np.sum(ms)), float(np.sum(flops))
     alg_tf = ev_flops / (ev_ms * 1e-3) / 1e12

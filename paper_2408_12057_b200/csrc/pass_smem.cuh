@@ -217,12 +217,19 @@ struct SmemOps {
     // early rejection: this lane's sum of max_h dlg(x_i, h) over its coordinates
     // (targets with kBoundFromV derive it from vs inside delta_pass)
     constexpr bool kBnd = Tgt::kEarly && !Tgt::kBoundFromV;
-    float bnd = kBnd ? bound_total(kf, lane, d, nq, xq) : 0.f;
+    float bnd = 0.f;
+    bool bnd_ok = false;  // bnd holds the current row's bound (computed before a checking proposal)
     double u_pre = 1.0;  // lane l holds u of proposal (q0 + l)
     int si = 0;  // p % n_steps
     for (int p = 0; p < nprop; ++p) {
       const float s = (float)kc.steps[si];
       si = si + 1 == kc.n_steps ? 0 : si + 1;
+      bool chk = Tgt::kEarly;  // does this proposal run early-rejection checks?
+      if constexpr (Tgt::kPerProposalCheck) chk = !kc.no_early && Tgt::early_worth(kf, s, d, 4 * G);
+      if (kBnd && chk && !bnd_ok) {
+        bnd = bound_total(kf, lane, d, nq, xq);
+        bnd_ok = true;
+      }
       const uint64_t base = (uint64_t)p * (uint64_t)d;
       if ((p % G) == 0) {  // lane l draws the uniform of proposal p + l
         const int pp = p + lane;
@@ -250,10 +257,16 @@ struct SmemOps {
           mfirst = max(0, (int)ceilf(need) - 2);
         }
       }
-      const float dl = aligned ? delta_pass<true>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst,
-                                                  rejected, vs_new, drawn)
-                               : delta_pass<false>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst,
-                                                   rejected, vs_new, drawn);
+#define ASMC_DELTA(A, C) \
+  delta_pass<A, C>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst, rejected, vs_new, drawn)
+      float dl;
+      if constexpr (Tgt::kPerProposalCheck) {
+        if (chk) dl = aligned ? ASMC_DELTA(true, true) : ASMC_DELTA(false, true);
+        else dl = aligned ? ASMC_DELTA(true, false) : ASMC_DELTA(false, false);
+      } else {
+        dl = aligned ? ASMC_DELTA(true, Tgt::kEarly) : ASMC_DELTA(false, Tgt::kEarly);
+      }
+#undef ASMC_DELTA
       if (rejected) continue;  // certainly rejected: the remaining normals are never drawn
       const double delta = group_sum<G>((double)dl);
       if (accept_decision(u, log_u, delta)) {  // kernel.cpp:35: accept iff log u < delta
@@ -264,12 +277,13 @@ struct SmemOps {
           xq = xalt;
           xalt = t;
           vs = vs_new;
-          if (kBnd) bnd = bound_total(kf, lane, d, nq, xq);
+          bnd_ok = false;
         } else {  // regenerate the proposal's normals
           const float nb = aligned ? accept_pass<true>(kf, k, lane, nq, base, s, xq)
                                    : accept_pass<false>(kf, k, lane, nq, base, s, xq);
           drawn += (uint32_t)((nq - lane + G - 1) / G);
-          if (kBnd) bnd = nb;
+          bnd = nb;
+          bnd_ok = kBnd;
           vs = vsum(T, lane, d, xq);
         }
       }
@@ -452,11 +466,13 @@ struct SmemOps {
 
   // sum over this lane's quads of f_beta(x + s z) - f_beta(x), writing x + s z to the
   // spare row and its vpart sum to vs_new.  Early rejection (exact): after quad-iteration
-  // m (m < 7, m >= mfirst; kNoChecks = none) the warp checks
+  // m (m < 7 in Tgt::kCheckMask, m >= mfirst; kNoChecks = none) the warp checks
   //   partial + sum over unprocessed coordinates of max_h dlg  <  log u
   // (certainly_rejected); then the proposal is rejected whatever the remaining normals
   // are, so they are not drawn.  Accepted proposals see the identical sum.
-  template <bool kAligned>
+  static constexpr int kLastCheck = 31 - __builtin_clz(Tgt::kCheckMask | 1u);  // last checked quad-iteration
+
+  template <bool kAligned, bool kCheck>
   __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKeyC& k, int lane, int d, int nq,
                                      uint64_t base, float s, const float4* xq, float4* xalt, float log_u,
                                      float bnd, float vs, int mfirst, bool& rejected, float& vs_new,
@@ -492,7 +508,7 @@ struct SmemOps {
           for (int e = 0; e < 4; ++e)
             if (kAligned || 4 * q + e < d) {
               dl += Tgt::dlg_vv(kf, xv[e], vv[e], xp[e], vp[e]);  // == dlg_cached
-              if (Tgt::kEarly) bp += Tgt::dmax(kf, xv[e], vv[e]);
+              if (kCheck && (kLastCheck >= 6 || m <= kLastCheck)) bp += Tgt::dmax(kf, xv[e], vv[e]);
               vn += vp[e];
             }
           if constexpr (kDual) xalt[nq + q] = make_float4(vp[0], vp[1], vp[2], vp[3]);
@@ -506,13 +522,14 @@ struct SmemOps {
               } else {
                 dl += Tgt::dlg(kf, xv[e], s * z[e]);
               }
-              if (Tgt::kEarly) bp += Tgt::kBoundFromV ? Tgt::vpart(kf, xv[e]) : Tgt::dmax(kf, xv[e], 0.f);
+              if (kCheck && (kLastCheck >= 6 || m <= kLastCheck))
+                bp += Tgt::kBoundFromV ? Tgt::vpart(kf, xv[e]) : Tgt::dmax(kf, xv[e], 0.f);
               vn += Tgt::vpart(kf, xp[e]);
             }
         }
         if constexpr (kDual) xalt[q] = make_float4(xp[0], xp[1], xp[2], xp[3]);
       }
-      if constexpr (Tgt::kEarly) {
+      if constexpr (kCheck) {
         // warp-uniform: every lane runs mmax iterations
         if (((Tgt::kCheckMask >> m) & 1u) && m + 1 < mmax && m >= mfirst) {
           const float rem = Tgt::kBoundFromV ? Tgt::bound_of_v(kf, vs - bp) : bnd - bp;

@@ -79,6 +79,7 @@ struct TgtGaussShift {
   // early rejection: max over h of dlg(x, h) (a concave quadratic in h)
   static constexpr bool kEarly = true;
   static constexpr unsigned kCheckMask = 0x7Fu;  // early-rejection checks after quad-iterations 0..6
+  static constexpr bool kPerProposalCheck = false;
   static constexpr bool kBoundFromV = false;
   static constexpr bool kQuadMH = false;
   __device__ static float bound_of_v(const F32&, float) { return 0.f; }
@@ -131,11 +132,24 @@ struct TgtMixture {
   }
   // early rejection: f_beta(y) = beta (hi + log1p) - (1 - beta) sr^2 / 2 <= beta lmix, so
   // max_h dlg(x, h) <= beta (lmix - vterm(x)) + sr(x)^2 / 2  (v = the cached vterm(x))
-#ifndef ASMC_MIX_EARLY
-#define ASMC_MIX_EARLY 0
-#endif
-  static constexpr bool kEarly = ASMC_MIX_EARLY != 0;
-  static constexpr unsigned kCheckMask = ASMC_MIX_EARLY == 2 ? 0x0Au : 0x7Fu;
+  // one check, after the first quad-iteration (c0 = 4G coordinates), and only for the
+  // proposals it can plausibly reject (early_worth; warp-uniform, a cost heuristic --
+  // the check is exact whenever it runs): the large steps of a {0.1, 1, 10} cycle, whose
+  // per-coordinate drop s^2 ((1 - beta) / 2r^2 + beta / 2 sigma_min^2) summed over the
+  // first c0 coordinates already exceeds ~1 per remaining coordinate of the bound.
+  // A/B on config 3 (tools/c3_drawn.py, ab_libs.py): checking every proposal at every
+  // quad-iteration draws 31 % fewer normals but issues 2.5 % more instructions (+1.2 %
+  // p-steps/s: per-coordinate bound terms, re-bounding after every accept, the vote
+  // between the interleaved Philox chains); this form +8 %; one predicted check per
+  // proposal at a runtime iteration (also catching the unit step near beta = 1) 0 %.
+  static constexpr bool kEarly = true;
+  static constexpr unsigned kCheckMask = 0x01u;
+  static constexpr bool kPerProposalCheck = true;
+  __device__ static bool early_worth(const F32& k, float s, int d, int c0) {
+    const float is = fminf(k.inv_s1, k.inv_s2);
+    const float drop = s * s * fmaf(k.beta, 0.5f * is * is - k.hr, k.hr);
+    return (float)c0 * drop > (float)(d - c0);
+  }
   static constexpr bool kBoundFromV = false;
   static constexpr bool kQuadMH = false;
   __device__ static float bound_of_v(const F32&, float) { return 0.f; }
@@ -242,6 +256,7 @@ struct TgtScale {
   // early rejection: max over h of -tau h (x + h/2) = tau x^2 / 2
   static constexpr bool kEarly = true;
   static constexpr unsigned kCheckMask = 0x7Fu;  // early-rejection checks after quad-iterations 0..6
+  static constexpr bool kPerProposalCheck = false;
   __device__ static float dmax(const F32& k, float x, float) { return 0.5f * k.tau * x * x; }
   // dmax summed over coordinates = (tau / 2) * sum vpart(x): the pass derives the bound of
   // the unprocessed coordinates from the carried vpart sum, no separate bound pass
