@@ -28,6 +28,7 @@
 // One cooperative launch per resampling event (phases separated by grid.sync()); under
 // st->resample_now gating the launch returns at once on steps that do not resample.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "engine_kernels.h"
@@ -177,28 +178,94 @@ __device__ __forceinline__ Op block_op(const Args& A, int mode, uint64_t b, doub
   return Op{gexp(__dsub_rn(pm, l)), true};
 }
 
+// ---- the grid phases work on one WARP per 256-particle block ------------------
+// Lane l holds particles b kT + 8 l .. 8 l + 7, consecutive, so lane-local order is
+// particle order and prefix operations are a lane-local pass plus one warp scan.  No CTA
+// barrier inside a phase, and each lane has its 8 loads in flight at once (the phases
+// are L2-latency bound: the 8 B per particle stay L2-resident across them).
+constexpr int kPer = kT / 32;
+
+__device__ __forceinline__ void warp_load(const Args& A, uint64_t b, double (&l)[kPer]) {
+  const uint64_t j0 = b * kT + kPer * (threadIdx.x & 31);
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) l[e] = j0 + e < A.n ? A.lw[j0 + e] : kNegInfD;
+}
+
+// block_op for the lane's 8 particles: v[e] and the rescale bits (LSE: the exclusive
+// prefix max in particle order, seeded with the blocks before, bmax[b] after P1)
+__device__ __forceinline__ unsigned warp_ops(const Args& A, int mode, uint64_t b, const double (&l)[kPer],
+                                             double l1, double (&v)[kPer]) {
+  const int ln = threadIdx.x & 31;
+  const uint64_t j0 = b * kT + kPer * ln;
+  if (mode == kModeCdf) {
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) v[e] = j0 + e < A.n ? gexp(__dsub_rn(l[e], l1)) : 0.0;
+    return 0u;
+  }
+  double inc = l[0];
+#pragma unroll
+  for (int e = 1; e < kPer; ++e) inc = fmax(inc, l[e]);
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (ln >= o) inc = fmax(inc, t);
+  }
+  const double up = __shfl_up_sync(0xffffffffu, inc, 1);
+  double pm = A.w.bmax[b];
+  if (ln > 0) pm = fmax(pm, up);
+  unsigned resc = 0u;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    if (l[e] == kNegInfD) {
+      v[e] = 0.0;
+    } else if (l[e] <= pm) {
+      v[e] = gexp(__dsub_rn(l[e], pm));
+    } else {
+      v[e] = gexp(__dsub_rn(pm, l[e]));
+      resc |= 1u << e;
+    }
+    pm = fmax(pm, l[e]);
+  }
+  return resc;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // ---- phases -------------------------------------------------------------------
 // P0: per-block max of log_w (LSE)
-__device__ void phase_block_max(const Args& A, double* sh) {
-  for (uint64_t b = blockIdx.x; b < A.nblk; b += gridDim.x) {
-    const uint64_t j = b * kT + threadIdx.x;
-    const double m = cta_max(j < A.n ? A.lw[j] : kNegInfD, sh);
-    if (threadIdx.x == 0) A.w.bmax[b] = m;
-    __syncthreads();
+__device__ void phase_block_max(const Args& A) {
+  const uint64_t nw = (uint64_t)gridDim.x * (kT / 32);
+  for (uint64_t b = (uint64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); b < A.nblk; b += nw) {
+    double l[kPer];
+    warp_load(A, b, l);
+    double m = l[0];
+#pragma unroll
+    for (int e = 1; e < kPer; ++e) m = fmax(m, l[e]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) A.w.bmax[b] = m;
   }
 }
 
 // P1 (CTA 0): bmax -> exclusive prefix max over blocks; gmax = max over all
 __device__ void phase_scan_max(const Args& A, double* buf, double* sh) {
   double carry = kNegInfD;
+  auto load = [&](uint64_t t0, double (&v)[4]) {  // tile t0's entries (next tile prefetched)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t i = t0 + 4 * threadIdx.x + e;
+      v[e] = i < A.nblk ? A.w.bmax[i] : kNegInfD;
+    }
+  };
+  double vn[4];
+  load(0, vn);
   for (uint64_t t0 = 0; t0 < A.nblk; t0 += kTile) {
     const int m = (int)min((uint64_t)kTile, A.nblk - t0);
     double v[4], loc = kNegInfD;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int i = 4 * threadIdx.x + e;
-      v[e] = i < m ? A.w.bmax[t0 + i] : kNegInfD;
-    }
+    for (int e = 0; e < 4; ++e) v[e] = vn[e];
+    load(t0 + kTile, vn);
     const double pre0 = cta_excl_max(fmax(fmax(v[0], v[1]), fmax(v[2], v[3])), carry, sh);
     loc = pre0;
 #pragma unroll
@@ -225,29 +292,29 @@ __device__ __forceinline__ Aff aff_then(Aff l, Aff r) {
   return Aff{__dmul_rn(r.a, l.a), __fma_rn(r.a, l.b, r.b)};
 }
 
-// P2: per-block composite of the element maps (approximate; any association)
-__device__ void phase_block_affine(const Args& A, int mode, double l1, double* sh, Aff* ash, int* ish) {
-  for (uint64_t b = blockIdx.x; b < A.nblk; b += gridDim.x) {
-    const Op op = block_op(A, mode, b, l1, sh);
-    Aff f = op.rescale ? Aff{op.v, 1.0} : Aff{1.0, op.v};
-    const int ln = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int o = 1; o < 32; o <<= 1) {  // ordered tree: lane i holds [i, i + 2o) when i % 2o == 0
+// P2: per-block composite of the element maps (approximate; any association): the
+// lane's 8 maps in order, then an ordered shuffle tree (lane i holds [i, i + 2o))
+__device__ void phase_block_affine(const Args& A, int mode, double l1) {
+  const int ln = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (kT / 32);
+  for (uint64_t b = (uint64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); b < A.nblk; b += nw) {
+    double l[kPer], v[kPer];
+    warp_load(A, b, l);
+    const unsigned resc = warp_ops(A, mode, b, l, l1, v);
+    Aff f = (resc & 1u) ? Aff{v[0], 1.0} : Aff{1.0, v[0]};
+#pragma unroll
+    for (int e = 1; e < kPer; ++e) f = aff_then(f, ((resc >> e) & 1u) ? Aff{v[e], 1.0} : Aff{1.0, v[e]});
+    for (int o = 1; o < 32; o <<= 1) {
       const Aff r{__shfl_down_sync(0xffffffffu, f.a, o), __shfl_down_sync(0xffffffffu, f.b, o)};
       if ((ln & (2 * o - 1)) == 0) f = aff_then(f, r);
     }
-    const int special = __syncthreads_or(op.rescale ? 1 : 0);
-    if (ln == 0) ash[w] = f;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      Aff t = ash[0];
-      for (int i = 1; i < kT / 32; ++i) t = aff_then(t, ash[i]);
-      A.w.ba[b] = t.a;
-      A.w.bb[b] = t.b;
+    const bool special = __any_sync(0xffffffffu, resc != 0u);
+    if (ln == 0) {
+      A.w.ba[b] = f.a;
+      A.w.bb[b] = f.b;
       A.w.kb[b] = special ? kUnstable : 0;  // refined in P4
     }
-    __syncthreads();
   }
-  (void)ish;
 }
 
 // P3 (CTA 0): approximate running value at every block start: sstart[b] (b = 0..nblk).
@@ -257,15 +324,24 @@ __device__ void phase_scan_affine(const Args& A, Aff* wsh) {
   const int ln = threadIdx.x & 31, w = threadIdx.x >> 5;
   double carry = 0.0;  // both chains start from s = 0 (logsum.hpp:47-48, engine.cpp:69)
   if (threadIdx.x == 0) A.w.sstart[0] = 0.0;
+  auto load = [&](uint64_t t0, Aff (&f)[4]) {  // tile t0's maps (next tile prefetched)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t i = t0 + 4 * threadIdx.x + e;
+      f[e] = i < A.nblk ? Aff{A.w.ba[i], A.w.bb[i]} : Aff{1.0, 0.0};
+    }
+  };
+  Aff fn[4];
+  load(0, fn);
   for (uint64_t t0 = 0; t0 < A.nblk; t0 += kTile) {
     const int m = (int)min((uint64_t)kTile, A.nblk - t0);
     Aff f[4], c{1.0, 0.0};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int i = 4 * threadIdx.x + e;
-      f[e] = i < m ? Aff{A.w.ba[t0 + i], A.w.bb[t0 + i]} : Aff{1.0, 0.0};
+      f[e] = fn[e];
       c = aff_then(c, f[e]);
     }
+    load(t0 + kTile, fn);
     Aff inc = c;  // inclusive over lanes <= ln
     for (int o = 1; o < 32; o <<= 1) {
       const Aff up{__shfl_up_sync(0xffffffffu, inc.a, o), __shfl_up_sync(0xffffffffu, inc.b, o)};
@@ -292,8 +368,12 @@ __device__ void phase_scan_affine(const Args& A, Aff* wsh) {
 }
 
 // P4: classify each block; stable blocks get their exact integer total at binade k
-__device__ void phase_classify(const Args& A, int mode, double l1, double* sh, unsigned long long* ush) {
-  for (uint64_t b = blockIdx.x; b < A.nblk; b += gridDim.x) {
+__device__ void phase_classify(const Args& A, int mode, double l1) {
+  const int ln = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (kT / 32);
+  for (uint64_t b = (uint64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); b < A.nblk; b += nw) {
+    double l[kPer];
+    warp_load(A, b, l);  // issued with the block's scalars below
     const int pre = A.w.kb[b];
     const uint64_t j0 = b * kT, j1 = min(A.n, j0 + kT);
     const double s0 = A.w.sstart[b], s1 = A.w.sstart[b + 1];
@@ -302,22 +382,22 @@ __device__ void phase_classify(const Args& A, int mode, double l1, double* sh, u
     const double lo = s0 - (s0 * ((double)(16 * j0 + 64) * 0x1p-53) + (double)(j0 + 1) * 0x1p-1072);
     const double hi = s1 + (s1 * ((double)(16 * j1 + 64) * 0x1p-53) + (double)(j1 + 1) * 0x1p-1072);
     const int ka = binade(lo), kbn = binade(hi);
-    const bool cand = (pre != kUnstable) && ka == kbn && ka < 2000;
-    if (!__syncthreads_or(cand ? 1 : 0)) {  // uniform
-      if (threadIdx.x == 0) A.w.kb[b] = kUnstable;
-      __syncthreads();
+    if (!((pre != kUnstable) && ka == kbn && ka < 2000)) {  // warp-uniform
+      if (ln == 0) A.w.kb[b] = kUnstable;
       continue;
     }
-    const Op op = block_op(A, mode, b, l1, sh);
+    double v[kPer];
+    const unsigned resc = warp_ops(A, mode, b, l, l1, v);
     bool tie = false, sat = false;
-    const unsigned long long r = add_units(op.v, ka, tie, sat);
-    const int bad = __syncthreads_or((tie || sat || op.rescale) ? 1 : 0);
-    const unsigned long long tot = cta_sum_u64(r, ush);
-    if (threadIdx.x == 0) {
+    unsigned long long r = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) r += add_units(v[e], ka, tie, sat);
+    const bool bad = __any_sync(0xffffffffu, tie || sat || resc != 0u);
+    const unsigned long long tot = warp_sum_u64(r);
+    if (ln == 0) {
       A.w.kb[b] = bad ? kUnstable : ka;
       A.w.tot[b] = tot;
     }
-    __syncthreads();
   }
 }
 
@@ -467,6 +547,18 @@ __device__ double phase_walk(const Args& A, int mode, double l1, double* sh, Wal
     W.replays = 0;
     W.t_replay = 0;
   }
+  // tile t0's classes and stable totals; the next tile's are loaded while this one walks
+  auto load = [&](uint64_t t0, int (&k)[4], unsigned long long (&v)[4]) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t i = t0 + 4 * threadIdx.x + e;
+      k[e] = i < A.nblk ? A.w.kb[i] : kUnstable;
+      v[e] = i < A.nblk ? A.w.tot[i] : 0ull;
+    }
+  };
+  int kn[4];
+  unsigned long long vn[4];
+  load(0, kn, vn);
   for (uint64_t t0 = 0; t0 < A.nblk; t0 += kTile) {
     const int m = (int)min((uint64_t)kTile, A.nblk - t0);
     int k4[4], h4[4];
@@ -474,10 +566,11 @@ __device__ double phase_walk(const Args& A, int mode, double l1, double* sh, Wal
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int i = 4 * threadIdx.x + e;
-      k4[e] = i < m ? A.w.kb[t0 + i] : kUnstable;
-      v4[e] = (i < m && k4[e] != kUnstable) ? A.w.tot[t0 + i] : 0ull;
+      k4[e] = kn[e];
+      v4[e] = k4[e] != kUnstable ? vn[e] : 0ull;
       if (i < m) W.kb[i] = k4[e];
     }
+    load(t0 + kTile, kn, vn);
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -557,19 +650,36 @@ __device__ double phase_walk(const Args& A, int mode, double l1, double* sh, Wal
   return W.s;
 }
 
-// P6 (grid, CDF): cum of the stable blocks from their exact start units
-__device__ void phase_materialize(const Args& A, double l1, double* sh, unsigned long long* ush) {
-  for (uint64_t b = blockIdx.x; b < A.nblk; b += gridDim.x) {
+// P6 (grid, CDF): cum of the stable blocks from their exact start units (the lane's
+// inclusive integer prefix plus the warp's exclusive scan of the lane totals)
+__device__ void phase_materialize(const Args& A, double l1) {
+  const int ln = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (kT / 32);
+  for (uint64_t b = (uint64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); b < A.nblk; b += nw) {
+    double l[kPer];
+    warp_load(A, b, l);
     const int k = A.w.kb[b];
-    if (k == kUnstable) continue;  // uniform per CTA
+    if (k == kUnstable) continue;  // warp-uniform (the walk's replay wrote its cum)
     const unsigned long long u0 = A.w.bstart[b];
-    const Op op = block_op(A, kModeCdf, b, l1, sh);
+    double v[kPer];
+    warp_ops(A, kModeCdf, b, l, l1, v);
     bool tie = false, sat = false;
-    const unsigned long long r = add_units(op.v, k, tie, sat);
-    const unsigned long long inc = cta_incl_u64(r, ush);
-    const uint64_t j = b * kT + threadIdx.x;
-    if (j < A.n) A.cum[j] = units_value(u0 + inc, k);
-    __syncthreads();
+    unsigned long long r[kPer], t = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      t += add_units(v[e], k, tie, sat);
+      r[e] = t;
+    }
+    unsigned long long inc = t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long x = __shfl_up_sync(0xffffffffu, inc, o);
+      if (ln >= o) inc += x;
+    }
+    const unsigned long long base = u0 + (inc - t);
+    const uint64_t j0 = b * kT + kPer * ln;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e)
+      if (j0 + e < A.n) A.cum[j0 + e] = units_value(base + r[e], k);
   }
 }
 
@@ -579,21 +689,29 @@ __device__ void phase_materialize(const Args& A, double l1, double* sh, unsigned
 // M(c) = first m with pos_m > c.  pos_m = (m + u) / n is evaluated exactly as the
 // reference does, M(c) from the estimate c n - u corrected by exact comparisons, so a
 // thread reads two neighbouring CDF values (coalesced) and writes its slots: no search.
-__device__ __forceinline__ double slot_pos(uint64_t m, double u, double dn) {
-  return __ddiv_rn(__dadd_rn((double)m, u), dn);
+// pos_m = fl(fl(m + u) / n) > c, decided by a multiply by the rounded reciprocal rn = fl(1/n) unless the
+// two are within 2^-50 relative: |x rn - fl(x / n)| <= 3.2 2^-53 (x / n), so outside that
+// band the product orders like the quotient; inside it (in practice never) the division
+// decides, as the reference computes it
+__device__ __forceinline__ bool slot_above(uint64_t m, double u, double dn, double rn, double c) {
+  const double x = __dadd_rn((double)m, u);
+  const double q = __dmul_rn(x, rn);
+  if (q > __dmul_rn(c, 1.0 + 0x1p-50)) return true;
+  if (q < __dmul_rn(c, 1.0 - 0x1p-50)) return false;
+  return __ddiv_rn(x, dn) > c;
 }
-__device__ __forceinline__ uint64_t first_slot_above(double c, double u, uint64_t n, double dn) {
+__device__ __forceinline__ uint64_t first_slot_above(double c, double u, uint64_t n, double dn, double rn) {
   if (c != c) return n;  // a NaN CDF (NaN log-weights): no walk over all slots
   double est = floor(__fma_rn(c, dn, -u));
   if (!(est >= 0.0)) est = 0.0;  // also NaN
   uint64_t m = est > (double)n ? n : (uint64_t)est;
-  while (m > 0 && slot_pos(m - 1, u, dn) > c) --m;
-  while (m < n && !(slot_pos(m, u, dn) > c)) ++m;
+  while (m > 0 && slot_above(m - 1, u, dn, rn, c)) --m;
+  while (m < n && !slot_above(m, u, dn, rn, c)) ++m;
   return m;
 }
 constexpr uint64_t kSlotRun = 8192;  // longer runs of one ancestor go to the whole grid (P8)
 __device__ void phase_ancestors(const Args& A, double u) {
-  const double dn = (double)A.n;
+  const double dn = (double)A.n, rn = __drcp_rn(dn);
   const int ln = threadIdx.x & 31;
   // warp-uniform trip count: every lane of a warp iterates while any lane has particles
   const uint64_t stride = (uint64_t)gridDim.x * kT;
@@ -601,8 +719,8 @@ __device__ void phase_ancestors(const Args& A, double u) {
     const uint64_t j = j0 + ln;
     uint64_t lo = 0, hi = 0;
     if (j < A.n) {
-      lo = j == 0 ? 0 : first_slot_above(A.cum[j - 1], u, A.n, dn);
-      hi = j + 1 == A.n ? A.n : first_slot_above(A.cum[j], u, A.n, dn);
+      lo = j == 0 ? 0 : first_slot_above(A.cum[j - 1], u, A.n, dn, rn);
+      hi = j + 1 == A.n ? A.n : first_slot_above(A.cum[j], u, A.n, dn, rn);
       if (hi - lo > kSlotRun) {  // a heavy ancestor: the rest of its slots go to the grid
         const unsigned int e = atomicAdd(A.w.novf, 1u);
         A.w.ovf[3 * e] = lo + kSlotRun;
@@ -637,7 +755,7 @@ __device__ void phase_heavy_slots(const Args& A) {
   }
 }
 
-__global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
+__global__ void __launch_bounds__(kT, 4) refcdf_kernel(Args A) {
   if (A.gated && !*(volatile int*)&A.st->resample_now) return;
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[kT / 32 + 2];
@@ -654,19 +772,19 @@ __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
   if (lead && threadIdx.x == 0) *A.w.novf = 0u;
 
   // ---- l1 = logsumexp(log_w) ----
-  phase_block_max(A, sh);
+  phase_block_max(A);
   grid.sync();
   MARK(1);
   if (lead) phase_scan_max(A, sh + 8, sh);
   grid.sync();
   MARK(2);
-  phase_block_affine(A, kModeLse, 0.0, sh, u.wa, nullptr);
+  phase_block_affine(A, kModeLse, 0.0);
   grid.sync();
   MARK(3);
   if (lead) phase_scan_affine(A, u.wa);
   grid.sync();
   MARK(4);
-  phase_classify(A, kModeLse, 0.0, sh, ush);
+  phase_classify(A, kModeLse, 0.0);
   grid.sync();
   MARK(5);
   if (lead) {
@@ -689,13 +807,13 @@ __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
   if (l1 == kNegInfD || A.want_anc < 0) return;  // degenerate (engine.cpp:66) / l1 only
 
   // ---- cum_j, the reference's sequential CDF ----
-  phase_block_affine(A, kModeCdf, l1, sh, u.wa, nullptr);
+  phase_block_affine(A, kModeCdf, l1);
   grid.sync();
   MARK(7);
   if (lead) phase_scan_affine(A, u.wa);
   grid.sync();
   MARK(8);
-  phase_classify(A, kModeCdf, l1, sh, ush);
+  phase_classify(A, kModeCdf, l1);
   grid.sync();
   MARK(9);
   if (lead) {
@@ -705,7 +823,7 @@ __global__ void __launch_bounds__(kT) refcdf_kernel(Args A) {
   }
   grid.sync();
   MARK(10);
-  phase_materialize(A, l1, sh, ush);
+  phase_materialize(A, l1);
   if (A.want_anc != 1) return;
   grid.sync();
   MARK(11);
@@ -766,6 +884,10 @@ cudaError_t launch_refcdf(const double* lw, uint64_t n, SmcState* st, int gated,
   if (per == 0) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, refcdf_kernel, kT, 0);
     if (e != cudaSuccess) return e;
+    if (const char* v = std::getenv("ASMC_REFCDF_PER")) {  // tuning experiments only
+      const int w = std::atoi(v);
+      if (w >= 1 && w < per) per = w;
+    }
     if (per < 1) per = 1;
   }
   Args A;

@@ -154,3 +154,16 @@ def test_run_smc_fp64_matches_reference_at_scale():
     for k in ("log_g0", "log_g1", "log_g2", "ess_trace", "cum_log_z"):
         x, y = np.asarray(a[k][1:]), np.asarray(b[k][1:])
         assert np.max(np.abs(x - y) / np.maximum(1, np.abs(x))) < 1e-10, k
+
+
+def test_ancestors_on_exact_slot_ties():
+    """Equal log-weights at power-of-two N with u = 0 put CDF values on (or within an ulp of)
+    the slot positions (m + u) / N, where the ancestor pass's multiply-by-reciprocal filter
+    must defer to the reference's division: the same ancestors as the rule (restatement)."""
+    rs = oracle.load("restate")
+    g = np.random.default_rng(5)
+    cases = [np.zeros(1 << 16), np.zeros((1 << 14) * 3 + 1), np.full(1 << 18, -3.0),
+             np.repeat(g.normal(0, 1, 1 << 10), 64)]
+    for lw in cases:
+        for u in (0.0, 0.5, 0.25, 1.0 - 2.0 ** -53):
+            assert (capi.systematic_resample(lw, u) == rs.systematic_resample_u(lw, u)).all(), (len(lw), u)
