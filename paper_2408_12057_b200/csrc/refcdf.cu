@@ -28,7 +28,6 @@
 // One cooperative launch per resampling event (phases separated by grid.sync()); under
 // st->resample_now gating the launch returns at once on steps that do not resample.
 #include <cooperative_groups.h>
-#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "engine_kernels.h"
@@ -884,10 +883,6 @@ cudaError_t launch_refcdf(const double* lw, uint64_t n, SmcState* st, int gated,
   if (per == 0) {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, refcdf_kernel, kT, 0);
     if (e != cudaSuccess) return e;
-    if (const char* v = std::getenv("ASMC_REFCDF_PER")) {  // tuning experiments only
-      const int w = std::atoi(v);
-      if (w >= 1 && w < per) per = w;
-    }
     if (per < 1) per = 1;
   }
   Args A;
