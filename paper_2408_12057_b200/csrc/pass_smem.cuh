@@ -67,19 +67,29 @@ struct SmemOps {
   }
 
   // vq[q] = vterm(x) for the cached-potential targets (after a load or a redraw); returns
-  // this lane's sum of the vterms (== vsum for these targets, same order)
+  // this lane's sum of the vterms (== vsum for these targets, same order); targets with
+  // per-proposal checks also get the lane's sum of x^2 (their bound from sums, move())
   __device__ static float refresh_v(const TgtParams& T, int lane, int d, float4* xq) {
+    float x2;
+    return refresh_vx(T, lane, d, xq, x2);
+  }
+  __device__ static float refresh_vx(const TgtParams& T, int lane, int d, float4* xq, float& x2) {
     float s = 0.f;
+    x2 = 0.f;
     if constexpr (kCache) {
       const int nq = (d + 3) >> 2;
       const typename Tgt::F32 kf = Tgt::f32(T, 0.0);
       for (int q = lane; q < nq; q += G) {
-        const float4 v = vquad(kf, xq[q]);
+        const float4 x = xq[q];
+        const float4 v = vquad(kf, x);
         xq[nq + q] = v;
-        const float vv[4] = {v.x, v.y, v.z, v.w};
+        const float vv[4] = {v.x, v.y, v.z, v.w}, xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (4 * q + e < d) s += vv[e];
+          if (4 * q + e < d) {
+            s += vv[e];
+            if constexpr (Tgt::kPerProposalCheck) x2 = fmaf(xv[e], xv[e], x2);
+          }
       }
     }
     return s;
@@ -156,10 +166,13 @@ struct SmemOps {
   }
 
   // kernel.cpp:26-63 on this particle; vs (the lane's vpart sum) follows x
+  // x2: this lane's sum of x^2 when known (Tgt::kPerProposalCheck targets after a load),
+  // else NaN -- the early-rejection bound is then summed from the row (bound_total)
   __device__ static void move(const TgtParams& T, const KernelCfg& kc, int lane, int d,
                               double beta, float4*& xq, float4*& xalt, const PhiloxKeyC& k, uint32_t& drawn,
-                              float& vs) {
+                              float& vs, float& x2) {
     const int nq = (d + 3) >> 2;
+    const float x2_unknown = __int_as_float(0x7fffffff);
     if (kc.kind == ASMC_KERNEL_IDEALIZED) {
       const double mu = Tgt::exact_mu(T, beta);
       for (int q = lane; q < nq; q += G) {
@@ -174,10 +187,12 @@ struct SmemOps {
       refresh_v(T, lane, d, xq);
       __syncwarp();
       vs = vsum(T, lane, d, xq);
+      x2 = x2_unknown;
       return;
     }
     if constexpr (kMove == kMoveSlice) {
       if (kc.kind == ASMC_KERNEL_SLICE) slice(T, kc, lane, d, beta, xq, xalt, k, drawn, vs);
+      x2 = x2_unknown;
       return;
     } else {
     if (kc.kind != (kHmc ? ASMC_KERNEL_HMC : ASMC_KERNEL_RWMH)) return;
@@ -208,6 +223,7 @@ struct SmemOps {
       }
       __syncwarp();
       vs = vsum(T, lane, d, xq);
+      x2 = x2_unknown;
       return;
     }
     // d % 4 == 0: every proposal's draw set starts on a Philox block, so the
@@ -227,7 +243,12 @@ struct SmemOps {
       bool chk = Tgt::kEarly;  // does this proposal run early-rejection checks?
       if constexpr (Tgt::kPerProposalCheck) chk = !kc.no_early && Tgt::early_worth(kf, s, d, 4 * G);
       if (kBnd && chk && !bnd_ok) {
-        bnd = bound_total(kf, lane, d, nq, xq);
+        if constexpr (Tgt::kPerProposalCheck) {
+          // the bound from the lane's sums when they are known: no pass over the row
+          bnd = x2 == x2 ? Tgt::bound_of_sums(kf, lane_coords(lane, d, nq), vs, x2) : bound_total(kf, lane, d, nq, xq);
+        } else {
+          bnd = bound_total(kf, lane, d, nq, xq);
+        }
         bnd_ok = true;
       }
       const uint64_t base = (uint64_t)p * (uint64_t)d;
@@ -257,8 +278,9 @@ struct SmemOps {
           mfirst = max(0, (int)ceilf(need) - 2);
         }
       }
+      float x2_new = 0.f;
 #define ASMC_DELTA(A, C) \
-  delta_pass<A, C>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst, rejected, vs_new, drawn)
+  delta_pass<A, C>(kf, k, lane, d, nq, base, s, xq, xalt, log_u, bnd, vs, mfirst, rejected, vs_new, x2_new, drawn)
       float dl;
       if constexpr (Tgt::kPerProposalCheck) {
         if (chk) dl = aligned ? ASMC_DELTA(true, true) : ASMC_DELTA(false, true);
@@ -277,6 +299,7 @@ struct SmemOps {
           xq = xalt;
           xalt = t;
           vs = vs_new;
+          x2 = Tgt::kPerProposalCheck ? x2_new : x2_unknown;
           bnd_ok = false;
         } else {  // regenerate the proposal's normals
           const float nb = aligned ? accept_pass<true>(kf, k, lane, nq, base, s, xq)
@@ -285,6 +308,7 @@ struct SmemOps {
           bnd = nb;
           bnd_ok = kBnd;
           vs = vsum(T, lane, d, xq);
+          x2 = x2_unknown;
         }
       }
     }
@@ -358,6 +382,13 @@ struct SmemOps {
     }
     __syncwarp();
     vs = vsum(T, lane, d, xq);
+  }
+
+  // number of coordinates in this lane's quads (lane, lane + G, ...; the last quad may be partial)
+  __device__ static int lane_coords(int lane, int d, int nq) {
+    if (lane >= nq) return 0;
+    const int mine = (nq - 1 - lane) / G + 1;
+    return 4 * mine - (((nq - 1) % G == lane) ? 4 * nq - d : 0);
   }
 
   // sum of the early-rejection bound over this lane's coordinates (same order as delta_pass)
@@ -476,8 +507,8 @@ struct SmemOps {
   __device__ static float delta_pass(const typename Tgt::F32& kf, const PhiloxKeyC& k, int lane, int d, int nq,
                                      uint64_t base, float s, const float4* xq, float4* xalt, float log_u,
                                      float bnd, float vs, int mfirst, bool& rejected, float& vs_new,
-                                     uint32_t& drawn) {
-    float dl = 0.f, bp = 0.f, vn = 0.f;
+                                     float& x2_new, uint32_t& drawn) {
+    float dl = 0.f, bp = 0.f, vn = 0.f, x2n = 0.f;
     float sA = 0.f, sB = 0.f;  // Tgt::kQuadMH: sum z x, sum z^2 (dl = Tgt::dl_from(s, A, B))
     const float lu = log_u;
     const int mmax = (nq + G - 1) / G;
@@ -508,6 +539,7 @@ struct SmemOps {
           for (int e = 0; e < 4; ++e)
             if (kAligned || 4 * q + e < d) {
               dl += Tgt::dlg_vv(kf, xv[e], vv[e], xp[e], vp[e]);  // == dlg_cached
+              if constexpr (Tgt::kPerProposalCheck) x2n = fmaf(xp[e], xp[e], x2n);
               if (kCheck && (kLastCheck >= 6 || m <= kLastCheck)) bp += Tgt::dmax(kf, xv[e], vv[e]);
               vn += vp[e];
             }
@@ -542,6 +574,7 @@ struct SmemOps {
       }
     }
     vs_new = vn;
+    x2_new = x2n;
     if constexpr (Tgt::kQuadMH) dl = Tgt::dl_from(kf, s, sA, sB);
     return dl;
   }
@@ -747,6 +780,7 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
     const uint64_t pid = A.mode == kModeTraj ? (active ? A.pids[local] : 0) : A.p_begin + local;
     double lw = 0.0;
     float vs = 0.f;  // this lane's sum of vpart(x) (SmemOps::vsum)
+    float x2 = __int_as_float(0x7fffffff);  // this lane's sum of x^2 if known (SmemOps::move)
     if (loads && use_pre) {
 #pragma unroll
       for (int i = 0; i < kPQ; ++i) {
@@ -756,7 +790,7 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
       if (r + 1 < G) load_pre(blk * kBlock + (uint64_t)(r + 1) * NG + g);
       lw = active ? A.lw[local] : 0.0;
       __syncwarp();
-      vs = Ops::refresh_v(A.tg, lane, d, xq);  // the prefetch path is cached-target only
+      vs = Ops::refresh_vx(A.tg, lane, d, xq, x2);  // the prefetch path is cached-target only
     } else if (loads) {
       const float4* src = reinterpret_cast<const float4*>(
           reinterpret_cast<const float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d);
@@ -776,7 +810,8 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
       }
       lw = active ? A.lw[local] : 0.0;
       __syncwarp();
-      vs = Tgt::kCacheV ? Ops::refresh_v(A.tg, lane, d, xq) : Ops::vsum(A.tg, lane, d, xq);
+      if constexpr (Tgt::kCacheV) vs = Ops::refresh_vx(A.tg, lane, d, xq, x2);
+      else vs = Ops::vsum(A.tg, lane, d, xq);
     } else {
       PhiloxKeyC k;
       k.init(A.rk[0], pid, 0);
@@ -809,7 +844,7 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
       PhiloxKeyC k;
       k.init(A.rk[1], pid, (uint64_t)t);
       __syncwarp();
-      Ops::move(A.tg, A.kc, lane, d, b1, xq, xalt, k, drawn, vs);
+      Ops::move(A.tg, A.kc, lane, d, b1, xq, xalt, k, drawn, vs, x2);
       __syncwarp();
       const double pre = lw;
       lw += lg;

@@ -145,6 +145,10 @@ struct TgtMixture {
   static constexpr bool kEarly = true;
   static constexpr unsigned kCheckMask = 0x01u;
   static constexpr bool kPerProposalCheck = true;
+  // sum of dmax over n coordinates from their sums: beta (n lmix - sum v) + sum x^2 / 2r^2
+  __device__ static float bound_of_sums(const F32& k, int n, float vsum, float x2sum) {
+    return fmaf(k.beta, fmaf((float)n, k.lmix, -vsum), k.hr * x2sum);
+  }
   __device__ static bool early_worth(const F32& k, float s, int d, int c0) {
     const float is = fminf(k.inv_s1, k.inv_s2);
     const float drop = s * s * fmaf(k.beta, 0.5f * is * is - k.hr, k.hr);
