@@ -106,7 +106,7 @@ def run_sais(target, kernel, n1, rounds, seed, exec_, rank, world, partials_fn=N
                 capi.sais_partials_dev(target, kernel, betas, n, p0, p1, local.data_ptr(), seed=seed, round=k,
                                        exec_=ex)
             with torch.cuda.stream(stream):
-                if world > 1 and dist.get_backend() == "nccl":  # device to device
+                if dist.is_initialized() and dist.get_backend() == "nccl":  # device to device (any world)
                     outs = [torch.empty_like(local) for _ in counts]
                     dist.all_gather(outs, local)
                 elif world > 1:  # gloo (the 2-ranks-on-one-GPU check): staged through the host
