@@ -597,17 +597,25 @@ int enqueue_smc_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs& 
   A.mode = kModeSmcInit;  // engine_detail.hpp:91-100
   LCH(launch_pass(ex, L, A, nblk, C->stream));
   const bool exact = ex.precision == ASMC_PREC_FP64;
+  // engine.cpp:161-173's gather x_new[m] = x[a_m], lw <- 0 is deferred into the next step
+  // pass: it reads row a_m and starts from log w = 0 (PassArgs::anc / pend), so a
+  // resampling event moves no rows of its own (2 n d B of HBM traffic saved per event)
+  A.anc = W.anc.p;
+  A.pend = &d_st->gather_pending;
   for (int t = 1; t <= T; ++t) {
     A.mode = kModeSmcStep;
     A.t_begin = A.t_end = t;
     A.row_base = t;
     LCH(launch_pass(ex, L, A, nblk, C->stream));
+    if (t > 1) LCH(launch_settle(W.xcur.p, d_st, C->stream));
     LCH(launch_fold(exact, W.part.p, nblk, nblk, 0, 1, kNAcc, W.chunk.p, W.tot.p, C->stream));
     LCH(launch_smc_decide(W.tot.p, t, T, n, policy, rho, seed, round, ex.rng, d_rd, C->stream));
     LCH(launch_resample_ref(C, W.lw.p, n, d_st, W.btot.p, W.cum.p, W.anc.p));
-    LCH(launch_gather(W.anc.p, n, d * real, W.xbuf.p, W.xcur.p, W.lw.p, d_st, C->sms, C->stream));
+    LCH(launch_defer_gather(d_st, C->stream));
     g_launches += 1;
   }
+  // the final step's event (if any): the rows are the round's final particles
+  LCH(launch_gather_pending(W.anc.p, n, d * real, W.xbuf.p, W.xcur.p, W.lw.p, d_st, C->sms, C->stream));
   return 0;
 }
 

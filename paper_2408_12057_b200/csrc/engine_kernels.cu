@@ -293,9 +293,11 @@ __global__ void smc_decide_kernel(const LogAcc* tot, int t, int T_in, uint64_t n
 // ------------------------------------------------------- resampling --
 // Ancestors: refcdf.cu (the reference's sequential CDF, bit for bit).
 // x_new[m] = x[a_m] (row copy, 16-byte vectors when the row allows), lw <- 0
+// `flag`: st->resample_now (immediate gather) or st->gather_pending (end-of-round
+// materialisation of a deferred one)
 __global__ void gather_kernel(const uint32_t* anc, uint64_t n, uint64_t row_bytes,
-                              void* const* xbuf, int* xcur, double* lw, const SmcState* st) {
-  if (!st->resample_now) return;
+                              void* const* xbuf, int* xcur, double* lw, const int* flag) {
+  if (!*flag) return;
   const int cur = *xcur;
   const char* src = (const char*)xbuf[cur];
   char* dst = (char*)xbuf[cur ^ 1];
@@ -324,6 +326,16 @@ __global__ void gather_kernel(const uint32_t* anc, uint64_t n, uint64_t row_byte
 __global__ void flip_kernel(int* xcur, SmcState* st) {
   if (st->resample_now) *xcur ^= 1;
   st->resample_now = 0;
+}
+
+__global__ void defer_gather_kernel(SmcState* st) {
+  if (st->resample_now) st->gather_pending = 1;
+  st->resample_now = 0;
+}
+
+__global__ void settle_kernel(int* xcur, SmcState* st) {
+  if (st->gather_pending) *xcur ^= 1;
+  st->gather_pending = 0;
 }
 
 // ------------------------------------------------------------ schedule --
@@ -615,11 +627,29 @@ cudaError_t launch_smc_decide(const LogAcc* tot_row, int t, int T, uint64_t n, i
 
 cudaError_t launch_gather(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,
                           int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s) {
-  gather_kernel<<<sms * 8, 256, 0, s>>>(anc, n, row_bytes, xbuf, xcur, lw, st);
+  gather_kernel<<<sms * 8, 256, 0, s>>>(anc, n, row_bytes, xbuf, xcur, lw, &st->resample_now);
   cudaError_t e = LAUNCH_OK();
   if (e != cudaSuccess) return e;
   flip_kernel<<<1, 1, 0, s>>>(xcur, st);
   return LAUNCH_OK();
+}
+
+cudaError_t launch_defer_gather(SmcState* st, cudaStream_t s) {
+  defer_gather_kernel<<<1, 1, 0, s>>>(st);
+  return LAUNCH_OK();
+}
+
+cudaError_t launch_settle(int* xcur, SmcState* st, cudaStream_t s) {
+  settle_kernel<<<1, 1, 0, s>>>(xcur, st);
+  return LAUNCH_OK();
+}
+
+cudaError_t launch_gather_pending(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,
+                                  int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s) {
+  gather_kernel<<<sms * 8, 256, 0, s>>>(anc, n, row_bytes, xbuf, xcur, lw, &st->gather_pending);
+  cudaError_t e = LAUNCH_OK();
+  if (e != cudaSuccess) return e;
+  return launch_settle(xcur, st, s);
 }
 
 

@@ -18,10 +18,12 @@ struct SmcState {
   double total;   // CDF total cum[n-1]
   double err_val;
   int resample_now;
+  int gather_pending;  // SSMC: the last event's gather is deferred into the next step pass
   int n_resample;
   int err;
   int err_step;
 };
+static_assert(sizeof(SmcState) == 88, "distributed.py SIZEOF_SMCSTATE mirrors this (e2e byte counts)");
 
 // Per-round outputs in device memory (arrays of T+1 unless noted).
 struct RoundDev {
@@ -77,6 +79,13 @@ cudaError_t launch_smc_decide(const LogAcc* tot_row, int t, int T, uint64_t n, i
                               cudaStream_t s, const double* zja_betas = nullptr);
 cudaError_t launch_gather(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,
                           int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s);
+// deferred gather (the pass kernels' SSMC step): mark the event's rows pending instead of
+// copying them; settle flips the buffers after the pass that consumed them; the pending
+// variant of the gather materialises rows still pending at the end of a round
+cudaError_t launch_defer_gather(SmcState* st, cudaStream_t s);
+cudaError_t launch_settle(int* xcur, SmcState* st, cudaStream_t s);
+cudaError_t launch_gather_pending(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,
+                                  int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s);
 cudaError_t launch_generate_schedule(const double* lambda, const double* beta, int knots, int t_new,
                                      double* out, double* scratch, int* err, cudaStream_t s);
 // batched seeds (SAIS round loop over many seeds in one launch per kernel)

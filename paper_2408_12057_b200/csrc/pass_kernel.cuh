@@ -82,7 +82,16 @@ struct PassArgs {
   uint64_t blocks_per_seed, betas_stride, part_seed_stride;
   unsigned long long* drawn;  // profiling: normals actually generated (null = off)
   PhiloxRoundKeys rk[2];      // Philox round keys of (seed, round, substep 0 | 1): set at launch
+  // SSMC step after a resampling event whose gather was deferred (*pend != 0): slot m
+  // reads row anc[m] of the live buffer with log w = 0 and writes its row to the other
+  // buffer (flipped after the pass) -- the gather's row copy fused into the step's loads
+  const uint32_t* anc;
+  const int* pend;
 };
+
+__device__ __forceinline__ bool pass_pending(const PassArgs& A) {
+  return A.mode == kModeSmcStep && A.pend && *(volatile const int*)A.pend;
+}
 
 // coordinate owned by (lane, slot k): quads of 4 consecutive coordinates dealt
 // round-robin over the G lanes (G = 1 gives k itself).
@@ -604,6 +613,7 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
   using FastT = Fast<Tgt, RNG, G, KMAX>;
   using ExactT = Exact<Tgt, SeqT, KMAX>;
 
+  const bool pend = pass_pending(A);
   for (int r = 0; r < G; ++r) {
     const uint64_t local = blk * kBlock + (uint64_t)r * NG + g;
     const bool active = local < A.n_local;
@@ -613,13 +623,14 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
 
     // ---- init / load -----------------------------------------------------
     if (mode_loads(A.mode)) {
-      const Real* xs = reinterpret_cast<const Real*>(A.xbuf[*A.xcur]) + local * (uint64_t)d;
+      const uint64_t row = (pend && active) ? (uint64_t)A.anc[local] : local;
+      const Real* xs = reinterpret_cast<const Real*>(A.xbuf[*A.xcur]) + row * (uint64_t)d;
 #pragma unroll(KMAX <= 64 ? KMAX : 1)
       for (int k = 0; k < KMAX; ++k) {
         const int i = coord_of<G>(lane, k);
         x[k] = (active && i < d) ? xs[i] : (Real)0;
       }
-      lw = active ? A.lw[local] : 0.0;
+      lw = (active && !pend) ? A.lw[local] : 0.0;
     } else {
       if constexpr (kExact) {
         SeqT st;
@@ -702,7 +713,7 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ Pa
     }
 
     if (mode_stores(A.mode) && active) {
-      Real* xs = reinterpret_cast<Real*>(A.xbuf[*A.xcur]) + local * (uint64_t)d;
+      Real* xs = reinterpret_cast<Real*>(A.xbuf[*A.xcur ^ (pend ? 1 : 0)]) + local * (uint64_t)d;
 #pragma unroll(KMAX <= 64 ? KMAX : 1)
       for (int k = 0; k < KMAX; ++k) {
         const int i = coord_of<G>(lane, k);

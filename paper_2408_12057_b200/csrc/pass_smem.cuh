@@ -750,10 +750,12 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
   constexpr int kPQ = kPre ? 8 : 1;  // quads per lane held (d <= 128)
   float4 pre[kPQ];
   const bool use_pre = kPre && loads && (d & 3) == 0 && nq <= G * kPQ;
+  const bool pend = pass_pending(A);  // deferred gather: rows through anc, out to the other buffer
   auto load_pre = [&](uint64_t loc) {
     const bool act = loc < A.n_local;
+    const uint64_t row = act ? (pend ? (uint64_t)A.anc[loc] : loc) : 0;
     const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A.xbuf[*A.xcur]) +
-                                                        (act ? loc : 0) * (uint64_t)d);
+                                                        row * (uint64_t)d);
 #pragma unroll
     for (int i = 0; i < kPQ; ++i) {
       const int q = lane + G * i;
@@ -764,7 +766,7 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
   for (int r = 0; r < G; ++r) {
     const uint64_t local = blk * kBlock + (uint64_t)r * NG + g;
     const bool active = local < A.n_local;
-    if (loads && tid == 0 && r + 1 < G) {
+    if (loads && !pend && tid == 0 && r + 1 < G) {
       // the next round's NG particle rows are one contiguous span of the state buffer:
       // one bulk L2 prefetch now, so their loads a particle-iteration later hit L2
       const uint64_t nl = blk * kBlock + (uint64_t)(r + 1) * NG;
@@ -788,12 +790,13 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
         if (q < nq) xq[q] = pre[i];
       }
       if (r + 1 < G) load_pre(blk * kBlock + (uint64_t)(r + 1) * NG + g);
-      lw = active ? A.lw[local] : 0.0;
+      lw = (active && !pend) ? A.lw[local] : 0.0;
       __syncwarp();
       vs = Ops::refresh_vx(A.tg, lane, d, xq, x2);  // the prefetch path is cached-target only
     } else if (loads) {
+      const uint64_t row = (pend && active) ? (uint64_t)A.anc[local] : local;
       const float4* src = reinterpret_cast<const float4*>(
-          reinterpret_cast<const float*>(A.xbuf[*A.xcur]) + local * (uint64_t)d);
+          reinterpret_cast<const float*>(A.xbuf[*A.xcur]) + row * (uint64_t)d);
       const bool vec = (d & 3) == 0;
       for (int q = lane; q < nq; q += G) {
         if (!active) {
@@ -808,7 +811,7 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
           xq[q] = make_float4(v[0], v[1], v[2], v[3]);
         }
       }
-      lw = active ? A.lw[local] : 0.0;
+      lw = (active && !pend) ? A.lw[local] : 0.0;
       __syncwarp();
       if constexpr (Tgt::kCacheV) vs = Ops::refresh_vx(A.tg, lane, d, xq, x2);
       else vs = Ops::vsum(A.tg, lane, d, xq);
@@ -860,7 +863,7 @@ __global__ void __launch_bounds__(kBlock, kMove == kMoveHmc ? 4 : ((G == 4 && Tg
       else warp_fold<G>(pre, lg, lw, active, nacc, myacc + (size_t)(t - A.t_begin) * nacc);
     }
     if (mode_stores(A.mode) && active) {
-      float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(A.xbuf[*A.xcur]) +
+      float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(A.xbuf[*A.xcur ^ (pend ? 1 : 0)]) +
                                               local * (uint64_t)d);
       if ((d & 3) == 0) {
         for (int q = lane; q < nq; q += G) dst[q] = xq[q];

@@ -24,7 +24,7 @@ import numpy as np
 from . import abi
 
 SIZEOF_ROUNDDEV = 80
-SIZEOF_SMCSTATE = 80
+SIZEOF_SMCSTATE = 88
 
 
 def chunk_partition(n, world, chunk=abi.FOLD_CHUNK):
