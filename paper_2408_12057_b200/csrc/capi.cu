@@ -614,8 +614,8 @@ int enqueue_smc_round(DevCtx* C, const asmc_exec& ex, Layout L, const PassArgs& 
     LCH(launch_defer_gather(d_st, C->stream));
     g_launches += 1;
   }
-  // the final step's event (if any): the rows are the round's final particles
-  LCH(launch_gather_pending(W.anc.p, n, d * real, W.xbuf.p, W.xcur.p, W.lw.p, d_st, C->sms, C->stream));
+  // a final-step event leaves its gather pending: no caller reads a round's final
+  // particles (the reports come from the accumulators), so the copy is never made
   return 0;
 }
 

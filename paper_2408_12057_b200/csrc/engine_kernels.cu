@@ -293,8 +293,7 @@ __global__ void smc_decide_kernel(const LogAcc* tot, int t, int T_in, uint64_t n
 // ------------------------------------------------------- resampling --
 // Ancestors: refcdf.cu (the reference's sequential CDF, bit for bit).
 // x_new[m] = x[a_m] (row copy, 16-byte vectors when the row allows), lw <- 0
-// `flag`: st->resample_now (immediate gather) or st->gather_pending (end-of-round
-// materialisation of a deferred one)
+// gated on `flag` (st->resample_now)
 __global__ void gather_kernel(const uint32_t* anc, uint64_t n, uint64_t row_bytes,
                               void* const* xbuf, int* xcur, double* lw, const int* flag) {
   if (!*flag) return;
@@ -642,14 +641,6 @@ cudaError_t launch_defer_gather(SmcState* st, cudaStream_t s) {
 cudaError_t launch_settle(int* xcur, SmcState* st, cudaStream_t s) {
   settle_kernel<<<1, 1, 0, s>>>(xcur, st);
   return LAUNCH_OK();
-}
-
-cudaError_t launch_gather_pending(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,
-                                  int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s) {
-  gather_kernel<<<sms * 8, 256, 0, s>>>(anc, n, row_bytes, xbuf, xcur, lw, &st->gather_pending);
-  cudaError_t e = LAUNCH_OK();
-  if (e != cudaSuccess) return e;
-  return launch_settle(xcur, st, s);
 }
 
 

@@ -80,12 +80,9 @@ cudaError_t launch_smc_decide(const LogAcc* tot_row, int t, int T, uint64_t n, i
 cudaError_t launch_gather(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,
                           int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s);
 // deferred gather (the pass kernels' SSMC step): mark the event's rows pending instead of
-// copying them; settle flips the buffers after the pass that consumed them; the pending
-// variant of the gather materialises rows still pending at the end of a round
+// copying them; settle flips the buffers after the pass that consumed them
 cudaError_t launch_defer_gather(SmcState* st, cudaStream_t s);
 cudaError_t launch_settle(int* xcur, SmcState* st, cudaStream_t s);
-cudaError_t launch_gather_pending(const uint32_t* anc, uint64_t n, uint64_t row_bytes, void* const* xbuf,
-                                  int* xcur, double* lw, SmcState* st, int sms, cudaStream_t s);
 cudaError_t launch_generate_schedule(const double* lambda, const double* beta, int knots, int t_new,
                                      double* out, double* scratch, int* err, cudaStream_t s);
 // batched seeds (SAIS round loop over many seeds in one launch per kernel)
