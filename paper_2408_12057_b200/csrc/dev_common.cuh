@@ -64,6 +64,20 @@ __device__ __forceinline__ void lacc_combine(LogAcc& a, const LogAcc& o) {
   }
 }
 
+// log|x| for the fp32 passes' ELBO accumulator (x = lg != 0, computed from fp32 potentials):
+// the binary exponent exactly, the log2 of the [1, 2) significand on the SFU (absolute error
+// < 2^-21), ~10 instructions instead of a full fp64 log -- the fp32 lg already carries ~1e-7
+// relative error.  Subnormal x take the fp64 log.
+__device__ __forceinline__ double log_abs_sfu(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x) & ~(1ull << 63);
+  const int e = (int)(b >> 52) - 1023;
+  if (e == -1023) return log(__longlong_as_double((long long)b));
+  const float m = (float)__longlong_as_double((long long)((b & ((1ull << 52) - 1)) | (1023ull << 52)));
+  float l2;
+  asm("lg2.approx.f32 %0, %1;" : "=f"(l2) : "f"(m));
+  return ((double)e + (double)l2) * 0.69314718055994530942;
+}
+
 // top-2 maxima as (max=m1, sum=m2); exact and order-free (engine_detail.hpp:130-154)
 __device__ __forceinline__ void top2_add(LogAcc& a, double v) {
   if (v > a.max) {

@@ -629,7 +629,7 @@ __device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_po
         double sign = 1.0;
         if (ln == kAccSq) l = 2.0 * lw_post;
         if (ln == kAccElbo) {
-          l = lg != 0.0 ? lw_pre + log(fabs(lg)) : -__builtin_huge_val();
+          l = lg != 0.0 ? lw_pre + log_abs_sfu(lg) : -__builtin_huge_val();
           sign = lg > 0.0 ? 1.0 : -1.0;
         }
         sacc_add(v, l, sign);
@@ -652,7 +652,7 @@ __device__ __forceinline__ void warp_fold(double lw_pre, double lg, double lw_po
       val = a == kAccG0 ? lw_pre : (a == kAccG1 ? lw_pre + lg : lw_pre + 2.0 * lg);
       if (a == kAccSq) val = 2.0 * lw_post;
       if (a == kAccElbo) {
-        val = lg != 0.0 ? lw_pre + log(fabs(lg)) : -__builtin_huge_val();
+        val = lg != 0.0 ? lw_pre + log_abs_sfu(lg) : -__builtin_huge_val();
         sign = lg > 0.0 ? 1.0 : -1.0;
       }
     }
@@ -686,7 +686,7 @@ __device__ __forceinline__ void warp_regfold_add(double lw_pre, double lg, doubl
   const int l = (threadIdx.x & 31) % G;
   if (!active) return;
   if (l == kAccElbo) {
-    if (lg != 0.0) sacc_add(f.acc, lw_pre + log(fabs(lg)), lg > 0.0 ? 1.0 : -1.0);
+    if (lg != 0.0) sacc_add(f.acc, lw_pre + log_abs_sfu(lg), lg > 0.0 ? 1.0 : -1.0);
   } else {
     lacc_add(f.acc, l == kAccG0 ? lw_pre : (l == kAccG1 ? lw_pre + lg : lw_pre + 2.0 * lg));
   }
