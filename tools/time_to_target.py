@@ -146,9 +146,11 @@ def measure_config(c, n_seeds, cpu_reps=3):
     from paper_2408_12057_b200 import capi
     plan_n, plan_t = capi.plan_steps(k + 1, cfg["n1"], tg.dim, 4096 << 20, cfg["mode"])
     ps_full = sum(a * b for a, b in zip(plan_n, plan_t))
-    n1p = max(64, cfg["n1"] // 64)
-    pn, pt = capi.plan_steps(1, n1p, tg.dim, 4096 << 20, cfg["mode"])
-    t_probe = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], n1p, 1, seed=int(seeds[0]),
+    # probe: a few rounds (round 1 alone is overhead-dominated and understates the rate,
+    # which would shrink the sample and inflate the extrapolated CPU time)
+    n1p, rp = max(64, cfg["n1"] // 64), min(k + 1, 3)
+    pn, pt = capi.plan_steps(rp, n1p, tg.dim, 4096 << 20, cfg["mode"])
+    t_probe = wall(lambda i: ref.run_rounds(tg, cfg["kernel"], cfg["mode"], n1p, rp, seed=int(seeds[0]),
                                             workers=workers), 1)
     rate = sum(a * b for a, b in zip(pn, pt)) / max(t_probe, 1e-6)
     n1c, rc, reps = cfg["n1"], k + 1, cpu_reps
@@ -158,7 +160,7 @@ def measure_config(c, n_seeds, cpu_reps=3):
         return sum(x * y for x, y in zip(a, b))
 
     if ps_full / rate > 20.0:  # scale N1 down, then drop the last rounds if still too long
-        n1c, reps = max(64, int(cfg["n1"] * 20.0 * rate / ps_full)), 1
+        n1c, reps = max(256, int(cfg["n1"] * 20.0 * rate / ps_full)), 1
         while rc > 1 and ps_of(n1c, rc) / rate > 30.0:
             rc -= 1
     ps_cpu = ps_of(n1c, rc)
