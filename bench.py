@@ -142,7 +142,7 @@ def cpu_sample(budget_s, dim, rounds, workers, window=None, tries=4):
     from a 4096-particle run and rescale from each real sample (p-steps are linear in N_1)
     until the sample lands inside `window`.  Returns (n1, kernel_applications, seconds,
     inside_window)."""
-    if window is None:  # 10-30 s of CPU work at the default budget
+    if window is None:  # 10-30 s of CPU work (wider only for a budget outside it)
         window = (min(10.0, 0.8 * budget_s), max(30.0, 1.5 * budget_s))
     n1 = 4096
     ka, dt = cpu_reference_run(n1, dim, rounds, workers)
@@ -414,7 +414,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n1", type=int, default=N1_PER_GPU, help="round-1 particles per GPU")
     ap.add_argument("--dim", type=int, default=D)
-    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds per CPU sample (10-30 s of CPU work)")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds per CPU sample (10-30 s of CPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-target measurement")
     ap.add_argument("--ttt-seeds", type=int, default=1000)
