@@ -52,6 +52,9 @@ struct RefCdfWork {
   unsigned int* novf;
   double* gmax;    // max log-weight
   double* l1;      // logsumexp of the log-weights (the reference's bits)
+  double* opv;     // per particle: the element operation's exp value of the current chain
+                   // (written once by the block-affine phase, read by classification,
+                   // replays and materialisation); sign bit set = LogAccumulator rescale
   unsigned long long* prof;  // optional: %globaltimer at each phase end (16 entries)
 };
 size_t refcdf_work_bytes(uint64_t n);

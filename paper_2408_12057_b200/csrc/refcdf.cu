@@ -156,26 +156,16 @@ __device__ __forceinline__ unsigned long long cta_incl_u64(unsigned long long v,
   return pre + inc;
 }
 
-// The element operation of particle j = b*kT + threadIdx.x in block b (all threads of
-// the CTA call it together).  LSE (LogAccumulator::add, logsum.hpp:20-28):
+// The element operation of particle j.  LSE (LogAccumulator::add, logsum.hpp:20-28):
 //   log_w == -inf          -> no-op (ADD 0)
 //   log_w <= running max   -> s += exp(log_w - max)          (ADD)
 //   log_w >  running max   -> s = s * exp(max - log_w) + 1    (RESCALE)
-// CDF (engine.cpp:68-75): s += exp(log_w - l1).
+// CDF (engine.cpp:68-75): s += exp(log_w - l1).  warp_ops evaluates them (P2) and caches
+// the values (RefCdfWork::opv); classification, replays and materialisation read the cache.
 struct Op {
   double v;
   bool rescale;
 };
-__device__ __forceinline__ Op block_op(const Args& A, int mode, uint64_t b, double l1, double* sh) {
-  const uint64_t j = b * kT + threadIdx.x;
-  const bool in = j < A.n;
-  const double l = in ? A.lw[j] : kNegInfD;
-  if (mode == kModeCdf) return Op{in ? gexp(__dsub_rn(l, l1)) : 0.0, false};
-  const double pm = cta_excl_max(l, A.w.bmax[b], sh);
-  if (l == kNegInfD) return Op{0.0, false};
-  if (l <= pm) return Op{gexp(__dsub_rn(l, pm)), false};
-  return Op{gexp(__dsub_rn(pm, l)), true};
-}
 
 // ---- the grid phases work on one WARP per 256-particle block ------------------
 // Lane l holds particles b kT + 8 l .. 8 l + 7, consecutive, so lane-local order is
@@ -223,6 +213,26 @@ __device__ __forceinline__ unsigned warp_ops(const Args& A, int mode, uint64_t b
       resc |= 1u << e;
     }
     pm = fmax(pm, l[e]);
+  }
+  return resc;
+}
+
+// the op cache: v with the rescale flag in its sign bit (v >= 0; a rescale by exp(-inf) = 0
+// is stored as -0.0)
+__device__ __forceinline__ void warp_store_ops(const Args& A, uint64_t b, const double (&v)[kPer], unsigned resc) {
+  const uint64_t j0 = b * kT + kPer * (threadIdx.x & 31);
+#pragma unroll
+  for (int e = 0; e < kPer; ++e)
+    if (j0 + e < A.n) A.w.opv[j0 + e] = ((resc >> e) & 1u) ? -v[e] : v[e];
+}
+__device__ __forceinline__ unsigned warp_cached_ops(const Args& A, uint64_t b, double (&v)[kPer]) {
+  const uint64_t j0 = b * kT + kPer * (threadIdx.x & 31);
+  unsigned resc = 0u;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const double c = j0 + e < A.n ? A.w.opv[j0 + e] : 0.0;
+    if (signbit(c)) resc |= 1u << e;
+    v[e] = fabs(c);
   }
   return resc;
 }
@@ -300,6 +310,7 @@ __device__ void phase_block_affine(const Args& A, int mode, double l1) {
     double l[kPer], v[kPer];
     warp_load(A, b, l);
     const unsigned resc = warp_ops(A, mode, b, l, l1, v);
+    warp_store_ops(A, b, v, resc);
     Aff f = (resc & 1u) ? Aff{v[0], 1.0} : Aff{1.0, v[0]};
 #pragma unroll
     for (int e = 1; e < kPer; ++e) f = aff_then(f, ((resc >> e) & 1u) ? Aff{v[e], 1.0} : Aff{1.0, v[e]});
@@ -371,8 +382,6 @@ __device__ void phase_classify(const Args& A, int mode, double l1) {
   const int ln = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * (kT / 32);
   for (uint64_t b = (uint64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); b < A.nblk; b += nw) {
-    double l[kPer];
-    warp_load(A, b, l);  // issued with the block's scalars below
     const int pre = A.w.kb[b];
     const uint64_t j0 = b * kT, j1 = min(A.n, j0 + kT);
     const double s0 = A.w.sstart[b], s1 = A.w.sstart[b + 1];
@@ -386,7 +395,7 @@ __device__ void phase_classify(const Args& A, int mode, double l1) {
       continue;
     }
     double v[kPer];
-    const unsigned resc = warp_ops(A, mode, b, l, l1, v);
+    const unsigned resc = warp_cached_ops(A, b, v);  // P2's ops of this chain
     bool tie = false, sat = false;
     unsigned long long r = 0;
 #pragma unroll
@@ -457,8 +466,10 @@ struct WalkSmem {
 // scan per segment, all elements at once), and each event is applied directly in fp64.
 // A block with many events (e.g. log-weights increasing with the index) is replayed by
 // one thread, element by element.
-__device__ void replay_block(const Args& A, int mode, uint64_t b, double l1, double* sh, WalkSmem& W) {
-  const Op op = block_op(A, mode, b, l1, sh);
+__device__ void replay_block(const Args& A, int mode, uint64_t b, WalkSmem& W) {
+  const uint64_t jj = b * kT + threadIdx.x;
+  const double cached = jj < A.n ? A.w.opv[jj] : 0.0;  // P2's op of this chain
+  const Op op{fabs(cached), (bool)signbit(cached)};
   const int i = threadIdx.x;
   const int m = (int)min((uint64_t)kT, A.n - b * kT);
   const double v = i < m ? op.v : 0.0;
@@ -626,7 +637,7 @@ __device__ double phase_walk(const Args& A, int mode, double l1, double* sh, Wal
       unsigned long long tr0 = 0;
       if (A.w.prof && threadIdx.x == 0) tr0 = gtimer();
       for (int i = W.heads[h]; i < W.stop_end; ++i) {
-        replay_block(A, mode, t0 + i, l1, sh, W);
+        replay_block(A, mode, t0 + i, W);
         if (threadIdx.x == 0) {
           ++W.replays;
           W.kb[i] = kUnstable;
@@ -655,13 +666,11 @@ __device__ void phase_materialize(const Args& A, double l1) {
   const int ln = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * (kT / 32);
   for (uint64_t b = (uint64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5); b < A.nblk; b += nw) {
-    double l[kPer];
-    warp_load(A, b, l);
     const int k = A.w.kb[b];
     if (k == kUnstable) continue;  // warp-uniform (the walk's replay wrote its cum)
     const unsigned long long u0 = A.w.bstart[b];
     double v[kPer];
-    warp_ops(A, kModeCdf, b, l, l1, v);
+    warp_cached_ops(A, b, v);
     bool tie = false, sat = false;
     unsigned long long r[kPer], t = 0;
 #pragma unroll
@@ -852,7 +861,7 @@ cudaError_t launch_exact_math(int which, const double* x, uint64_t n, double* ou
 size_t refcdf_work_bytes(uint64_t n) {
   const uint64_t nb = (n + kT - 1) / kT;
   // 6 double/u64 arrays + 1 int array of nb + 2 entries, 3 scalars, 16-byte alignment each
-  return (size_t)(nb + 2) * (6 * 8 + 4) + 24 * (nb / 4 + 2) + 18 * 16 + 256;
+  return (size_t)(nb + 2) * (6 * 8 + 4) + 24 * (nb / 4 + 2) + 18 * 16 + 256 + 8 * (size_t)n + 16;
 }
 
 void refcdf_work_carve(void* base, uint64_t n, RefCdfWork* w) {
@@ -874,6 +883,7 @@ void refcdf_work_carve(void* base, uint64_t n, RefCdfWork* w) {
   w->novf = (unsigned int*)take(16);
   w->gmax = (double*)take(16);
   w->l1 = (double*)take(16);
+  w->opv = (double*)take(8 * n);
   w->prof = nullptr;
 }
 
