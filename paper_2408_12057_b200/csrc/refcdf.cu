@@ -219,20 +219,42 @@ __device__ __forceinline__ unsigned warp_ops(const Args& A, int mode, uint64_t b
 
 // the op cache: v with the rescale flag in its sign bit (v >= 0; a rescale by exp(-inf) = 0
 // is stored as -0.0)
+// (16-byte vector accesses: the cache is 16-byte aligned and a lane's 8 values contiguous)
 __device__ __forceinline__ void warp_store_ops(const Args& A, uint64_t b, const double (&v)[kPer], unsigned resc) {
   const uint64_t j0 = b * kT + kPer * (threadIdx.x & 31);
+  double c[kPer];
 #pragma unroll
-  for (int e = 0; e < kPer; ++e)
-    if (j0 + e < A.n) A.w.opv[j0 + e] = ((resc >> e) & 1u) ? -v[e] : v[e];
+  for (int e = 0; e < kPer; ++e) c[e] = ((resc >> e) & 1u) ? -v[e] : v[e];
+  if (j0 + kPer <= A.n) {
+    double2* dst = reinterpret_cast<double2*>(A.w.opv + j0);
+#pragma unroll
+    for (int e = 0; e < kPer; e += 2) dst[e / 2] = make_double2(c[e], c[e + 1]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < kPer; ++e)
+      if (j0 + e < A.n) A.w.opv[j0 + e] = c[e];
+  }
 }
 __device__ __forceinline__ unsigned warp_cached_ops(const Args& A, uint64_t b, double (&v)[kPer]) {
   const uint64_t j0 = b * kT + kPer * (threadIdx.x & 31);
+  double c[kPer];
+  if (j0 + kPer <= A.n) {
+    const double2* src = reinterpret_cast<const double2*>(A.w.opv + j0);
+#pragma unroll
+    for (int e = 0; e < kPer; e += 2) {
+      const double2 q = src[e / 2];
+      c[e] = q.x;
+      c[e + 1] = q.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) c[e] = j0 + e < A.n ? A.w.opv[j0 + e] : 0.0;
+  }
   unsigned resc = 0u;
 #pragma unroll
   for (int e = 0; e < kPer; ++e) {
-    const double c = j0 + e < A.n ? A.w.opv[j0 + e] : 0.0;
-    if (signbit(c)) resc |= 1u << e;
-    v[e] = fabs(c);
+    if (signbit(c[e])) resc |= 1u << e;
+    v[e] = fabs(c[e]);
   }
   return resc;
 }
