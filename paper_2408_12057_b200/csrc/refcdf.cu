@@ -743,21 +743,24 @@ constexpr uint64_t kSlotRun = 8192;  // longer runs of one ancestor go to the wh
 __device__ void phase_ancestors(const Args& A, double u) {
   const double dn = (double)A.n, rn = __drcp_rn(dn);
   const int ln = threadIdx.x & 31;
-  // warp-uniform trip count: every lane of a warp iterates while any lane has particles
-  const uint64_t stride = (uint64_t)gridDim.x * kT;
-  for (uint64_t j0 = (uint64_t)blockIdx.x * kT + (threadIdx.x & ~31u); j0 < A.n; j0 += stride) {
-    const uint64_t j = j0 + ln;
-    uint64_t lo = 0, hi = 0;
-    if (j < A.n) {
-      lo = j == 0 ? 0 : first_slot_above(A.cum[j - 1], u, A.n, dn, rn);
-      hi = j + 1 == A.n ? A.n : first_slot_above(A.cum[j], u, A.n, dn, rn);
-      if (hi - lo > kSlotRun) {  // a heavy ancestor: the rest of its slots go to the grid
-        const unsigned int e = atomicAdd(A.w.novf, 1u);
-        A.w.ovf[3 * e] = lo + kSlotRun;
-        A.w.ovf[3 * e + 1] = hi;
-        A.w.ovf[3 * e + 2] = j;
-        hi = lo + kSlotRun;
-      }
+  // one M(cum) per lane: a warp covers 31 particles, lane l >= 1 owns particle
+  // j = j0 + l - 1 and evaluates M(cum_j), its upper end; its lower end M(cum_{j-1}) is
+  // lane l - 1's value (lane 0 evaluates M(cum_{j0-1}) only).  Warp-uniform trip count.
+  const uint64_t nwarp = (uint64_t)gridDim.x * (kT / 32);
+  for (uint64_t j0 = ((uint64_t)blockIdx.x * (kT / 32) + (threadIdx.x >> 5)) * 31; j0 < A.n; j0 += nwarp * 31) {
+    const uint64_t idx = j0 + ln;  // = j + 1: the CDF entry this lane evaluates is idx - 1
+    uint64_t mv = 0;
+    if (idx >= 1 && idx <= A.n) mv = idx == A.n ? A.n : first_slot_above(A.cum[idx - 1], u, A.n, dn, rn);
+    uint64_t lo = __shfl_up_sync(0xffffffffu, mv, 1), hi = mv;
+    const bool own = ln >= 1 && idx - 1 < A.n;
+    const uint64_t j = idx - 1;
+    if (!own) lo = hi = 0;
+    if (own && hi - lo > kSlotRun) {  // a heavy ancestor: the rest of its slots go to the grid
+      const unsigned int e = atomicAdd(A.w.novf, 1u);
+      A.w.ovf[3 * e] = lo + kSlotRun;
+      A.w.ovf[3 * e + 1] = hi;
+      A.w.ovf[3 * e + 2] = j;
+      hi = lo + kSlotRun;
     }
     // short runs (the common case: ~1 slot per particle) by their own lane; the warp
     // writes the longer ones together, 32 slots at a time
@@ -769,7 +772,7 @@ __device__ void phase_ancestors(const Args& A, double u) {
       const int src = __ffs(bal) - 1;
       bal &= bal - 1;
       const uint64_t a = __shfl_sync(0xffffffffu, lo, src), e = __shfl_sync(0xffffffffu, hi, src);
-      for (uint64_t m = a + ln; m < e; m += 32) A.anc[m] = (uint32_t)(j0 + src);
+      for (uint64_t m = a + ln; m < e; m += 32) A.anc[m] = (uint32_t)(j0 + src - 1);
     }
   }
 }
