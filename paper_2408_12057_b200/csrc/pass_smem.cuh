@@ -685,11 +685,15 @@ __device__ __forceinline__ void warp_regfold_add(double lw_pre, double lg, doubl
                                                  RegFold& f) {
   const int l = (threadIdx.x & 31) % G;
   if (!active) return;
+  // one signed add for every lane (sacc_add(l, 1) == lacc_add(l) bit for bit): a single
+  // exp per warp instead of one per branch
+  const double la = log_abs_sfu(lg);
+  double val = l == kAccG0 ? lw_pre : (l == kAccG1 ? lw_pre + lg : lw_pre + 2.0 * lg), sg = 1.0;
   if (l == kAccElbo) {
-    if (lg != 0.0) sacc_add(f.acc, lw_pre + log_abs_sfu(lg), lg > 0.0 ? 1.0 : -1.0);
-  } else {
-    lacc_add(f.acc, l == kAccG0 ? lw_pre : (l == kAccG1 ? lw_pre + lg : lw_pre + 2.0 * lg));
+    val = lg != 0.0 ? lw_pre + la : -__builtin_huge_val();
+    sg = lg > 0.0 ? 1.0 : -1.0;
   }
+  sacc_add(f.acc, val, sg);
   if (l == 0) {
     lacc_add(f.sq, 2.0 * lw_post);
     top2_add(f.top, lw_post);
