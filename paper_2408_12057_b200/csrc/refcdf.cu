@@ -103,16 +103,6 @@ __device__ __forceinline__ unsigned long long add_units(double e, int k, bool& t
 }
 
 // ---- CTA helpers --------------------------------------------------------------
-__device__ __forceinline__ double cta_max(double v, double* sh) {
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double r = sh[0];
-  for (int i = 1; i < kT / 32; ++i) r = fmax(r, sh[i]);
-  return r;
-}
-
 // exclusive prefix max over the CTA's elements (thread order), seeded with `seed`
 __device__ __forceinline__ double cta_excl_max(double v, double seed, double* sh) {
   const int ln = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -128,16 +118,6 @@ __device__ __forceinline__ double cta_excl_max(double v, double seed, double* sh
   for (int i = 0; i < w; ++i) pre = fmax(pre, sh[i]);
   const double up = __shfl_up_sync(0xffffffffu, inc, 1);
   return ln == 0 ? pre : fmax(pre, up);
-}
-
-__device__ __forceinline__ unsigned long long cta_sum_u64(unsigned long long v, unsigned long long* sh) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-  __syncthreads();
-  unsigned long long r = 0;
-  for (int i = 0; i < kT / 32; ++i) r += sh[i];
-  return r;
 }
 
 // inclusive prefix sum over the CTA's elements (thread order)
