@@ -61,7 +61,23 @@ int fail(int code, const char* fmt, ...) {
 struct DevCtx {
   cudaStream_t stream = nullptr;
   int sms = 148;
+  char* pinned = nullptr;  // page-locked staging for the per-call result copies (grown on demand)
+  size_t pinned_cap = 0;
 };
+
+// page-locked staging of at least `bytes` (kept for the context's lifetime)
+int pinned_staging(DevCtx* C, size_t bytes, char** out) {
+  if (C->pinned_cap < bytes) {
+    if (C->pinned) cudaFreeHost(C->pinned);
+    C->pinned = nullptr;
+    C->pinned_cap = 0;
+    const size_t cap = bytes < 65536 ? 65536 : bytes * 2;
+    CU(cudaHostAlloc(reinterpret_cast<void**>(&C->pinned), cap, cudaHostAllocPortable));
+    C->pinned_cap = cap;
+  }
+  *out = C->pinned;
+  return 0;
+}
 
 int get_ctx(int device, DevCtx** out, uint64_t user_stream = 0) {
   static thread_local std::map<int, DevCtx> ctxs;
@@ -85,10 +101,10 @@ int get_ctx(int device, DevCtx** out, uint64_t user_stream = 0) {
     CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     it = ctxs.emplace(device, c).first;
   }
-  static thread_local DevCtx user;
+  static thread_local DevCtx user;  // the caller's stream; its own (persistent) staging
   if (user_stream) {
-    user = it->second;
     user.stream = reinterpret_cast<cudaStream_t>(user_stream);
+    user.sms = it->second.sms;
     *out = &user;
     return 0;
   }
@@ -1186,25 +1202,66 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
     }
     CU(cudaEventRecord(ev[k + 1], C->stream));
   }
+  // every result of every round in one page-locked staging area: the copies are enqueued
+  // behind the rounds and the call synchronises once (per-array synchronous copies cost
+  // ~10 us each -- most of a small run's wall time)
+  struct Off {
+    size_t g0, g1, g2, es, cz, lam, b, rs, scal, st;
+  };
+  std::vector<Off> off(rounds);
+  size_t bytes = 16;  // gerr first
+  for (int k = 0; k < rounds; ++k) {
+    const size_t d8 = sizeof(double) * (ts[k] + 1);
+    Off& o = off[k];
+    o.g0 = bytes, bytes += d8;
+    o.g1 = bytes, bytes += d8;
+    o.g2 = bytes, bytes += d8;
+    o.es = bytes, bytes += d8;
+    o.cz = bytes, bytes += d8;
+    o.lam = bytes, bytes += d8;
+    o.b = bytes, bytes += d8;
+    o.scal = bytes, bytes += 2 * sizeof(double);
+    o.st = bytes, bytes += (sizeof(SmcState) + 15) / 16 * 16;
+    o.rs = bytes, bytes += (size_t)(ts[k] + 1 + 15) / 16 * 16;
+  }
+  char* H;
+  TRY(pinned_staging(C, bytes, &H));
+  CU(cudaMemcpyAsync(H, gerr.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
+  for (int k = 0; k < rounds; ++k) {
+    const size_t d8 = sizeof(double) * (ts[k] + 1);
+    const Off& o = off[k];
+    CU(cudaMemcpyAsync(H + o.g0, R[k].g0.p, d8, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaMemcpyAsync(H + o.g1, R[k].g1.p, d8, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaMemcpyAsync(H + o.g2, R[k].g2.p, d8, cudaMemcpyDeviceToHost, C->stream));
+    if (mode == ASMC_MODE_SSMC) CU(cudaMemcpyAsync(H + o.es, R[k].ess.p, d8, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaMemcpyAsync(H + o.cz, R[k].cz.p, d8, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaMemcpyAsync(H + o.lam, R[k].lam.p, d8, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaMemcpyAsync(H + o.b, betas[k].p, d8, cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaMemcpyAsync(H + o.scal, R[k].scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaMemcpyAsync(H + o.st, R[k].st.p, sizeof(SmcState), cudaMemcpyDeviceToHost, C->stream));
+    CU(cudaMemcpyAsync(H + o.rs, R[k].rs.p, ts[k] + 1, cudaMemcpyDeviceToHost, C->stream));
+  }
   CU(cudaStreamSynchronize(C->stream));
   int herr = 0;
-  CU(cudaMemcpy(&herr, gerr.p, sizeof(int), cudaMemcpyDeviceToHost));
+  std::memcpy(&herr, H, sizeof(int));
   int rc = 0;
   for (int k = 0; k < rounds && !rc; ++k) {
     const int T = ts[k];
-    std::vector<double> g0(T + 1), g1(T + 1), g2(T + 1), es(T + 1), cz(T + 1), b(T + 1);
-    std::vector<uint8_t> rs(T + 1);
-    std::vector<int32_t> rt(T + 1);
-    asmc_report rep{g0.data(), g1.data(), g2.data(), es.data(), cz.data(), rs.data(), rt.data(),
-                    0, 0, 0, 0, 0, 0};
+    const Off& o = off[k];
+    const double* g0 = reinterpret_cast<const double*>(H + o.g0);
+    const double* g1 = reinterpret_cast<const double*>(H + o.g1);
+    const double* g2 = reinterpret_cast<const double*>(H + o.g2);
+    const double* es = reinterpret_cast<const double*>(H + o.es);
+    const double* cz = reinterpret_cast<const double*>(H + o.cz);
+    const double* lam = reinterpret_cast<const double*>(H + o.lam);
+    const double* b = reinterpret_cast<const double*>(H + o.b);
+    const double* scal = reinterpret_cast<const double*>(H + o.scal);
+    const uint8_t* rs = reinterpret_cast<const uint8_t*>(H + o.rs);
     SmcState st;
-    TRY(copy_round(C->stream, R[k], T, mode == ASMC_MODE_SSMC, &rep, &st));
+    std::memcpy(&st, H + o.st, sizeof st);
     TRY(device_error(st.err, st.err_step, st.err_val));
     if (herr == ASMC_ERR_EVALUATION) return device_error(herr, 0, 0.0);
     if (herr) return fail(herr, "schedule generation after round %d failed validation", k + 1);
-    std::vector<double> lam(T + 1);
-    CU(cudaMemcpy(lam.data(), R[k].lam.p, sizeof(double) * (T + 1), cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(b.data(), betas[k].p, sizeof(double) * (T + 1), cudaMemcpyDeviceToHost));
     float ms = 0.f;
     CU(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
     const size_t r0 = (size_t)k * stride;
@@ -1220,8 +1277,8 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
       if (out->resampled) out->resampled[r0 + t] = rs[t];
       if (out->lambda) out->lambda[r0 + t] = lam[t];
     }
-    if (out->log_z_hat) out->log_z_hat[k] = rep.log_z_hat;
-    if (out->elbo_hat) out->elbo_hat[k] = rep.elbo_hat;
+    if (out->log_z_hat) out->log_z_hat[k] = scal[0];
+    if (out->elbo_hat) out->elbo_hat[k] = scal[1];
     if (out->wall_seconds) out->wall_seconds[k] = ms * 1e-3;
     if (out->kernel_applications) out->kernel_applications[k] = ns[k] * (uint64_t)T;
   }
