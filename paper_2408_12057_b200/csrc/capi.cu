@@ -786,7 +786,7 @@ int enqueue_lg_round(DevCtx* C, const LgData& D, const asmc_target_desc* t, cons
   return 0;
 }
 
-int copy_round(cudaStream_t s, RoundBufs& R, int T, bool smc, asmc_report* out, SmcState* st);
+int copy_round(DevCtx* C, RoundBufs& R, int T, bool smc, asmc_report* out, SmcState* st);
 
 // ------------------------------------------------------ config 5: Ising --
 int is_check(const asmc_target_desc* t, const asmc_kernel_desc* k, const asmc_exec& ex) {
@@ -891,7 +891,7 @@ int run_is_single(const asmc_target_desc* target, const asmc_kernel_desc* kernel
   LgWork W;
   TRY(enqueue_is_round(C, target, kernel, d_betas.p, T, n, policy, rho, seed, round, R.rd.p, R.st.p, W));
   SmcState st;
-  TRY(copy_round(C->stream, R, T, smc, out, &st));
+  TRY(copy_round(C, R, T, smc, out, &st));
   TRY(device_error(st.err, st.err_step, st.err_val));
   out->kernel_applications = n * (uint64_t)T;
   out->wall_seconds = now_s() - t0;
@@ -917,7 +917,7 @@ int run_lg_single(const asmc_target_desc* target, const asmc_kernel_desc* kernel
   LgWork W;
   TRY(enqueue_lg_round(C, D, target, kernel, d_betas.p, T, n, policy, rho, seed, round, R.rd.p, R.st.p, W));
   SmcState st;
-  TRY(copy_round(C->stream, R, T, smc, out, &st));
+  TRY(copy_round(C, R, T, smc, out, &st));
   TRY(device_error(st.err, st.err_step, st.err_val));
   out->kernel_applications = n * (uint64_t)T;
   out->wall_seconds = now_s() - t0;
@@ -971,32 +971,45 @@ int stepouter_partials(const asmc_target_desc* target, const asmc_kernel_desc* k
   return 0;
 }
 
-int copy_round(cudaStream_t s, RoundBufs& R, int T, bool smc, asmc_report* out, SmcState* st) {
-  std::vector<double> tmp(T + 1);
-  auto get = [&](const double* src, double* dst) -> int {
-    if (!dst) return 0;
-    CU(cudaMemcpyAsync(dst, src, sizeof(double) * (T + 1), cudaMemcpyDeviceToHost, s));
+int copy_round(DevCtx* C, RoundBufs& R, int T, bool smc, asmc_report* out, SmcState* st) {
+  // one page-locked staging area, one synchronisation (see asmc_run_rounds)
+  cudaStream_t s = C->stream;
+  const size_t d8 = sizeof(double) * (T + 1);
+  const size_t o_g0 = 0, o_g1 = d8, o_g2 = 2 * d8, o_es = 3 * d8, o_cz = 4 * d8, o_scal = 5 * d8,
+               o_st = o_scal + 16, o_rt = o_st + (sizeof(SmcState) + 15) / 16 * 16,
+               o_rs = o_rt + (sizeof(int32_t) * (T + 1) + 15) / 16 * 16, bytes = o_rs + T + 1;
+  char* H;
+  TRY(pinned_staging(C, bytes, &H));
+  auto get = [&](const void* src, size_t off, size_t n, bool want) -> int {
+    if (!want) return 0;
+    CU(cudaMemcpyAsync(H + off, src, n, cudaMemcpyDeviceToHost, s));
     return 0;
   };
-  TRY(get(R.g0.p, out->log_g0));
-  TRY(get(R.g1.p, out->log_g1));
-  TRY(get(R.g2.p, out->log_g2));
-  if (smc) TRY(get(R.ess.p, out->ess_trace));
-  TRY(get(R.cz.p, out->cum_log_z));
-  if (out->resampled)
-    CU(cudaMemcpyAsync(out->resampled, R.rs.p, T + 1, cudaMemcpyDeviceToHost, s));
-  double scal[2];
-  CU(cudaMemcpyAsync(scal, R.scal.p, sizeof scal, cudaMemcpyDeviceToHost, s));
-  CU(cudaMemcpyAsync(st, R.st.p, sizeof(SmcState), cudaMemcpyDeviceToHost, s));
-  std::vector<int32_t> rt(T + 1);
-  CU(cudaMemcpyAsync(rt.data(), R.rt.p, sizeof(int32_t) * (T + 1), cudaMemcpyDeviceToHost, s));
+  TRY(get(R.g0.p, o_g0, d8, out->log_g0 != nullptr));
+  TRY(get(R.g1.p, o_g1, d8, out->log_g1 != nullptr));
+  TRY(get(R.g2.p, o_g2, d8, out->log_g2 != nullptr));
+  TRY(get(R.ess.p, o_es, d8, smc && out->ess_trace != nullptr));
+  TRY(get(R.cz.p, o_cz, d8, out->cum_log_z != nullptr));
+  TRY(get(R.rs.p, o_rs, T + 1, out->resampled != nullptr));
+  TRY(get(R.scal.p, o_scal, 2 * sizeof(double), true));
+  TRY(get(R.st.p, o_st, sizeof(SmcState), true));
+  TRY(get(R.rt.p, o_rt, sizeof(int32_t) * (T + 1), smc));
   CU(cudaStreamSynchronize(s));
+  if (out->log_g0) std::memcpy(out->log_g0, H + o_g0, d8);
+  if (out->log_g1) std::memcpy(out->log_g1, H + o_g1, d8);
+  if (out->log_g2) std::memcpy(out->log_g2, H + o_g2, d8);
+  if (smc && out->ess_trace) std::memcpy(out->ess_trace, H + o_es, d8);
+  if (out->cum_log_z) std::memcpy(out->cum_log_z, H + o_cz, d8);
+  if (out->resampled) std::memcpy(out->resampled, H + o_rs, T + 1);
+  double scal[2];
+  std::memcpy(scal, H + o_scal, sizeof scal);
+  std::memcpy(st, H + o_st, sizeof(SmcState));
   out->log_z_hat = scal[0];
   out->elbo_hat = scal[1];
   if (smc) {
     out->n_resample_times = st->n_resample;
     if (out->resample_times)
-      for (int i = 0; i < st->n_resample; ++i) out->resample_times[i] = rt[i];
+      std::memcpy(out->resample_times, H + o_rt, sizeof(int32_t) * (size_t)st->n_resample);
   } else {
     out->n_resample_times = 1;
     if (out->resample_times) out->resample_times[0] = T;
@@ -1051,7 +1064,7 @@ int asmc_run_sais_single(const asmc_target_desc* target, const asmc_kernel_desc*
   const PassArgs base = base_args(target, kernel);
   TRY(enqueue_sais_round(C, ex, L, base, d_betas.p, T, n, seed, round, R.rd.p, &R.st.p->err, W));
   SmcState st;
-  TRY(copy_round(C->stream, R, T, false, out, &st));
+  TRY(copy_round(C, R, T, false, out, &st));
   TRY(device_error(st.err, st.err_step, st.err_val));
   out->kernel_applications = n * (uint64_t)T;
   out->wall_seconds = now_s() - t0;
@@ -1088,7 +1101,7 @@ int asmc_run_smc(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
   const PassArgs base = base_args(target, kernel);
   TRY(enqueue_smc_round(C, ex, L, base, d_betas.p, T, n, policy, rho, seed, round, R.rd.p, R.st.p, W));
   SmcState st;
-  TRY(copy_round(C->stream, R, T, true, out, &st));
+  TRY(copy_round(C, R, T, true, out, &st));
   TRY(device_error(st.err, st.err_step, st.err_val));
   out->kernel_applications = n * (uint64_t)T;
   out->wall_seconds = now_s() - t0;
@@ -1553,7 +1566,7 @@ int asmc_fold_partials_dev(const asmc_logacc* partials_dev, uint64_t chunks, int
   LCH(launch_fold_chunks_final(chunk.p, chunks, 1, T, 4, tot.p, C->stream));
   LCH(launch_sais_report(tot.p, T, n, R.rd.p, C->stream));
   SmcState st;
-  TRY(copy_round(C->stream, R, T, false, out, &st));
+  TRY(copy_round(C, R, T, false, out, &st));
   TRY(device_error(st.err, st.err_step, st.err_val));
   out->kernel_applications = n * (uint64_t)T;
   return 0;
@@ -1582,7 +1595,7 @@ int asmc_fold_partials(const asmc_logacc* partials, uint64_t chunks, int32_t T, 
   LCH(launch_fold_chunks_final(chunk.p, chunks, 1, T, 4, tot.p, C->stream));
   LCH(launch_sais_report(tot.p, T, n, R.rd.p, C->stream));
   SmcState st;
-  TRY(copy_round(C->stream, R, T, false, out, &st));
+  TRY(copy_round(C, R, T, false, out, &st));
   TRY(device_error(st.err, st.err_step, st.err_val));
   out->kernel_applications = n * (uint64_t)T;
   return 0;
@@ -2018,7 +2031,7 @@ int asmc_run_zja(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
     SmcWork W;  // run_smc(policy never): the report carries the ESS trace, as the reference's pilot
     TRY(enqueue_smc_round(C, ex, L, base, d_pb.p, K, n, ASMC_POLICY_NEVER, 0.5, o->seed, 1, R.rd.p, R.st.p, W));
     SmcState st;
-    TRY(copy_round(C->stream, R, K, true, &out->pilot, &st));
+    TRY(copy_round(C, R, K, true, &out->pilot, &st));
     TRY(device_error(st.err, st.err_step, st.err_val));
     out->pilot.kernel_applications = n * (uint64_t)K;
     std::vector<double> lam(K + 1);
@@ -2100,7 +2113,7 @@ int asmc_run_zja(const asmc_target_desc* target, const asmc_kernel_desc* kernel,
   }
   if (t + 1 > out->capacity) return fail(ASMC_ERR_INVALID_ARGUMENT, "output capacity too small (%d needed)", t + 1);
   SmcState st;
-  TRY(copy_round(C->stream, R, t, true, &out->main, &st));
+  TRY(copy_round(C, R, t, true, &out->main, &st));
   TRY(device_error(st.err, st.err_step, st.err_val));
   out->main.kernel_applications = n * (uint64_t)t;
   out->main.wall_seconds = now_s() - t0;
@@ -2276,6 +2289,8 @@ int asmc_smc_shard_create(const asmc_target_desc* target, const asmc_kernel_desc
   DevCtx* C;
   if ((rc = get_ctx(ex.device, &C, ex.stream))) return drop(rc);
   h->C = *C;
+  h->C.pinned = nullptr;  // the shard's own staging (the context's stays the context's)
+  h->C.pinned_cap = 0;
   h->ex = ex;
   h->T = T;
   h->policy = policy;
@@ -2331,6 +2346,7 @@ int asmc_smc_shard_create(const asmc_target_desc* target, const asmc_kernel_desc
 void asmc_smc_shard_destroy(asmc_smc_shard* h) {
   if (!h) return;
   cudaStreamSynchronize(h->C.stream);
+  if (h->C.pinned) cudaFreeHost(h->C.pinned);
   delete h;
 }
 
@@ -2446,7 +2462,7 @@ int asmc_smc_shard_report(asmc_smc_shard* h, asmc_report* out) {
   if (T < 1 || h->t_done != T || h->resampling)
     return fail(ASMC_ERR_INVALID_ARGUMENT, "report before step %d completed", h->T);
   SmcState st;
-  TRY(copy_round(h->C.stream, h->R, T, true, out, &st));
+  TRY(copy_round(&h->C, h->R, T, true, out, &st));
   TRY(device_error(st.err, st.err_step, st.err_val));
   out->kernel_applications = h->n * (uint64_t)T;
   return 0;
