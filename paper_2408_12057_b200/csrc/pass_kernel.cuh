@@ -476,7 +476,10 @@ __device__ void block_reduce(const double* s_lw, const double* s_lg, const doubl
     // FADD/FMA (no exp on the sequential path).  Called by all NG == blockDim threads.
     static_assert(NG == kBlock, "exact-order fold: one thread per particle of the block");
     constexpr int kL = kAccTop2;  // log-sum accumulators g0, g1, g2, elbo, sq
-    __shared__ double s_e[kL][NG];
+    // element q's add as sum <- sum * m + a in two roundings: below the running max
+    // (m, a) = (1, sign e) -- the reference's sum += e --, a new max (e, sign) -- its
+    // sum = sum e + 1 --, a skipped element (1, -0), an exact identity
+    __shared__ double s_m[kL][NG], s_a[kL][NG];
     __shared__ unsigned char s_f[kL][NG];  // 0 = skipped, 1 = below the running max, 2 = new max
     __shared__ double s_wmax[NG / 32][kL];
     const int g = threadIdx.x;
@@ -513,11 +516,14 @@ __device__ void block_reduce(const double* s_lw, const double* s_lg, const doubl
       const double ex = ln == 0 ? pre : fmax(pre, up);  // running max before element g
       if (k >= nl || l[k] == -__builtin_huge_val()) {
         s_f[k][g] = 0;
-        s_e[k][g] = 0.0;
+        s_m[k][g] = 1.0;
+        s_a[k][g] = -0.0;
       } else {
         const bool below = l[k] <= ex;
-        s_e[k][g] = exp(below ? l[k] - ex : ex - l[k]);
+        const double e = exp(below ? l[k] - ex : ex - l[k]);
         s_f[k][g] = below ? 1 : 2;
+        s_m[k][g] = below ? 1.0 : e;
+        s_a[k][g] = below ? sg[k] * e : sg[k];
       }
     }
     __syncthreads();
@@ -528,22 +534,22 @@ __device__ void block_reduce(const double* s_lw, const double* s_lg, const doubl
         for (int q = 0; q < NG; ++q)
           if (s_act[q]) top2_add(acc, s_post[q]);
       } else {
-        const double sign = a == kAccElbo ? 0.0 : 1.0;  // elbo: per-element sign below
-        double sum = 0.0, mx = -__builtin_huge_val();
+        // the particle-order chain, branch-free (loads independent of the chain)
+        double sum = 0.0;
+        int qlast = -1;  // the last new max: the accumulator's max after the block
+#pragma unroll 8
         for (int q = 0; q < NG; ++q) {
-          const unsigned char f = s_f[a][q];
-          if (f == 0) continue;
-          const double sq = a == kAccElbo ? (s_lg[q] > 0.0 ? 1.0 : -1.0) : sign;
-          if (f == 1) {
-            sum += sq * s_e[a][q];
-          } else {
-            sum = sum * s_e[a][q] + sq;
-            mx = a == kAccG0 ? s_lw[q]
-                 : a == kAccG1 ? s_lw[q] + s_lg[q]
-                 : a == kAccG2 ? s_lw[q] + 2.0 * s_lg[q]
-                 : a == kAccElbo ? s_lw[q] + log(fabs(s_lg[q]))
-                                 : 2.0 * s_post[q];
-          }
+          sum = __dadd_rn(__dmul_rn(sum, s_m[a][q]), s_a[a][q]);
+          qlast = s_f[a][q] == 2 ? q : qlast;
+        }
+        double mx = -__builtin_huge_val();
+        if (qlast >= 0) {
+          const int q = qlast;
+          mx = a == kAccG0 ? s_lw[q]
+               : a == kAccG1 ? s_lw[q] + s_lg[q]
+               : a == kAccG2 ? s_lw[q] + 2.0 * s_lg[q]
+               : a == kAccElbo ? s_lw[q] + log(fabs(s_lg[q]))
+                               : 2.0 * s_post[q];
         }
         acc = LogAcc{mx, sum};
       }
@@ -589,8 +595,11 @@ __device__ void block_reduce(const double* s_lw, const double* s_lg, const doubl
 }
 
 // =============================================================== kernel
+// small-dimension (register-resident, KMAX = 16) instantiations: 2 CTAs per SM, so a
+// round of up to 296 blocks (~76k particles) is resident at once (config 1's rounds are
+// 64-182 blocks: with one 236-register CTA per SM its last round ran in two waves)
 template <class Tgt, int RNG, typename Real, int G, int KMAX>
-__global__ void __launch_bounds__(kBlock) pass_kernel(const __grid_constant__ PassArgs A) {
+__global__ void __launch_bounds__(kBlock, KMAX <= 16 ? 2 : 1) pass_kernel(const __grid_constant__ PassArgs A) {
   constexpr int NG = kBlock / G;
   constexpr bool kExact = std::is_same<Real, double>::value;
   static_assert(!kExact || G == 1, "reference-order path is one lane per particle");

@@ -72,9 +72,11 @@ struct XoStream {
     const double u2 = uniform();
     const double r = sqrt(-2.0 * log(u1));
     const double a = 6.283185307179586477 * u2;
-    cached = r * sin(a);
+    double sa, ca;
+    sincos(a, &sa, &ca);  // one argument reduction for both (the same bits as sin and cos)
+    cached = r * sa;
     have = true;
-    return r * cos(a);
+    return r * ca;
   }
 };
 
@@ -152,8 +154,10 @@ __device__ __forceinline__ void bm_pair_f64(uint32_t a, uint32_t b, double& n_co
   const double u2 = (double)b * 0x1.0p-32;
   const double r = sqrt(-2.0 * log(u1));
   const double ang = 6.283185307179586477 * u2;
-  n_cos = r * cos(ang);
-  n_sin = r * sin(ang);
+  double sa, ca;
+  sincos(ang, &sa, &ca);
+  n_cos = r * ca;
+  n_sin = r * sa;
 }
 
 template <typename Real>

@@ -34,9 +34,15 @@ struct TgtParams {
   float f[16];  // host-precomputed beta-independent fp32 constants (TgtMixture::F32)
 };
 
-// target.cpp:16-19 with log(sigma) supplied
+// target.cpp:16-19 with log(sigma) supplied.  A power-of-two sigma (every configured target)
+// divides exactly by scaling: the multiply by 2^-k rounds the same exact value as the
+// division, so the bits are the reference's (an fp64 division is ~20 instructions)
 __device__ __forceinline__ double lnpdf64(double x, double mu, double sigma, double log_sigma) {
-  const double s = (x - mu) / sigma;
+  const long long b = __double_as_longlong(sigma);
+  const int ex = (int)((b >> 52) & 0x7ff);
+  const bool pow2 = (b & 0x000FFFFFFFFFFFFFll) == 0 && ex > 1 && ex < 0x7fe && b > 0;
+  const double dx = x - mu;
+  const double s = pow2 ? dx * __drcp_rn(sigma) : dx / sigma;
   return -0.5 * s * s - log_sigma - kLogSqrt2Pi;
 }
 
