@@ -463,7 +463,7 @@ struct Fast {
 // ============================================================ reductions
 // Per-step CTA reduction of the groups' (pre-update log w, lg, post log w)
 // into accumulator a, combined into the block partial across iterations r.
-template <bool kExactOrder, int NG>
+template <bool kExactOrder, int NG, bool kChain = false>
 __device__ void block_reduce(const double* s_lw, const double* s_lg, const double* s_post,
                              const int* s_act, int nacc, LogAcc* dst, bool first) {
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -476,10 +476,18 @@ __device__ void block_reduce(const double* s_lw, const double* s_lg, const doubl
     // FADD/FMA (no exp on the sequential path).  Called by all NG == blockDim threads.
     static_assert(NG == kBlock, "exact-order fold: one thread per particle of the block");
     constexpr int kL = kAccTop2;  // log-sum accumulators g0, g1, g2, elbo, sq
-    // element q's add as sum <- sum * m + a in two roundings: below the running max
-    // (m, a) = (1, sign e) -- the reference's sum += e --, a new max (e, sign) -- its
-    // sum = sum e + 1 --, a skipped element (1, -0), an exact identity
-    __shared__ double s_m[kL][NG], s_a[kL][NG];
+    // kChain (register-resident instantiations): element q's add as sum <- sum * m + a in
+    // two roundings -- below the running max (m, a) = (1, sign e), the reference's
+    // sum += e; a new max (e, sign), its sum = sum e + 1; skipped (1, -0), an identity --
+    // a branch-free chain.  Otherwise the chain branches on the flag and reads e (half
+    // the shared memory for the local-memory instantiations).
+    struct ChainS {
+      double m[kL][NG], a[kL][NG];
+    };
+    struct FlagS {
+      double e[kL][NG];
+    };
+    __shared__ typename std::conditional<kChain, ChainS, FlagS>::type S;
     __shared__ unsigned char s_f[kL][NG];  // 0 = skipped, 1 = below the running max, 2 = new max
     __shared__ double s_wmax[NG / 32][kL];
     const int g = threadIdx.x;
@@ -516,14 +524,22 @@ __device__ void block_reduce(const double* s_lw, const double* s_lg, const doubl
       const double ex = ln == 0 ? pre : fmax(pre, up);  // running max before element g
       if (k >= nl || l[k] == -__builtin_huge_val()) {
         s_f[k][g] = 0;
-        s_m[k][g] = 1.0;
-        s_a[k][g] = -0.0;
+        if constexpr (kChain) {
+          S.m[k][g] = 1.0;
+          S.a[k][g] = -0.0;
+        } else {
+          S.e[k][g] = 0.0;
+        }
       } else {
         const bool below = l[k] <= ex;
         const double e = exp(below ? l[k] - ex : ex - l[k]);
         s_f[k][g] = below ? 1 : 2;
-        s_m[k][g] = below ? 1.0 : e;
-        s_a[k][g] = below ? sg[k] * e : sg[k];
+        if constexpr (kChain) {
+          S.m[k][g] = below ? 1.0 : e;
+          S.a[k][g] = below ? sg[k] * e : sg[k];
+        } else {
+          S.e[k][g] = e;
+        }
       }
     }
     __syncthreads();
@@ -534,13 +550,27 @@ __device__ void block_reduce(const double* s_lw, const double* s_lg, const doubl
         for (int q = 0; q < NG; ++q)
           if (s_act[q]) top2_add(acc, s_post[q]);
       } else {
-        // the particle-order chain, branch-free (loads independent of the chain)
+        // the particle-order chain
         double sum = 0.0;
         int qlast = -1;  // the last new max: the accumulator's max after the block
+        if constexpr (kChain) {
 #pragma unroll 8
-        for (int q = 0; q < NG; ++q) {
-          sum = __dadd_rn(__dmul_rn(sum, s_m[a][q]), s_a[a][q]);
-          qlast = s_f[a][q] == 2 ? q : qlast;
+          for (int q = 0; q < NG; ++q) {
+            sum = __dadd_rn(__dmul_rn(sum, S.m[a][q]), S.a[a][q]);
+            qlast = s_f[a][q] == 2 ? q : qlast;
+          }
+        } else {
+          for (int q = 0; q < NG; ++q) {
+            const unsigned char f = s_f[a][q];
+            if (f == 0) continue;
+            const double sq = a == kAccElbo ? (s_lg[q] > 0.0 ? 1.0 : -1.0) : 1.0;
+            if (f == 1) {
+              sum = __dadd_rn(sum, __dmul_rn(sq, S.e[a][q]));
+            } else {
+              sum = __dadd_rn(__dmul_rn(sum, S.e[a][q]), sq);
+              qlast = q;
+            }
+          }
         }
         double mx = -__builtin_huge_val();
         if (qlast >= 0) {
@@ -597,9 +627,11 @@ __device__ void block_reduce(const double* s_lw, const double* s_lg, const doubl
 // =============================================================== kernel
 // small-dimension (register-resident, KMAX = 16) instantiations: 2 CTAs per SM, so a
 // round of up to 296 blocks (~76k particles) is resident at once (config 1's rounds are
-// 64-182 blocks: with one 236-register CTA per SM its last round ran in two waves)
+// 64-182 blocks: with one 236-register CTA per SM its last round ran in two waves); the
+// local-memory (KMAX = 1024) ones 3 per SM (they otherwise drift to 120 registers, 2 per
+// SM: 1.0e7 -> 7.7e6 p-steps/s on config 2's shape in reference arithmetic)
 template <class Tgt, int RNG, typename Real, int G, int KMAX>
-__global__ void __launch_bounds__(kBlock, KMAX <= 16 ? 2 : 1) pass_kernel(const __grid_constant__ PassArgs A) {
+__global__ void __launch_bounds__(kBlock, KMAX <= 16 ? 2 : 3) pass_kernel(const __grid_constant__ PassArgs A) {
   constexpr int NG = kBlock / G;
   constexpr bool kExact = std::is_same<Real, double>::value;
   static_assert(!kExact || G == 1, "reference-order path is one lane per particle");
@@ -716,7 +748,7 @@ __global__ void __launch_bounds__(kBlock, KMAX <= 16 ? 2 : 1) pass_kernel(const 
         s_dst[tid] = part[((size_t)(t - A.row_base) * kNAcc + tid) * A.part_stride + blk];
       }
       __syncthreads();
-      block_reduce<kExact, NG>(s_lw, s_lg, s_post, s_act, nacc, s_dst, first);
+      block_reduce<kExact, NG, (KMAX <= 16)>(s_lw, s_lg, s_post, s_act, nacc, s_dst, first);
       __syncthreads();
       if (tid < nacc) part[((size_t)(t - A.row_base) * kNAcc + tid) * A.part_stride + blk] = s_dst[tid];
     }
