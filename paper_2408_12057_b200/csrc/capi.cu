@@ -63,6 +63,7 @@ struct DevCtx {
   int sms = 148;
   char* pinned = nullptr;  // page-locked staging for the per-call result copies (grown on demand)
   size_t pinned_cap = 0;
+  std::vector<cudaEvent_t> events;  // reusable timing events (asmc_run_rounds)
 };
 
 // page-locked staging of at least `bytes` (kept for the context's lifetime)
@@ -117,11 +118,16 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   cudaStream_t s = nullptr;
+  bool own = true;
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && own) cudaFreeAsync(p, s);
+  }
+  void borrow(T* q) {  // a view into a caller-owned arena (not freed here)
+    p = q;
+    own = false;
   }
   int alloc(size_t n, cudaStream_t st) {
     s = st;
@@ -491,6 +497,34 @@ struct RoundBufs {
     host = RoundDev{g0.p, g1.p, g2.p, ess.p, cz.p, rs.p, rt.p, lam.p, scal.p, st.p};
     CU(cudaMemcpyAsync(rd.p, &host, sizeof host, cudaMemcpyHostToDevice, s));
     return 0;
+  }
+  // the same buffers as views into one arena (asmc_run_rounds: one allocation and one
+  // zero-fill for all rounds; the caller uploads `host` to rd)
+  static size_t a256(size_t b) { return (b + 255) / 256 * 256; }
+  static size_t carve_bytes(int T) {
+    const size_t d8 = sizeof(double) * (T + 1);
+    return 6 * a256(d8) + a256(2 * sizeof(double)) + a256(T + 1) + a256(sizeof(int32_t) * (T + 1)) +
+           a256(sizeof(SmcState)) + a256(sizeof(RoundDev));
+  }
+  void carve(int T, char*& cur) {
+    const size_t d8 = sizeof(double) * (T + 1);
+    auto take = [&](size_t b) {
+      char* r = cur;
+      cur += a256(b);
+      return r;
+    };
+    g0.borrow(reinterpret_cast<double*>(take(d8)));
+    g1.borrow(reinterpret_cast<double*>(take(d8)));
+    g2.borrow(reinterpret_cast<double*>(take(d8)));
+    ess.borrow(reinterpret_cast<double*>(take(d8)));
+    cz.borrow(reinterpret_cast<double*>(take(d8)));
+    lam.borrow(reinterpret_cast<double*>(take(d8)));
+    scal.borrow(reinterpret_cast<double*>(take(2 * sizeof(double))));
+    rs.borrow(reinterpret_cast<uint8_t*>(take(T + 1)));
+    rt.borrow(reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (T + 1))));
+    st.borrow(reinterpret_cast<SmcState*>(take(sizeof(SmcState))));
+    rd.borrow(reinterpret_cast<RoundDev*>(take(sizeof(RoundDev))));
+    host = RoundDev{g0.p, g1.p, g2.p, ess.p, cz.p, rs.p, rt.p, lam.p, scal.p, st.p};
   }
 };
 
@@ -1172,22 +1206,71 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
   LgData lgd;
   if (lg) TRY(lg_upload(C, target, lgd));
   const int stride = out->max_steps + 1;
+  // every round's outputs, schedules and scratch in one arena (one allocation, one
+  // zero-fill), the uploads from the page-locked staging, the timing events reused: a
+  // small run (config 1) is otherwise dominated by ~50 tiny allocations and copies
   std::vector<RoundBufs> R(rounds);
   std::vector<DBuf<double>> betas(rounds);
   DBuf<double> sched_scratch;
-  TRY(sched_scratch.alloc(5 * (size_t)(tmax + 1), C->stream));
-  for (int k = 0; k < rounds; ++k) {
-    TRY(R[k].alloc(ts[k], C->stream));
-    TRY(betas[k].alloc(ts[k] + 1, C->stream));
-  }
-  const double b01[2] = {0.0, 1.0};
-  CU(cudaMemcpyAsync(betas[0].p, b01, sizeof b01, cudaMemcpyHostToDevice, C->stream));
-  const PassArgs base = base_args(target, kernel);
   DBuf<int> gerr;  // pass-kernel evaluation errors and schedule-generation failures
-  TRY(gerr.alloc(1, C->stream));
-  CU(cudaMemsetAsync(gerr.p, 0, sizeof(int), C->stream));
-  std::vector<cudaEvent_t> ev(rounds + 1);
-  for (auto& e : ev) CU(cudaEventCreate(&e));
+  size_t arena_bytes = 256 + RoundBufs::a256(sizeof(double) * 5 * (tmax + 1));
+  for (int k = 0; k < rounds; ++k)
+    arena_bytes += RoundBufs::carve_bytes(ts[k]) + RoundBufs::a256(sizeof(double) * (ts[k] + 1));
+  DBuf<char> arena;
+  TRY(arena.alloc(arena_bytes, C->stream));
+  CU(cudaMemsetAsync(arena.p, 0, arena_bytes, C->stream));  // SmcState, gerr = 0
+  {
+    char* cur = arena.p;
+    gerr.borrow(reinterpret_cast<int*>(cur));
+    cur += 256;
+    sched_scratch.borrow(reinterpret_cast<double*>(cur));
+    cur += RoundBufs::a256(sizeof(double) * 5 * (tmax + 1));
+    for (int k = 0; k < rounds; ++k) {
+      R[k].carve(ts[k], cur);
+      betas[k].borrow(reinterpret_cast<double*>(cur));
+      cur += RoundBufs::a256(sizeof(double) * (ts[k] + 1));
+    }
+  }
+  // results layout in the page-locked staging (filled after the rounds, see below); the
+  // uploads use its head, which the result copies overwrite only after the kernels ran
+  struct Off {
+    size_t g0, g1, g2, es, cz, lam, b, rs, scal, st;
+  };
+  std::vector<Off> off(rounds);
+  size_t bytes = 16;  // gerr first
+  for (int k = 0; k < rounds; ++k) {
+    const size_t d8 = sizeof(double) * (ts[k] + 1);
+    Off& o = off[k];
+    o.g0 = bytes, bytes += d8;
+    o.g1 = bytes, bytes += d8;
+    o.g2 = bytes, bytes += d8;
+    o.es = bytes, bytes += d8;
+    o.cz = bytes, bytes += d8;
+    o.lam = bytes, bytes += d8;
+    o.b = bytes, bytes += d8;
+    o.scal = bytes, bytes += 2 * sizeof(double);
+    o.st = bytes, bytes += (sizeof(SmcState) + 15) / 16 * 16;
+    o.rs = bytes, bytes += (size_t)(ts[k] + 1 + 15) / 16 * 16;
+  }
+  const size_t up_bytes = 16 + sizeof(RoundDev) * rounds;
+  char* H;
+  TRY(pinned_staging(C, bytes > up_bytes ? bytes : up_bytes, &H));
+  {
+    const double b01[2] = {0.0, 1.0};
+    std::memcpy(H, b01, sizeof b01);
+    for (int k = 0; k < rounds; ++k) std::memcpy(H + 16 + sizeof(RoundDev) * k, &R[k].host, sizeof(RoundDev));
+    CU(cudaMemcpyAsync(betas[0].p, H, sizeof b01, cudaMemcpyHostToDevice, C->stream));
+    for (int k = 0; k < rounds; ++k)
+      CU(cudaMemcpyAsync(R[k].rd.p, H + 16 + sizeof(RoundDev) * k, sizeof(RoundDev), cudaMemcpyHostToDevice,
+                         C->stream));
+  }
+  const PassArgs base = base_args(target, kernel);
+  while ((int)C->events.size() < rounds + 1) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    C->events.push_back(e);
+  }
+  const std::vector<cudaEvent_t> ev(C->events.begin(), C->events.begin() + rounds + 1);
   CU(cudaEventRecord(ev[0], C->stream));
   for (int k = 0; k < rounds; ++k) {
     if (lg) {  // config 4: step-outer tensor-core engine (SAIS = policy never)
@@ -1215,30 +1298,9 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
     }
     CU(cudaEventRecord(ev[k + 1], C->stream));
   }
-  // every result of every round in one page-locked staging area: the copies are enqueued
+  // every result of every round in the page-locked staging: the copies are enqueued
   // behind the rounds and the call synchronises once (per-array synchronous copies cost
   // ~10 us each -- most of a small run's wall time)
-  struct Off {
-    size_t g0, g1, g2, es, cz, lam, b, rs, scal, st;
-  };
-  std::vector<Off> off(rounds);
-  size_t bytes = 16;  // gerr first
-  for (int k = 0; k < rounds; ++k) {
-    const size_t d8 = sizeof(double) * (ts[k] + 1);
-    Off& o = off[k];
-    o.g0 = bytes, bytes += d8;
-    o.g1 = bytes, bytes += d8;
-    o.g2 = bytes, bytes += d8;
-    o.es = bytes, bytes += d8;
-    o.cz = bytes, bytes += d8;
-    o.lam = bytes, bytes += d8;
-    o.b = bytes, bytes += d8;
-    o.scal = bytes, bytes += 2 * sizeof(double);
-    o.st = bytes, bytes += (sizeof(SmcState) + 15) / 16 * 16;
-    o.rs = bytes, bytes += (size_t)(ts[k] + 1 + 15) / 16 * 16;
-  }
-  char* H;
-  TRY(pinned_staging(C, bytes, &H));
   CU(cudaMemcpyAsync(H, gerr.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
   for (int k = 0; k < rounds; ++k) {
     const size_t d8 = sizeof(double) * (ts[k] + 1);
@@ -1295,7 +1357,6 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
     if (out->wall_seconds) out->wall_seconds[k] = ms * 1e-3;
     if (out->kernel_applications) out->kernel_applications[k] = ns[k] * (uint64_t)T;
   }
-  for (auto& e : ev) cudaEventDestroy(e);
   return rc;
 }
 
