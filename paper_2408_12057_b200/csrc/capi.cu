@@ -1231,30 +1231,11 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
       cur += RoundBufs::a256(sizeof(double) * (ts[k] + 1));
     }
   }
-  // results layout in the page-locked staging (filled after the rounds, see below); the
-  // uploads use its head, which the result copies overwrite only after the kernels ran
-  struct Off {
-    size_t g0, g1, g2, es, cz, lam, b, rs, scal, st;
-  };
-  std::vector<Off> off(rounds);
-  size_t bytes = 16;  // gerr first
-  for (int k = 0; k < rounds; ++k) {
-    const size_t d8 = sizeof(double) * (ts[k] + 1);
-    Off& o = off[k];
-    o.g0 = bytes, bytes += d8;
-    o.g1 = bytes, bytes += d8;
-    o.g2 = bytes, bytes += d8;
-    o.es = bytes, bytes += d8;
-    o.cz = bytes, bytes += d8;
-    o.lam = bytes, bytes += d8;
-    o.b = bytes, bytes += d8;
-    o.scal = bytes, bytes += 2 * sizeof(double);
-    o.st = bytes, bytes += (sizeof(SmcState) + 15) / 16 * 16;
-    o.rs = bytes, bytes += (size_t)(ts[k] + 1 + 15) / 16 * 16;
-  }
+  // the results come back as ONE copy of the arena into the page-locked staging (after
+  // the rounds, see below); the uploads use the staging's head before that
   const size_t up_bytes = 16 + sizeof(RoundDev) * rounds;
   char* H;
-  TRY(pinned_staging(C, bytes > up_bytes ? bytes : up_bytes, &H));
+  TRY(pinned_staging(C, arena_bytes > up_bytes ? arena_bytes : up_bytes, &H));
   {
     const double b01[2] = {0.0, 1.0};
     std::memcpy(H, b01, sizeof b01);
@@ -1298,42 +1279,27 @@ int asmc_run_rounds(const asmc_target_desc* target, const asmc_kernel_desc* kern
     }
     CU(cudaEventRecord(ev[k + 1], C->stream));
   }
-  // every result of every round in the page-locked staging: the copies are enqueued
-  // behind the rounds and the call synchronises once (per-array synchronous copies cost
-  // ~10 us each -- most of a small run's wall time)
-  CU(cudaMemcpyAsync(H, gerr.p, sizeof(int), cudaMemcpyDeviceToHost, C->stream));
-  for (int k = 0; k < rounds; ++k) {
-    const size_t d8 = sizeof(double) * (ts[k] + 1);
-    const Off& o = off[k];
-    CU(cudaMemcpyAsync(H + o.g0, R[k].g0.p, d8, cudaMemcpyDeviceToHost, C->stream));
-    CU(cudaMemcpyAsync(H + o.g1, R[k].g1.p, d8, cudaMemcpyDeviceToHost, C->stream));
-    CU(cudaMemcpyAsync(H + o.g2, R[k].g2.p, d8, cudaMemcpyDeviceToHost, C->stream));
-    if (mode == ASMC_MODE_SSMC) CU(cudaMemcpyAsync(H + o.es, R[k].ess.p, d8, cudaMemcpyDeviceToHost, C->stream));
-    CU(cudaMemcpyAsync(H + o.cz, R[k].cz.p, d8, cudaMemcpyDeviceToHost, C->stream));
-    CU(cudaMemcpyAsync(H + o.lam, R[k].lam.p, d8, cudaMemcpyDeviceToHost, C->stream));
-    CU(cudaMemcpyAsync(H + o.b, betas[k].p, d8, cudaMemcpyDeviceToHost, C->stream));
-    CU(cudaMemcpyAsync(H + o.scal, R[k].scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, C->stream));
-    CU(cudaMemcpyAsync(H + o.st, R[k].st.p, sizeof(SmcState), cudaMemcpyDeviceToHost, C->stream));
-    CU(cudaMemcpyAsync(H + o.rs, R[k].rs.p, ts[k] + 1, cudaMemcpyDeviceToHost, C->stream));
-  }
+  // every result of every round (the whole arena) in one copy to the page-locked staging,
+  // enqueued behind the rounds: one synchronisation for the call
+  CU(cudaMemcpyAsync(H, arena.p, arena_bytes, cudaMemcpyDeviceToHost, C->stream));
   CU(cudaStreamSynchronize(C->stream));
+  auto host_of = [&](const void* dp) { return H + (static_cast<const char*>(dp) - arena.p); };
   int herr = 0;
-  std::memcpy(&herr, H, sizeof(int));
+  std::memcpy(&herr, host_of(gerr.p), sizeof(int));
   int rc = 0;
   for (int k = 0; k < rounds && !rc; ++k) {
     const int T = ts[k];
-    const Off& o = off[k];
-    const double* g0 = reinterpret_cast<const double*>(H + o.g0);
-    const double* g1 = reinterpret_cast<const double*>(H + o.g1);
-    const double* g2 = reinterpret_cast<const double*>(H + o.g2);
-    const double* es = reinterpret_cast<const double*>(H + o.es);
-    const double* cz = reinterpret_cast<const double*>(H + o.cz);
-    const double* lam = reinterpret_cast<const double*>(H + o.lam);
-    const double* b = reinterpret_cast<const double*>(H + o.b);
-    const double* scal = reinterpret_cast<const double*>(H + o.scal);
-    const uint8_t* rs = reinterpret_cast<const uint8_t*>(H + o.rs);
+    const double* g0 = reinterpret_cast<const double*>(host_of(R[k].g0.p));
+    const double* g1 = reinterpret_cast<const double*>(host_of(R[k].g1.p));
+    const double* g2 = reinterpret_cast<const double*>(host_of(R[k].g2.p));
+    const double* es = reinterpret_cast<const double*>(host_of(R[k].ess.p));
+    const double* cz = reinterpret_cast<const double*>(host_of(R[k].cz.p));
+    const double* lam = reinterpret_cast<const double*>(host_of(R[k].lam.p));
+    const double* b = reinterpret_cast<const double*>(host_of(betas[k].p));
+    const double* scal = reinterpret_cast<const double*>(host_of(R[k].scal.p));
+    const uint8_t* rs = reinterpret_cast<const uint8_t*>(host_of(R[k].rs.p));
     SmcState st;
-    std::memcpy(&st, H + o.st, sizeof st);
+    std::memcpy(&st, host_of(R[k].st.p), sizeof st);
     TRY(device_error(st.err, st.err_step, st.err_val));
     if (herr == ASMC_ERR_EVALUATION) return device_error(herr, 0, 0.0);
     if (herr) return fail(herr, "schedule generation after round %d failed validation", k + 1);
