@@ -102,8 +102,10 @@ int get_ctx(int device, DevCtx** out, uint64_t user_stream = 0) {
     CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     it = ctxs.emplace(device, c).first;
   }
-  static thread_local DevCtx user;  // the caller's stream; its own (persistent) staging
+  // the caller's stream: a per-device view with its own (persistent) staging and events
+  static thread_local std::map<int, DevCtx> users;
   if (user_stream) {
+    DevCtx& user = users[device];
     user.stream = reinterpret_cast<cudaStream_t>(user_stream);
     user.sms = it->second.sms;
     *out = &user;
